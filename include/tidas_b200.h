@@ -1,0 +1,180 @@
+/*
+ * tidas_b200 — C ABI of the B200-native DAS / tiDAS hot path.
+ *
+ * Plain C: device pointers, sizes, enums, a cudaStream_t passed as void*.
+ * Every entry point returns TIDAS_OK (0) or an error code; the message of the
+ * last failure on the calling thread is tidas_last_error(). Nothing here
+ * allocates device memory except the per-(device, N) Bluestein plan cache of
+ * tidas_rf_analytic for non-power-of-two traces; no entry point synchronises
+ * the stream.
+ *
+ * The reference (/root/reference/pkg/src/tidas) is a pure-Python package with
+ * no FFI layer; each entry point below replaces the inner numerical loop of the
+ * reference function cited beside it, and the Python package
+ * paper_2507_15464_b200 keeps the reference's signatures on top of it
+ * (INTEGRATION.md shows the ctypes binding).
+ */
+#ifndef TIDAS_B200_H
+#define TIDAS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TIDAS_OK 0
+#define TIDAS_EINVAL 1       /* bad argument (ValueError on the Python side) */
+#define TIDAS_ECUDA 2        /* CUDA launch / runtime failure */
+#define TIDAS_EUNSUPPORTED 3 /* shape outside what the kernels support */
+
+/* element types of RF / maps */
+enum tidas_dtype { TIDAS_F64 = 0, TIDAS_F32 = 1, TIDAS_I16 = 2 };
+/* arithmetic precision of a kernel instantiation */
+enum tidas_prec { TIDAS_PREC_F32 = 0, TIDAS_PREC_F64 = 1 };
+/* receive aperture / apodization */
+enum tidas_aperture {
+  TIDAS_AP_REF_BOXCAR = 0, /* array-centred boxcar, per-depth half count (geometry.py:188-199) */
+  TIDAS_AP_HANN = 1        /* pixel-centred Hann, half-width z / (2 F#) (north star) */
+};
+/* pixel value */
+enum tidas_out {
+  TIDAS_OUT_ENVELOPE = 0, /* (1-f)|C(k0)| + f|C(k0+1)| per transmit, summed (das.py:165-193) */
+  TIDAS_OUT_COHERENT = 1, /* |sum over transmits of (1-f) C(k0) + f C(k0+1)| */
+  TIDAS_OUT_IQ = 2        /* complex sum over transmits of (1-f) C(k0) + f C(k0+1) */
+};
+
+const char* tidas_last_error(void);
+int tidas_abi_version(void);
+
+/* One-time per-device setup (FFT twiddle tables). Idempotent, thread-safe. */
+int tidas_init(int device);
+
+/*
+ * K1 — RF ingest: dtype convert (f64/f32/i16, times `scale`) + periodic analytic
+ * signal of every row (scipy.signal.hilbert semantics, metrics.py:30-34).
+ *   rf      : n_rows rows, row r at rf + r * rf_row_stride elements, n_samples each
+ *   out     : n_rows x n_samples complex (float2 for PREC_F32, double2 for PREC_F64),
+ *             row-contiguous ("channel-contiguous")
+ *   support : optional (may be NULL) int32[n_rows][2] first / last nonzero sample
+ *             (-1, -1 for an all-zero row) — the head/tail-zero precondition of
+ *             the exact analytic gather
+ * Replaces: metrics.envelope's hilbert (metrics.py:34) hoisted from per pixel
+ * (das.py:172) to once per channel.
+ */
+int tidas_rf_analytic(const void* rf, int rf_dtype, int64_t rf_row_stride, double scale,
+                      void* out, int out_prec, int64_t n_rows, int32_t n_samples,
+                      int32_t* support, void* stream);
+
+/*
+ * Spectral fractional delay (das.py:108-111, method="spectral"): complex
+ * IFFT(FFT(x) * exp(-2 pi i f shift / fs)) per row, f on numpy's fftfreq grid;
+ * the caller keeps the real part. x: [n_rows][n_samples] double, out: double2.
+ */
+int tidas_spectral_shift_f64(const double* x, int64_t n_rows, int32_t n_samples, double shift,
+                             void* out, void* stream);
+
+/*
+ * Expected arrival t* (seconds) of steered plane waves at every pixel:
+ *   out[a][iz][ix] = (x sin a + z cos a + (n_el-1)/2 pitch |sin a|) / c + z / c
+ * (the focused-transmit table of the reference,
+ * das.py:135-137 / simulate.py:156-175, is computed by the host).
+ */
+int tidas_plane_wave_arrivals(const double* x, int32_t nx, const double* z, int32_t nz,
+                              const double* angles, int32_t n_angles, int32_t n_el,
+                              double pitch, double c, double* out, void* stream);
+
+/* K2 — fused DAS image over a rectilinear pixel grid. */
+typedef struct {
+  int32_t n_frames;   /* F */
+  int32_t n_angles;   /* A (transmits per frame) */
+  int32_t n_el;       /* channels per transmit (even) */
+  int32_t n_samples;  /* N */
+  int32_t nx, nz;     /* pixel grid */
+  double pitch;       /* element pitch [m]; x_n = (n + 0.5) pitch, n in [-n_el/2, n_el/2) */
+  double c;           /* sound speed [m/s] */
+  double fs;          /* sampling frequency [Hz] */
+  double t0;          /* time of sample 0 [s] */
+  int32_t aperture;   /* enum tidas_aperture */
+  double f_number;    /* Hann: half-width z / (2 f_number) */
+  int32_t out_mode;   /* enum tidas_out */
+  int32_t prec;       /* enum tidas_prec: analytic / out element precision */
+} tidas_das_desc_t;
+
+/*
+ *   analytic : [F][A][n_el][N] complex (from tidas_rf_analytic, same prec)
+ *   t_star   : [A][nz][nx] double, expected arrival per transmit and pixel
+ *   x, z     : pixel coordinates [m], double[nx], double[nz]
+ *   ap_half  : int32[nz] aperture half count for TIDAS_AP_REF_BOXCAR (else NULL)
+ *   out      : [F][nz][nx] real (complex for TIDAS_OUT_IQ) of `prec`
+ * Replaces: das_value / das_line (das.py:181-221) — O(channels) per pixel.
+ */
+int tidas_das_image(const tidas_das_desc_t* desc, const void* analytic,
+                    const double* t_star, const double* x, const double* z,
+                    const int32_t* ap_half, void* out, void* stream);
+
+/*
+ * K3 — delayed sum (das.py:140-149, float64, bit-identical to the reference):
+ *   out[p][k] = sum_{j in order} lerp-shift(traces[rows[p][j]], shift[p][j])[k]
+ * for n_profiles independent profiles of length n_taps (rows are absolute trace
+ * rows; shift = delay * fs in samples), with the reference's integer-shift rule
+ * and zero fill.  traces: [n_rows][N] double.  out: [n_profiles][N] double.
+ * If lo/hi (int32[n_profiles], may be NULL) are given only samples [lo, hi)
+ * are produced (the rest of the row is left untouched).
+ */
+int tidas_delayed_sum_f64(const double* traces, int32_t n_rows, int32_t n_samples,
+                          const int32_t* rows, const double* shifts, int32_t n_taps,
+                          int32_t n_profiles, const int32_t* lo, const int32_t* hi,
+                          double* out, void* stream);
+
+/*
+ * K4 — windowed envelope read (tidas.py:522-530 / das.py:174-178):
+ *   for pixel p: window [lo_p, hi_p) of trace[tr_p]; if hi-lo < 4 -> 0; else
+ *   theta_p * interp(|analytic_L(trace[lo:hi])|, pos_p - lo), left/right = 0,
+ * with the L-point periodic analytic signal (L <= 256).
+ */
+int tidas_window_envelope_f64(const double* traces, int32_t n_samples,
+                              const int32_t* trace_of, const int32_t* lo,
+                              const int32_t* hi, const double* pos,
+                              const double* theta, int32_t n_pixels, double* out,
+                              void* stream);
+
+/*
+ * Dot products over windows: out[p] = (sum a*b, sum a*a) over [lo_p, hi_p) of
+ * rows a = A[p], b = B[p] (estimate_theta_aligned, tidas.py:302-314).
+ */
+int tidas_window_dots_f64(const double* a, const double* b, int32_t n_samples,
+                          const int32_t* lo, const int32_t* hi, int32_t n_pairs,
+                          double* out, void* stream);
+
+/*
+ * K6 / K7 — tiDAS row convolution and its adjoint (north star (d)), float32:
+ *   fwd: y[b][i][x] = sum_k K[i][k] g[b][i][x + k - H]          (H = (T-1)/2)
+ *   adj: g[b][i][x] = sum_k K[i][k] y[b][i][x - k + H]
+ * zero outside [0, nx). maps [batch][nz][nx], K [nz][T], T odd, T <= 255.
+ */
+int tidas_rowconv_fwd_f32(const float* g, const float* K, float* y, int64_t batch,
+                          int32_t nz, int32_t nx, int32_t taps, void* stream);
+int tidas_rowconv_adj_f32(const float* y, const float* K, float* g, int64_t batch,
+                          int32_t nz, int32_t nx, int32_t taps, void* stream);
+
+/*
+ * RF synthesis (simulate.py:193-259 model), for seeded inputs:
+ *   out[f][a][e][k] += sum_s w_se pulse(k/fs - tau_se),
+ *   tau_se = t_tx[f][a][s] + hypot(x_s - x_e, z_s) / c,  w_se = amp_s (z_s / r_se if spreading)
+ * accumulated with atomics (order-dependent to the last ulp when scatterers
+ * overlap). Scatterers of frame f are sx/sz/amp[f * n_scat + s]; t_tx is the
+ * transmit arrival of each scatterer (focused: simulate.py:156-175; plane wave:
+ * tidas_plane_wave_arrivals minus z / c). out must be zeroed by the caller;
+ * out_dtype F32 or F64. Replaces: synthesize_frame's double loop (simulate.py:238-246).
+ */
+int tidas_synthesize(const double* sx, const double* sz, const double* amp, const double* t_tx,
+                     int32_t n_scat, int32_t n_frames, int32_t n_angles, int32_t n_el,
+                     double pitch, double c, double fs, double f0, double fbw,
+                     int32_t spreading, int32_t n_samples, void* out, int out_dtype,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIDAS_B200_H */

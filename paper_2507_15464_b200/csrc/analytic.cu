@@ -1,0 +1,344 @@
+// K1 — RF ingest + periodic analytic signal, one CTA per channel row.
+//
+// Reference: the envelope of every DAS pixel is the periodic Hilbert transform
+// (scipy.signal.hilbert, metrics.py:30-34) of that pixel's full delayed-sum
+// trace (das.py:165-178). Hilbert is linear and commutes with the circular
+// shifts the delayed sum applies when each channel's head is zero,
+// so it is hoisted to once per channel: load the row (f64 / f32 / int16, times
+// `scale`), FFT, multiply by scipy's one-sided mask h / N, inverse FFT, store
+// the complex row. Power-of-two rows run entirely in shared memory
+// (fft.cuh); other lengths use Bluestein's chirp-z on a power-of-two grid
+// (bluestein_* below), which keeps the exact length-N periodic semantics.
+#include <math.h>
+
+#include <mutex>
+#include <map>
+#include <tuple>
+
+#include "fft.cuh"
+
+namespace tidas {
+
+__global__ void init_twiddles_kernel() {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= TW_N) return;
+  double sn, cs;
+  // exp(-2 pi i k / TW_N); sincospi keeps the multiples of 1/4 exact
+  sincospi(-2.0 * (double)k / (double)TW_N, &sn, &cs);
+  g_tw64[k] = make_double2(cs, sn);
+  g_tw32[k] = make_float2((float)cs, (float)sn);
+}
+
+template <typename In> __device__ __forceinline__ double load_as_double(const In* p) {
+  return (double)(*p);
+}
+
+// Spectral operator applied between the forward and inverse transforms, already
+// divided by N: scipy.signal.hilbert's one-sided mask (shift is NaN), or the
+// delay phase ramp exp(-2 pi i f delay) of das.py:108-111 (shift = delay * fs,
+// f on numpy's fftfreq grid).
+template <typename R> __device__ __forceinline__ cplx<R> spectral_op(cplx<R> v, int k, int N, double shift);
+
+template <typename R> __device__ __forceinline__ R hilbert_mask(int k, int N) {
+  const R invN = R(1) / R(N);
+  if (k == 0) return invN;
+  if ((N & 1) == 0) {
+    if (k < N / 2) return R(2) * invN;
+    if (k == N / 2) return invN;
+    return R(0);
+  }
+  return k < (N + 1) / 2 ? R(2) * invN : R(0);
+}
+
+template <typename R> __device__ __forceinline__ cplx<R> spectral_op(cplx<R> v, int k, int N, double shift) {
+  if (isnan(shift)) return cscale(v, hilbert_mask<R>(k, N));
+  const int kk = (k < (N + 1) / 2) ? k : k - N;  // fftfreq order
+  double sn, cs;
+  sincospi(-2.0 * (double)kk * shift / (double)N, &sn, &cs);
+  cplx<R> w;
+  w.x = (R)(cs / N);
+  w.y = (R)(sn / N);
+  return cmul(v, w);
+}
+
+template <typename R, typename In>
+__global__ void __launch_bounds__(512) analytic_pow2_kernel(const In* __restrict__ rf,
+                                                             int64_t stride, R scale,
+                                                             cplx<R>* __restrict__ out,
+                                                             int logN,
+                                                             int32_t* __restrict__ support,
+                                                             double shift) {
+  using C = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  __shared__ int first_nz, last_nz;
+  const int N = 1 << logN;
+  const int64_t row = blockIdx.x;
+  const In* src = rf + row * stride;
+  if (threadIdx.x == 0) { first_nz = N; last_nz = -1; }
+  int lo = N, hi = -1;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    const R v = R(load_as_double(src + n)) * scale;
+    if (v != R(0)) { lo = min(lo, n); hi = max(hi, n); }
+    C c; c.x = v; c.y = R(0);
+    s[n] = c;
+  }
+  __syncthreads();
+  if (support) {
+    if (lo < N) atomicMin(&first_nz, lo);
+    if (hi >= 0) atomicMax(&last_nz, hi);
+  }
+  fft_inplace<R, false>(s, logN);
+  for (int k = threadIdx.x; k < N; k += blockDim.x) s[k] = spectral_op<R>(s[k], k, N, shift);
+  __syncthreads();
+  fft_inplace<R, true>(s, logN);
+  C* dst = out + row * (int64_t)N;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) dst[n] = s[n];
+  if (support && threadIdx.x == 0) {
+    const bool any = last_nz >= 0;
+    support[2 * row] = any ? first_nz : -1;
+    support[2 * row + 1] = any ? last_nz : -1;
+  }
+}
+
+// ----------------------------------------------------------- Bluestein path
+//
+// DFT_N(x)_k = conj(b_k) * sum_n (x_n conj(b_n)) b_{k-n},  b_j = exp(i pi j^2 / N)
+// evaluated as an M-point circular convolution (M = pow2 >= 2N - 1). The
+// chirp spectrum B = FFT_M(b~) is precomputed once per (device, N, precision).
+
+template <typename R> __device__ __forceinline__ cplx<R> chirp(int64_t j, int N, bool conj_) {
+  // exp(+- i pi j^2 / N) with j^2 reduced mod 2N exactly in integers
+  const int64_t q = (j * j) % (2 * (int64_t)N);
+  double sn, cs;
+  sincospi((double)q / (double)N, &sn, &cs);
+  cplx<R> r;
+  r.x = (R)cs;
+  r.y = conj_ ? (R)(-sn) : (R)sn;
+  return r;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(512) chirp_spectrum_kernel(int N, int logM, cplx<R>* B) {
+  using C = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  const int M = 1 << logM;
+  const bool conj_ = blockIdx.x == 1;  // row 0: b, row 1: conj(b)
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    C v = cmake<C>(0.0, 0.0);
+    if (j < N) v = chirp<R>(j, N, conj_);
+    else if (j > M - N) v = chirp<R>(M - j, N, conj_);
+    s[j] = v;
+  }
+  __syncthreads();
+  fft_inplace<R, false>(s, logM);
+  for (int j = threadIdx.x; j < M; j += blockDim.x) B[(int64_t)blockIdx.x * M + j] = s[j];
+}
+
+// s holds x (length N, zero beyond); on return s[0..N) = DFT_N(x) (fwd) or
+// N * IDFT_N(x) (inv, unnormalised), using chirp spectrum Bspec (b for fwd,
+// conj(b) for inv).
+template <typename R, bool INV>
+__device__ void bluestein_dft(cplx<R>* s, int N, int logM, const cplx<R>* __restrict__ Bspec) {
+  using C = cplx<R>;
+  const int M = 1 << logM;
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    C v = cmake<C>(0.0, 0.0);
+    if (j < N) v = cmul(s[j], chirp<R>(j, N, !INV));
+    s[j] = v;
+  }
+  __syncthreads();
+  fft_inplace<R, false>(s, logM);
+  const R invM = R(1) / R(M);
+  for (int j = threadIdx.x; j < M; j += blockDim.x) s[j] = cscale(cmul(s[j], Bspec[j]), invM);
+  __syncthreads();
+  fft_inplace<R, true>(s, logM);
+  for (int k = threadIdx.x; k < N; k += blockDim.x) s[k] = cmul(s[k], chirp<R>(k, N, !INV));
+  __syncthreads();
+}
+
+template <typename R, typename In>
+__global__ void __launch_bounds__(512) analytic_bluestein_kernel(
+    const In* __restrict__ rf, int64_t stride, R scale, cplx<R>* __restrict__ out, int N,
+    int logM, const cplx<R>* __restrict__ Bfwd, const cplx<R>* __restrict__ Binv,
+    int32_t* __restrict__ support, double shift) {
+  using C = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  __shared__ int first_nz, last_nz;
+  const int M = 1 << logM;
+  const int64_t row = blockIdx.x;
+  const In* src = rf + row * stride;
+  if (threadIdx.x == 0) { first_nz = N; last_nz = -1; }
+  int lo = N, hi = -1;
+  for (int n = threadIdx.x; n < M; n += blockDim.x) {
+    R v = R(0);
+    if (n < N) {
+      v = R(load_as_double(src + n)) * scale;
+      if (v != R(0)) { lo = min(lo, n); hi = max(hi, n); }
+    }
+    C c; c.x = v; c.y = R(0);
+    s[n] = c;
+  }
+  __syncthreads();
+  if (support) {
+    if (lo < N) atomicMin(&first_nz, lo);
+    if (hi >= 0) atomicMax(&last_nz, hi);
+  }
+  bluestein_dft<R, false>(s, N, logM, Bfwd);
+  for (int k = threadIdx.x; k < M; k += blockDim.x)
+    s[k] = k < N ? spectral_op<R>(s[k], k, N, shift) : cmake<C>(0.0, 0.0);
+  __syncthreads();
+  bluestein_dft<R, true>(s, N, logM, Binv);
+  C* dst = out + row * (int64_t)N;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) dst[n] = s[n];
+  if (support && threadIdx.x == 0) {
+    const bool any = last_nz >= 0;
+    support[2 * row] = any ? first_nz : -1;
+    support[2 * row + 1] = any ? last_nz : -1;
+  }
+}
+
+// ------------------------------------------------------------------ host
+
+static std::mutex g_mu;
+static std::map<int, bool> g_init_done;
+static std::map<std::tuple<int, int, int>, void*> g_chirp_cache;  // (dev, N, prec) -> B
+
+int ensure_init(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_init_done.count(device)) return TIDAS_OK;
+  int prev = 0;
+  TIDAS_CUDA_CHECK(cudaGetDevice(&prev));
+  TIDAS_CUDA_CHECK(cudaSetDevice(device));
+  init_twiddles_kernel<<<TW_N / 256, 256>>>();
+  TIDAS_LAUNCH_CHECK();
+  TIDAS_CUDA_CHECK(cudaDeviceSynchronize());
+  TIDAS_CUDA_CHECK(cudaSetDevice(prev));
+  g_init_done[device] = true;
+  return TIDAS_OK;
+}
+
+static int ilog2_exact(int64_t n) {
+  if (n <= 0 || (n & (n - 1))) return -1;
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return l;
+}
+
+template <typename R> static int threads_for(int logN) {
+  return (1 << logN) / FFT_EPT;
+}
+
+template <typename R>
+static int get_chirp_spectra(int device, int N, int logM, const cplx<R>** out) {
+  using C = cplx<R>;
+  std::lock_guard<std::mutex> lk(g_mu);
+  const auto key = std::make_tuple(device, N, (int)sizeof(R));
+  auto it = g_chirp_cache.find(key);
+  if (it != g_chirp_cache.end()) { *out = reinterpret_cast<const C*>(it->second); return TIDAS_OK; }
+  const int M = 1 << logM;
+  void* B = nullptr;
+  TIDAS_CUDA_CHECK(cudaMalloc(&B, sizeof(C) * 2 * (size_t)M));
+  const size_t smem = sizeof(C) * (size_t)M;
+  auto kern = chirp_spectrum_kernel<R>;
+  TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<2, threads_for<R>(logM), smem>>>(N, logM, reinterpret_cast<C*>(B));
+  TIDAS_LAUNCH_CHECK();
+  TIDAS_CUDA_CHECK(cudaDeviceSynchronize());
+  g_chirp_cache[key] = B;
+  *out = reinterpret_cast<const C*>(B);
+  return TIDAS_OK;
+}
+
+template <typename R, typename In>
+static int launch_analytic(const In* rf, int64_t stride, double scale, void* out, int64_t n_rows,
+                           int32_t N, int32_t* support, double shift, cudaStream_t st) {
+  using C = cplx<R>;
+  int dev = 0;
+  TIDAS_CUDA_CHECK(cudaGetDevice(&dev));
+  int rc = ensure_init(dev);
+  if (rc) return rc;
+  const int logN = ilog2_exact(N);
+  if (logN >= 0) {
+    TIDAS_REQUIRE(logN >= 4 && logN <= FFT_MAX_LOG, "power-of-two n_samples must be in [16, %d]",
+                  1 << FFT_MAX_LOG);
+    const size_t smem = sizeof(C) * (size_t)N;
+    TIDAS_REQUIRE(smem <= 227 * 1024, "n_samples=%d too long for the on-chip FFT at this precision", N);
+    auto kern = analytic_pow2_kernel<R, In>;
+    TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)n_rows, threads_for<R>(logN), smem, st>>>(rf, stride, (R)scale,
+                                                                reinterpret_cast<C*>(out), logN, support, shift);
+    TIDAS_LAUNCH_CHECK();
+    return TIDAS_OK;
+  }
+  int logM = 0;
+  while ((1 << logM) < 2 * N - 1) ++logM;
+  logM = logM < 4 ? 4 : logM;
+  const size_t smem = sizeof(C) * ((size_t)1 << logM);
+  TIDAS_REQUIRE(logM <= FFT_MAX_LOG && smem <= 227 * 1024,
+                "non-power-of-two n_samples=%d needs a %d-point Bluestein grid: too long", N,
+                1 << logM);
+  const C* B = nullptr;
+  rc = get_chirp_spectra<R>(dev, N, logM, &B);
+  if (rc) return rc;
+  auto kern = analytic_bluestein_kernel<R, In>;
+  TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)n_rows, threads_for<R>(logM), smem, st>>>(
+      rf, stride, (R)scale, reinterpret_cast<C*>(out), N, logM, B, B + ((size_t)1 << logM), support,
+      shift);
+  TIDAS_LAUNCH_CHECK();
+  return TIDAS_OK;
+}
+
+template <typename R>
+static int dispatch_analytic(const void* rf, int dtype, int64_t stride, double scale, void* out,
+                             int64_t n_rows, int32_t N, int32_t* support, double shift,
+                             cudaStream_t st) {
+  switch (dtype) {
+    case TIDAS_F64:
+      return launch_analytic<R>(static_cast<const double*>(rf), stride, scale, out, n_rows, N, support, shift, st);
+    case TIDAS_F32:
+      return launch_analytic<R>(static_cast<const float*>(rf), stride, scale, out, n_rows, N, support, shift, st);
+    case TIDAS_I16:
+      return launch_analytic<R>(static_cast<const int16_t*>(rf), stride, scale, out, n_rows, N, support, shift, st);
+  }
+  set_error("unknown rf dtype %d", dtype);
+  return TIDAS_EINVAL;
+}
+
+}  // namespace tidas
+
+extern "C" int tidas_init(int device) { return tidas::ensure_init(device); }
+
+extern "C" int tidas_rf_analytic(const void* rf, int rf_dtype, int64_t rf_row_stride, double scale,
+                                 void* out, int out_prec, int64_t n_rows, int32_t n_samples,
+                                 int32_t* support, void* stream) {
+  using namespace tidas;
+  TIDAS_REQUIRE(rf && out, "null pointer");
+  TIDAS_REQUIRE(n_rows >= 0 && n_rows < (int64_t(1) << 31), "n_rows out of range");
+  TIDAS_REQUIRE(n_samples >= 4, "envelope needs at least 4 samples");
+  TIDAS_REQUIRE(rf_row_stride >= n_samples, "row stride shorter than the row");
+  if (n_rows == 0) return TIDAS_OK;
+  const double hilbert = nan("");
+  if (out_prec == TIDAS_PREC_F32)
+    return dispatch_analytic<float>(rf, rf_dtype, rf_row_stride, scale, out, n_rows, n_samples, support, hilbert, as_stream(stream));
+  if (out_prec == TIDAS_PREC_F64)
+    return dispatch_analytic<double>(rf, rf_dtype, rf_row_stride, scale, out, n_rows, n_samples, support, hilbert, as_stream(stream));
+  set_error("unknown precision %d", out_prec);
+  return TIDAS_EINVAL;
+}
+
+extern "C" int tidas_spectral_shift_f64(const double* x, int64_t n_rows, int32_t n_samples,
+                                        double shift, void* out, void* stream) {
+  using namespace tidas;
+  TIDAS_REQUIRE(x && out, "null pointer");
+  TIDAS_REQUIRE(n_samples >= 1 && !isnan(shift), "bad arguments");
+  if (n_rows == 0) return TIDAS_OK;
+  if (n_samples < 16) {
+    set_error("spectral delay needs at least 16 samples on the device path");
+    return TIDAS_EUNSUPPORTED;
+  }
+  return launch_analytic<double>(x, n_samples, 1.0, out, n_rows, n_samples, nullptr, shift, as_stream(stream));
+}

@@ -1,0 +1,441 @@
+// K2 — fused DAS image: time of flight on the fly, two-stage linear
+// interpolation, apodization, channel sum, envelope — one pass over the
+// analytic RF per frame.
+//
+// Reference pixel (das.py:181-193): envelope of the dynamic-focus delayed sum
+// (das.py:140-162, linear two-tap shift with the integer rule das.py:89-107)
+// sampled at t* by np.interp (das.py:165-178). With the per-channel analytic
+// signal A_n (analytic.cu) this is, exactly:
+//   pos = (t* - t0) fs, k0 = floor(pos), f = pos - k0   (0 outside [0, N-1])
+//   s_n = D_n fs, m_n = floor(s_n), mu_n = s_n - m_n
+//   C(k) = sum_n w_n [(1-mu_n) A_n[k - m_n] + mu_n A_n[k - m_n - 1]]   (mod N)
+//   value = (1-f) |C(k0)| + f |C(k0+1)|
+// so each (pixel, channel) reads three consecutive complex samples.
+//
+// Layout / schedule (B200):
+//   * CTA = 32 depths (lanes) x 8 columns (warps); each thread owns one pixel
+//     for FB frames, so the time-of-flight math (FP32, cancellation-free
+//     s = -dx^2 / (sqrt(dx^2 + z^2) + z) in sample units) is paid once per
+//     (pixel, channel) and reused for FB frames.
+//   * Per channel the CTA's sample window (min..max tap over its 256 pixels,
+//     ~130-200 samples) is copied global->shared with cp.async, double-buffered
+//     one channel ahead, so the 3 taps per pixel are shared-memory reads and the
+//     8 columns reuse one window (lateral reuse of the same channel row).
+//   * t* (one per pixel and transmit) is precomputed in float64 (plane-wave
+//     table kernel or the host's focused-transmit table) and split into an
+//     integer sample index plus an FP32 fraction — the FP32 ulp at index 8192
+//     would otherwise cost 1e-5 relative error.
+#include <math.h>
+#include <climits>
+
+#include "common.cuh"
+
+namespace tidas {
+
+constexpr int DAS_TZ = 32;   // depths per CTA (lanes)
+constexpr int DAS_TX = 8;    // columns per CTA (warps)
+constexpr int DAS_NT = DAS_TZ * DAS_TX;
+constexpr int DAS_WMAX = 448;  // staged window capacity (samples) per frame
+
+__host__ __device__ constexpr int win_pad(int p) { return p + (p >> 4); }
+constexpr int DAS_WSTRIDE = win_pad(DAS_WMAX) + 2;  // padded per-frame window stride
+
+struct DasParams {
+  int F, A, E, N, nx, nz;
+  double pitch, c, fs, t0, f_number;
+  const int32_t* ap_half;
+  const double* t_star;
+  const double* xg;
+  const double* zg;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <typename R> __device__ __forceinline__ void cp_async_elem(cplx<R>* s, const cplx<R>* g);
+template <> __device__ __forceinline__ void cp_async_elem<float>(float2* s, const float2* g) { cp_async8(s, g); }
+template <> __device__ __forceinline__ void cp_async_elem<double>(double2* s, const double2* g) { cp_async16(s, g); }
+
+// Per-(pixel, channel) interpolation parameters: tap index j (C(k0) reads j, j-1;
+// C(k0+1) reads j+1, j) and the weights w (1 - mu), w mu.
+template <typename R> struct Tap {
+  int j;
+  R w0, w1;
+};
+
+// Pixel geometry in the units each precision computes in.
+template <typename R> struct PixelGeo;
+
+template <> struct PixelGeo<float> {
+  // sample units (metres * fs / c)
+  float z, z2, a, pia, dxref, pitch;
+  int nref;
+  __device__ void init(const DasParams& p, double x, double z_m) {
+    const double k = p.fs / p.c;
+    z = (float)(z_m * k);
+    z2 = z * z;
+    a = (float)(z_m / (2.0 * p.f_number) * k);
+    pia = 3.14159265358979f / a;
+    pitch = (float)(p.pitch * k);
+    const int half = p.E / 2;
+    int nr = (int)rint(x / p.pitch - 0.5);
+    nr = max(-half, min(half - 1, nr));
+    nref = nr;
+    dxref = (float)((((double)nr + 0.5) * p.pitch - x) * k);
+  }
+  template <int AP>
+  __device__ __forceinline__ void tap(const DasParams&, int n, int k0, bool in_ap, Tap<float>& t) const {
+    const float dx = fmaf((float)(n - nref), pitch, dxref);  // x_n - x
+    const float q = dx * dx;
+    const float rr = q + z2;
+    const float r = rr * rsqrtf(rr);
+    const float s = -__fdividef(q, r + z);  // D_n fs, cancellation-free
+    const float m = floorf(s);
+    const float mu = s - m;
+    float w;
+    if (AP == TIDAS_AP_HANN) {
+      w = (fabsf(dx) < a) ? fmaf(0.5f, __cosf(dx * pia), 0.5f) : 0.0f;
+    } else {
+      w = 1.0f;
+    }
+    w = in_ap ? w : 0.0f;
+    t.j = k0 - (int)m;
+    t.w1 = w * mu;
+    t.w0 = w - t.w1;
+  }
+};
+
+template <> struct PixelGeo<double> {
+  // metres / seconds, exactly the reference expressions (das.py:126-132, 82-97)
+  double x, z, a;
+  __device__ void init(const DasParams& p, double x_m, double z_m) {
+    x = x_m;
+    z = z_m;
+    a = z_m / (2.0 * p.f_number);
+  }
+  template <int AP>
+  __device__ __forceinline__ void tap(const DasParams& p, int n, int k0, bool in_ap, Tap<double>& t) const {
+    const double xn = ((double)n + 0.5) * p.pitch;
+    const double delay = __ddiv_rn(__dsub_rn(z, hypot(x - xn, z)), p.c);
+    const double s = __dmul_rn(delay, p.fs);
+    const double nearest = rint(s);
+    double m, mu;
+    if (fabs(s - nearest) < 1e-9) { m = nearest; mu = 0.0; }
+    else { m = floor(s); mu = s - m; }
+    double w;
+    if (AP == TIDAS_AP_HANN) {
+      const double d = xn - x;
+      w = (fabs(d) < a) ? 0.5 * (1.0 + cos(M_PI * d / a)) : 0.0;
+    } else {
+      w = 1.0;
+    }
+    w = in_ap ? w : 0.0;
+    t.j = k0 - (int)m;
+    t.w0 = w * (1.0 - mu);
+    t.w1 = w * mu;
+  }
+};
+
+__device__ __forceinline__ int wrapN(int e, int N) { return e < 0 ? e + N : (e >= N ? e - N : e); }
+
+template <typename R, int AP, int OUT, int FB>
+__global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
+                                                           const cplx<R>* __restrict__ A,
+                                                           void* __restrict__ out_) {
+  using C = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* win = reinterpret_cast<C*>(smem_raw);                 // [2][FB][DAS_WSTRIDE]
+  __shared__ int2 wwin[2][DAS_TX];                         // per-warp tap range per slot
+  __shared__ int ch_lo_s, ch_hi_s;
+
+  const int lane = threadIdx.x, wid = threadIdx.y;
+  const int tid = wid * DAS_TZ + lane;
+  const int iz = blockIdx.x * DAS_TZ + lane;
+  const int ix = blockIdx.y * DAS_TX + wid;
+  const int f0 = blockIdx.z * FB;
+  const bool pix = (iz < p.nz) && (ix < p.nx);
+  const int half = p.E / 2;
+
+  const double x = pix ? p.xg[ix] : 0.0;
+  const double zm = pix ? p.zg[iz] : 1.0;
+  PixelGeo<R> geo;
+  geo.init(p, x, zm);
+
+  // receive aperture (channel range) of this pixel
+  int n_lo = half, n_hi = -half - 1;
+  if (pix) {
+    if (AP == TIDAS_AP_HANN) {
+      const double a = zm / (2.0 * p.f_number);
+      n_lo = (int)floor((x - a) / p.pitch - 0.5);       // one extra each side: the
+      n_hi = (int)ceil((x + a) / p.pitch - 0.5);        // predicate |dx| < a decides
+    } else {
+      const int h = p.ap_half[iz];
+      n_lo = -h;
+      n_hi = h - 1;
+    }
+    n_lo = max(n_lo, -half);
+    n_hi = min(n_hi, half - 1);
+  }
+  if (tid == 0) { ch_lo_s = INT_MAX; ch_hi_s = INT_MIN; }
+  __syncthreads();
+  {
+    const int wl = __reduce_min_sync(0xffffffffu, n_lo);
+    const int wh = __reduce_max_sync(0xffffffffu, n_hi);
+    if (lane == 0) { atomicMin(&ch_lo_s, wl); atomicMax(&ch_hi_s, wh); }
+  }
+  __syncthreads();
+  const int c_lo = ch_lo_s, c_hi = ch_hi_s;
+  int ap_h = 0;
+  if (AP == TIDAS_AP_REF_BOXCAR && pix) ap_h = p.ap_half[iz];
+
+  R acc_env[FB];
+  C acc_iq[FB];
+#pragma unroll
+  for (int b = 0; b < FB; ++b) { acc_env[b] = R(0); acc_iq[b].x = R(0); acc_iq[b].y = R(0); }
+
+  const int64_t rowN = p.N;
+  for (int a = 0; a < p.A; ++a) {
+    // arrival split into integer index + fraction in float64
+    int k0 = 0;
+    R fr = R(0);
+    bool vpos = false;
+    if (pix) {
+      const double pos = (p.t_star[((int64_t)a * p.nz + iz) * p.nx + ix] - p.t0) * p.fs;
+      vpos = (pos >= 0.0) && (pos <= (double)(p.N - 1));
+      if (vpos) {
+        const double fl = floor(pos);
+        k0 = (int)fl;
+        fr = (R)(pos - fl);
+      }
+    }
+    const bool active_px = pix && vpos;
+    if (c_lo > c_hi) continue;
+
+    C c0[FB], c1[FB];
+#pragma unroll
+    for (int b = 0; b < FB; ++b) { c0[b].x = c0[b].y = R(0); c1[b].x = c1[b].y = R(0); }
+
+    // --- stage helper: compute taps of channel n, publish the warp's range
+    auto compute_tap = [&](int n, int slot, Tap<R>& t) {
+      bool in_ap = active_px && n >= n_lo && n <= n_hi;
+      if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
+      geo.template tap<AP>(p, n, k0, in_ap, t);
+      const bool live = in_ap && (t.w0 != R(0) || t.w1 != R(0));
+      const int lo = __reduce_min_sync(0xffffffffu, live ? t.j - 1 : INT_MAX);
+      const int hi = __reduce_max_sync(0xffffffffu, live ? t.j + 1 : INT_MIN);
+      if (lane == 0) wwin[slot][wid] = make_int2(lo, hi);
+      if (!live) { t.w0 = R(0); t.w1 = R(0); }
+    };
+    // --- after a barrier: CTA window of a slot
+    auto window_of = [&](int slot, int& lo, int& hi) {
+      lo = INT_MAX; hi = INT_MIN;
+#pragma unroll
+      for (int w = 0; w < DAS_TX; ++w) { lo = min(lo, wwin[slot][w].x); hi = max(hi, wwin[slot][w].y); }
+    };
+    // --- issue the copies of channel n's window into buffer `slot`
+    auto issue = [&](int n, int slot, int lo, int hi) {
+      const int W = hi - lo + 1;
+      if (W <= 0 || W > DAS_WMAX) return;
+      C* dst = win + (size_t)slot * FB * DAS_WSTRIDE;
+      for (int i = tid; i < W * FB; i += DAS_NT) {
+        const int b = i / W, e = i - b * W;
+        const int fb = min(f0 + b, p.F - 1);
+        const C* src = A + (((int64_t)fb * p.A + a) * p.E + (n + half)) * rowN;
+        cp_async_elem<R>(dst + b * DAS_WSTRIDE + win_pad(e), src + wrapN(lo + e, p.N));
+      }
+    };
+
+    Tap<R> cur, nxt;
+    int slot = 0;
+    compute_tap(c_lo, 0, cur);
+    __syncthreads();
+    int cur_lo, cur_hi;
+    window_of(0, cur_lo, cur_hi);
+    issue(c_lo, 0, cur_lo, cur_hi);
+    cp_async_commit();
+
+    for (int n = c_lo; n <= c_hi; ++n) {
+      const bool has_next = n < c_hi;
+      if (has_next) compute_tap(n + 1, slot ^ 1, nxt);
+      __syncthreads();  // (A) next window published; previous gather done
+      int nx_lo = 0, nx_hi = -1;
+      if (has_next) {
+        window_of(slot ^ 1, nx_lo, nx_hi);
+        issue(n + 1, slot ^ 1, nx_lo, nx_hi);
+      }
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();  // (B) current window resident
+      const int W = cur_hi - cur_lo + 1;
+      if (W > 0) {
+        if (W <= DAS_WMAX) {
+          const C* wb = win + (size_t)slot * FB * DAS_WSTRIDE;
+          const int e = cur.j - cur_lo;  // position of tap j-1 is e-1
+#pragma unroll
+          for (int b = 0; b < FB; ++b) {
+            if (cur.w0 == R(0) && cur.w1 == R(0)) break;
+            const C am1 = wb[b * DAS_WSTRIDE + win_pad(e - 1)];
+            const C a0 = wb[b * DAS_WSTRIDE + win_pad(e)];
+            const C ap1 = wb[b * DAS_WSTRIDE + win_pad(e + 1)];
+            c0[b].x += cur.w0 * a0.x + cur.w1 * am1.x;
+            c0[b].y += cur.w0 * a0.y + cur.w1 * am1.y;
+            c1[b].x += cur.w0 * ap1.x + cur.w1 * a0.x;
+            c1[b].y += cur.w0 * ap1.y + cur.w1 * a0.y;
+          }
+        } else if (cur.w0 != R(0) || cur.w1 != R(0)) {
+          // oversized window (steep geometry): gather straight from global
+#pragma unroll
+          for (int b = 0; b < FB; ++b) {
+            const int fb = min(f0 + b, p.F - 1);
+            const C* src = A + (((int64_t)fb * p.A + a) * p.E + (n + half)) * rowN;
+            const C am1 = src[wrapN(cur.j - 1, p.N)];
+            const C a0 = src[wrapN(cur.j, p.N)];
+            const C ap1 = src[wrapN(cur.j + 1, p.N)];
+            c0[b].x += cur.w0 * a0.x + cur.w1 * am1.x;
+            c0[b].y += cur.w0 * a0.y + cur.w1 * am1.y;
+            c1[b].x += cur.w0 * ap1.x + cur.w1 * a0.x;
+            c1[b].y += cur.w0 * ap1.y + cur.w1 * a0.y;
+          }
+        }
+      }
+      cur = nxt;
+      cur_lo = nx_lo;
+      cur_hi = nx_hi;
+      slot ^= 1;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+
+    if (active_px) {
+      const R g = R(1) - fr;
+#pragma unroll
+      for (int b = 0; b < FB; ++b) {
+        if (OUT == TIDAS_OUT_ENVELOPE) {
+          // np.interp: fp[j] + (fp[j+1] - fp[j]) * f, exact fp[j] at f == 0
+          const R e0 = cabs_(c0[b]);
+          acc_env[b] += (fr == R(0)) ? e0 : e0 + (cabs_(c1[b]) - e0) * fr;
+        } else {
+          acc_iq[b].x += g * c0[b].x + fr * c1[b].x;
+          acc_iq[b].y += g * c0[b].y + fr * c1[b].y;
+        }
+      }
+    }
+  }
+
+  if (!pix) return;
+#pragma unroll
+  for (int b = 0; b < FB; ++b) {
+    const int f = f0 + b;
+    if (f >= p.F) break;
+    const int64_t o = ((int64_t)f * p.nz + iz) * p.nx + ix;
+    if (OUT == TIDAS_OUT_ENVELOPE) reinterpret_cast<R*>(out_)[o] = acc_env[b];
+    else if (OUT == TIDAS_OUT_COHERENT) reinterpret_cast<R*>(out_)[o] = cabs_(acc_iq[b]);
+    else reinterpret_cast<C*>(out_)[o] = acc_iq[b];
+  }
+}
+
+__global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double* z, int nz,
+                                           const double* angles, int na, int n_el, double pitch,
+                                           double c, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)na * nz * nx;
+  if (i >= total) return;
+  const int ix = (int)(i % nx);
+  const int iz = (int)((i / nx) % nz);
+  const int a = (int)(i / ((int64_t)nx * nz));
+  double sn, cs;
+  sincos(angles[a], &sn, &cs);
+  const double origin = 0.5 * (double)(n_el - 1) * pitch * fabs(sn);
+  out[i] = (x[ix] * sn + z[iz] * cs + origin) / c + z[iz] / c;
+}
+
+template <typename R, int AP, int OUT, int FB>
+static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
+  using C = cplx<R>;
+  auto kern = das_image_kernel<R, AP, OUT, FB>;
+  const size_t smem = sizeof(C) * 2 * FB * DAS_WSTRIDE;
+  TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 block(DAS_TZ, DAS_TX);
+  dim3 grid((p.nz + DAS_TZ - 1) / DAS_TZ, (p.nx + DAS_TX - 1) / DAS_TX, (p.F + FB - 1) / FB);
+  TIDAS_REQUIRE(grid.y <= 65535 && grid.z <= 65535, "pixel grid / frame batch too large");
+  kern<<<grid, block, smem, st>>>(p, reinterpret_cast<const C*>(A), out);
+  TIDAS_LAUNCH_CHECK();
+  return TIDAS_OK;
+}
+
+template <typename R, int AP, int OUT>
+static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
+  if (sizeof(R) == 8) return launch_das<R, AP, OUT, 1>(p, A, out, st);
+  if (p.F >= 4) return launch_das<R, AP, OUT, 4>(p, A, out, st);
+  if (p.F >= 2) return launch_das<R, AP, OUT, 2>(p, A, out, st);
+  return launch_das<R, AP, OUT, 1>(p, A, out, st);
+}
+
+template <typename R, int AP>
+static int dispatch_out(int out_mode, const DasParams& p, const void* A, void* out, cudaStream_t st) {
+  switch (out_mode) {
+    case TIDAS_OUT_ENVELOPE: return dispatch_fb<R, AP, TIDAS_OUT_ENVELOPE>(p, A, out, st);
+    case TIDAS_OUT_COHERENT: return dispatch_fb<R, AP, TIDAS_OUT_COHERENT>(p, A, out, st);
+    case TIDAS_OUT_IQ: return dispatch_fb<R, AP, TIDAS_OUT_IQ>(p, A, out, st);
+  }
+  set_error("unknown out_mode %d", out_mode);
+  return TIDAS_EINVAL;
+}
+
+template <typename R>
+static int dispatch_ap(const tidas_das_desc_t* d, const DasParams& p, const void* A, void* out, cudaStream_t st) {
+  if (d->aperture == TIDAS_AP_HANN) return dispatch_out<R, TIDAS_AP_HANN>(d->out_mode, p, A, out, st);
+  if (d->aperture == TIDAS_AP_REF_BOXCAR) return dispatch_out<R, TIDAS_AP_REF_BOXCAR>(d->out_mode, p, A, out, st);
+  set_error("unknown aperture %d", d->aperture);
+  return TIDAS_EINVAL;
+}
+
+}  // namespace tidas
+
+extern "C" int tidas_das_image(const tidas_das_desc_t* d, const void* analytic, const double* t_star,
+                               const double* x, const double* z, const int32_t* ap_half, void* out,
+                               void* stream) {
+  using namespace tidas;
+  TIDAS_REQUIRE(d && analytic && t_star && x && z && out, "null pointer");
+  TIDAS_REQUIRE(d->n_el >= 2 && d->n_el % 2 == 0, "n_el must be even and >= 2");
+  TIDAS_REQUIRE(d->n_samples >= 4, "n_samples must be >= 4");
+  TIDAS_REQUIRE(d->n_frames >= 0 && d->n_angles >= 1 && d->nx >= 0 && d->nz >= 0, "bad sizes");
+  TIDAS_REQUIRE(d->fs > 0 && d->c > 0 && d->pitch > 0, "fs, c, pitch must be positive");
+  TIDAS_REQUIRE(d->aperture != TIDAS_AP_REF_BOXCAR || ap_half, "REF_BOXCAR needs ap_half");
+  TIDAS_REQUIRE(d->aperture != TIDAS_AP_HANN || d->f_number > 0, "f_number must be positive");
+  if (d->n_frames == 0 || d->nx == 0 || d->nz == 0) return TIDAS_OK;
+  DasParams p;
+  p.F = d->n_frames; p.A = d->n_angles; p.E = d->n_el; p.N = d->n_samples;
+  p.nx = d->nx; p.nz = d->nz;
+  p.pitch = d->pitch; p.c = d->c; p.fs = d->fs; p.t0 = d->t0; p.f_number = d->f_number;
+  p.ap_half = ap_half; p.t_star = t_star; p.xg = x; p.zg = z;
+  cudaStream_t st = as_stream(stream);
+  if (d->prec == TIDAS_PREC_F32) return dispatch_ap<float>(d, p, analytic, out, st);
+  if (d->prec == TIDAS_PREC_F64) return dispatch_ap<double>(d, p, analytic, out, st);
+  set_error("unknown precision %d", d->prec);
+  return TIDAS_EINVAL;
+}
+
+extern "C" int tidas_plane_wave_arrivals(const double* x, int32_t nx, const double* z, int32_t nz,
+                                         const double* angles, int32_t n_angles, int32_t n_el,
+                                         double pitch, double c, double* out, void* stream) {
+  using namespace tidas;
+  TIDAS_REQUIRE(x && z && angles && out, "null pointer");
+  TIDAS_REQUIRE(nx >= 0 && nz >= 0 && n_angles >= 0, "bad sizes");
+  const int64_t total = (int64_t)n_angles * nz * nx;
+  if (total == 0) return TIDAS_OK;
+  plane_wave_arrivals_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(
+      x, nx, z, nz, angles, n_angles, n_el, pitch, c, out);
+  TIDAS_LAUNCH_CHECK();
+  return TIDAS_OK;
+}

@@ -1,0 +1,215 @@
+"""Tensor-native DAS imaging on the B200 (north star (a) + (b)).
+
+``DasPlan`` holds the frame-invariant geometry on the device (pixel grid,
+per-transmit arrival table t*, aperture), ``das_image`` runs K1 (RF ingest +
+analytic signal) and K2 (fused DAS) over a batch of frames. Frames are
+processed in chunks whose complex analytic RF stays resident in the 126 MB L2
+between the two kernels.
+
+Semantics: the pixel value is the reference's das_value
+(das.py:181-193) — envelope of the dynamic-focus delayed sum at t*, two-tap
+linear interpolation — generalised to steered plane waves, a pixel-centred Hann
+F# aperture and coherent / incoherent compounding.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_COMPLEX = {_lib.PREC_F32: torch.complex64, _lib.PREC_F64: torch.complex128}
+_REAL = {_lib.PREC_F32: torch.float32, _lib.PREC_F64: torch.float64}
+OUT_MODES = {"envelope": _lib.OUT_ENVELOPE, "coherent": _lib.OUT_COHERENT, "iq": _lib.OUT_IQ}
+
+
+@dataclass
+class DasPlan:
+    """Device-resident geometry of one imaging setup.
+
+    n_el, pitch [m], fs [Hz], c [m/s], n_samples: acquisition;
+    x [nx], z [nz]: pixel grid [m]; t_star [A][nz][nx]: expected arrival per
+    transmit (float64, seconds); aperture: ("hann", f_number) or
+    ("ref", ap_half[nz]); out: "envelope" | "coherent" | "iq"; prec: "f32" | "f64".
+    """
+
+    n_el: int
+    pitch: float
+    fs: float
+    c: float
+    n_samples: int
+    x: torch.Tensor
+    z: torch.Tensor
+    t_star: torch.Tensor
+    aperture: tuple
+    out: str = "envelope"
+    prec: str = "f32"
+    t0: float = 0.0
+    ap_half: Optional[torch.Tensor] = None
+    chunk_bytes: int = 32 << 20
+    _desc: Optional[_lib.DasDesc] = field(default=None, repr=False)
+
+    @property
+    def n_angles(self) -> int:
+        return int(self.t_star.shape[0])
+
+    @property
+    def nx(self) -> int:
+        return int(self.x.shape[0])
+
+    @property
+    def nz(self) -> int:
+        return int(self.z.shape[0])
+
+    @property
+    def prec_code(self) -> int:
+        return _lib.PREC_F32 if self.prec == "f32" else _lib.PREC_F64
+
+    def desc(self, n_frames: int) -> _lib.DasDesc:
+        d = _lib.DasDesc()
+        d.n_frames = n_frames
+        d.n_angles = self.n_angles
+        d.n_el = self.n_el
+        d.n_samples = self.n_samples
+        d.nx, d.nz = self.nx, self.nz
+        d.pitch, d.c, d.fs, d.t0 = self.pitch, self.c, self.fs, self.t0
+        if self.aperture[0] == "hann":
+            d.aperture, d.f_number = _lib.AP_HANN, float(self.aperture[1])
+        else:
+            d.aperture, d.f_number = _lib.AP_REF_BOXCAR, 1.0
+        d.out_mode = OUT_MODES[self.out]
+        d.prec = self.prec_code
+        return d
+
+
+def _dev(a, dtype, device) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
+
+
+def plane_wave_plan(*, n_el: int, pitch: float, fs: float, c: float, n_samples: int,
+                    x: Sequence[float], z: Sequence[float], angles: Sequence[float] = (0.0,),
+                    f_number: float = 1.5, out: str = "envelope", prec: str = "f32",
+                    device=None) -> DasPlan:
+    """Plan for steered plane-wave transmits and the pixel-centred Hann F# aperture.
+
+    The arrival table t*[a][iz][ix] is built on the device in float64
+    (tidas_plane_wave_arrivals)."""
+    L = _lib.lib()
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    xd = _dev(x, torch.float64, device)
+    zd = _dev(z, torch.float64, device)
+    ad = _dev(np.atleast_1d(angles), torch.float64, device)
+    ts = torch.empty((ad.numel(), zd.numel(), xd.numel()), dtype=torch.float64, device=device)
+    _lib.check(L.tidas_plane_wave_arrivals(
+        _lib.ptr(xd), xd.numel(), _lib.ptr(zd), zd.numel(), _lib.ptr(ad), ad.numel(), n_el,
+        float(pitch), float(c), _lib.ptr(ts), _lib.stream_handle()))
+    return DasPlan(n_el=n_el, pitch=pitch, fs=fs, c=c, n_samples=n_samples, x=xd, z=zd,
+                   t_star=ts, aperture=("hann", float(f_number)), out=out, prec=prec)
+
+
+def table_plan(*, n_el: int, pitch: float, fs: float, c: float, n_samples: int, x, z,
+               t_star: np.ndarray, aperture: tuple, out: str = "envelope", prec: str = "f64",
+               t0: float = 0.0, device=None) -> DasPlan:
+    """Plan with a host-computed arrival table (e.g. the reference's focused
+    transmit, das.py:135-137) and either aperture ("ref", ap_half[nz]) or
+    ("hann", f_number)."""
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    ts = np.asarray(t_star, dtype=np.float64)
+    if ts.ndim == 2:
+        ts = ts[None]
+    ap_half = None
+    if aperture[0] == "ref":
+        ap_half = _dev(np.asarray(aperture[1], dtype=np.int32), torch.int32, device)
+    return DasPlan(n_el=n_el, pitch=pitch, fs=fs, c=c, n_samples=n_samples,
+                   x=_dev(x, torch.float64, device), z=_dev(z, torch.float64, device),
+                   t_star=_dev(ts, torch.float64, device), aperture=aperture, out=out,
+                   prec=prec, t0=t0, ap_half=ap_half)
+
+
+def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=None,
+                support: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """K1: periodic analytic signal of every row of rf [..., N] (f64/f32/int16).
+
+    Returns complex64 (prec "f32") or complex128 (prec "f64") of the same shape.
+    ``support`` (int32 [rows, 2]) receives first / last nonzero sample per row.
+    """
+    L = _lib.lib()
+    if not rf.is_cuda:
+        raise ValueError("rf must be a CUDA tensor")
+    if rf.dtype not in _lib.DTYPE_CODE:
+        raise ValueError(f"unsupported rf dtype {rf.dtype}")
+    rf = rf.contiguous()
+    n = int(rf.shape[-1])
+    rows = rf.numel() // n if n else 0
+    pc = _lib.PREC_F32 if prec == "f32" else _lib.PREC_F64
+    if out is None:
+        out = torch.empty(rf.shape, dtype=_COMPLEX[pc], device=rf.device)
+    _lib.check(L.tidas_rf_analytic(_lib.ptr(rf), _lib.DTYPE_CODE[rf.dtype], n, float(scale),
+                                   _lib.ptr(out), pc, rows, n, _lib.ptr(support),
+                                   _lib.stream_handle(stream)))
+    return out
+
+
+def das_from_analytic(analytic: torch.Tensor, plan: DasPlan, out=None, stream=None) -> torch.Tensor:
+    """K2 on a precomputed analytic batch [F][A][E][N] -> image [F][nz][nx]."""
+    L = _lib.lib()
+    F = int(analytic.shape[0])
+    if analytic.dtype != _COMPLEX[plan.prec_code]:
+        raise ValueError("analytic precision does not match the plan")
+    if tuple(analytic.shape[1:]) != (plan.n_angles, plan.n_el, plan.n_samples):
+        raise ValueError(f"analytic shape {tuple(analytic.shape)} does not match the plan "
+                         f"[F][{plan.n_angles}][{plan.n_el}][{plan.n_samples}]")
+    if out is None:
+        dt = _COMPLEX[plan.prec_code] if plan.out == "iq" else _REAL[plan.prec_code]
+        out = torch.empty((F, plan.nz, plan.nx), dtype=dt, device=analytic.device)
+    d = plan.desc(F)
+    _lib.check(L.tidas_das_image(C.byref(d), _lib.ptr(analytic), _lib.ptr(plan.t_star),
+                                 _lib.ptr(plan.x), _lib.ptr(plan.z), _lib.ptr(plan.ap_half),
+                                 _lib.ptr(out), _lib.stream_handle(stream)))
+    return out
+
+
+class DasWorkspace:
+    """Reusable analytic-RF scratch for ``das_image`` (keeps a chunk L2-sized)."""
+
+    def __init__(self, plan: DasPlan, device=None):
+        self.plan = plan
+        per_frame = plan.n_angles * plan.n_el * plan.n_samples * (8 if plan.prec == "f32" else 16)
+        self.chunk = max(1, plan.chunk_bytes // per_frame)
+        device = device or plan.x.device
+        self.buf = torch.empty((self.chunk, plan.n_angles, plan.n_el, plan.n_samples),
+                               dtype=_COMPLEX[plan.prec_code], device=device)
+
+
+def das_image(rf: torch.Tensor, plan: DasPlan, *, scale: float = 1.0, out=None,
+              workspace: Optional[DasWorkspace] = None, stream=None) -> torch.Tensor:
+    """Fused DAS of a frame batch.
+
+    rf  : CUDA tensor [F][A][E][N] (or [F][E][N] for one transmit), f64/f32/int16,
+          sample-contiguous rows ("channel-contiguous").
+    out : optional [F][nz][nx] result buffer.
+    """
+    if rf.dim() == 3:
+        rf = rf.unsqueeze(1)
+    if rf.dim() != 4:
+        raise ValueError("rf must be [F][A][E][N] or [F][E][N]")
+    F = int(rf.shape[0])
+    if out is None:
+        dt = _COMPLEX[plan.prec_code] if plan.out == "iq" else _REAL[plan.prec_code]
+        out = torch.empty((F, plan.nz, plan.nx), dtype=dt, device=rf.device)
+    ws = workspace or DasWorkspace(plan, rf.device)
+    for f0 in range(0, F, ws.chunk):
+        f1 = min(F, f0 + ws.chunk)
+        an = ws.buf[: f1 - f0]
+        rf_analytic(rf[f0:f1], plan.prec, scale=scale, out=an, stream=stream)
+        das_from_analytic(an, plan, out=out[f0:f1], stream=stream)
+    return out
+
+
+def launches_per_call(F: int, plan: DasPlan, workspace: DasWorkspace) -> int:
+    """Number of library kernels ``das_image`` launches for F frames."""
+    return 2 * ((F + workspace.chunk - 1) // workspace.chunk)

@@ -1,0 +1,64 @@
+"""Frame sharding across GPUs (north star (e)).
+
+Frames (and tiDAS maps) are independent units: each rank owns a
+contiguous range of them, computes its images with no data-path collective,
+and NCCL over NVLink is used only to gather the images. Mirrors the
+reference's index-gathered, worker-count-invariant sweeps
+(experiments.py:195-199; test_experiments.py:124-131).
+"""
+from __future__ import annotations
+
+import os
+from typing import Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_units: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous [start, stop) of ``n_units`` owned by ``rank`` (balanced +-1)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank / world size")
+    base, extra = divmod(n_units, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def env_rank_world() -> Tuple[int, int, int]:
+    """(rank, world_size, local_rank) from the torchrun environment (1 process if unset)."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def init(backend: Optional[str] = None) -> Tuple[int, int]:
+    """Initialise the process group when launched by torchrun; returns (rank, world)."""
+    rank, world, local = env_rank_world()
+    if world > 1 and not dist.is_initialized():
+        backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return rank, world
+
+
+def gather_images(local: torch.Tensor, n_units: int, out: Optional[torch.Tensor] = None,
+                  group=None) -> Optional[torch.Tensor]:
+    """All-gather per-rank image shards [n_local][...] into [n_units][...] on every rank.
+
+    Shards may differ by one unit; they are padded to the largest shard for
+    ``all_gather_into_tensor`` (one NCCL call over NVLink) and trimmed."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return local if out is None else out.copy_(local)
+    tail = tuple(local.shape[1:])
+    cap = shard_range(n_units, 0, world)[1]
+    padded = local.new_zeros((cap,) + tail)
+    padded[: local.shape[0]] = local
+    buf = local.new_empty((cap * world,) + tail)
+    dist.all_gather_into_tensor(buf, padded, group=group)
+    parts = []
+    for r in range(world):
+        a, b = shard_range(n_units, r, world)
+        parts.append(buf[r * cap: r * cap + (b - a)])
+    res = torch.cat(parts)
+    return res if out is None else out.copy_(res)

@@ -1,0 +1,175 @@
+"""GPU parity: K1 (analytic RF) and K2 (fused DAS image) against the oracle.
+
+Tolerance (north star): relative L2 <= 1e-5 for the FP32 kernels against the
+float64 oracle; float64 kernels against the reference's golden vectors at
+1e-12 of the line maximum.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2507_15464_b200 as tb
+from oracle import das as od
+from oracle import geom
+from oracle import simulate as osim
+from tests.setups import CFG1, CFG2, CFG3, CFG5, grid, plane_t_star, speckle_rf
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+FP32_TOL = 1e-5
+
+
+def rel_l2(a, b):
+    return od.rel_l2(np.asarray(a), np.asarray(b))
+
+
+# ------------------------------------------------------------------ K1
+
+
+@pytest.mark.parametrize("n", [16, 2048, 4096, 8192])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int16])
+def test_analytic_pow2(n, dtype, rng):
+    x = (rng.standard_normal((6, n)) * (1000 if dtype == np.int16 else 1)).astype(dtype)
+    ref = od.analytic_signal(x.astype(np.float64))
+    for prec, tol in (("f64", 1e-13), ("f32", 2e-6)):
+        if prec == "f64" and n > 8192:
+            continue
+        got = tb.rf_analytic(torch.as_tensor(x).to(DEV), prec).cpu().numpy()
+        assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < tol, (prec, n, dtype)
+
+
+@pytest.mark.parametrize("n", [17, 100, 1000, 2285, 4096 - 3])
+def test_analytic_bluestein_any_length(n, rng):
+    x = rng.standard_normal((3, n))
+    ref = od.analytic_signal(x)
+    got = tb.rf_analytic(torch.as_tensor(x).to(DEV), "f64").cpu().numpy()
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-12
+    got32 = tb.rf_analytic(torch.as_tensor(x).to(DEV), "f32").cpu().numpy()
+    assert np.max(np.abs(got32 - ref)) / np.max(np.abs(ref)) < 5e-6
+
+
+def test_analytic_support_scan():
+    x = np.zeros((3, 64))
+    x[0, 10:20] = 1.0
+    x[1, 63] = -2.0
+    sup = torch.empty((3, 2), dtype=torch.int32, device=DEV)
+    tb.rf_analytic(torch.as_tensor(x).to(DEV), "f64", support=sup)
+    assert sup.cpu().tolist() == [[10, 19], [63, 63], [-1, -1]]
+
+
+def test_analytic_rejects_short_rows():
+    with pytest.raises(ValueError):
+        tb.rf_analytic(torch.zeros((2, 3), dtype=torch.float64, device=DEV))
+
+
+# ------------------------------------------------------------------ K2
+
+
+def _plane_case(cfg, rf, nz, nx, angles=(0.0,), out="envelope", prec="f32", rf_dtype=torch.float32):
+    x, z = grid(cfg, nz, nx)
+    plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                              n_samples=rf.shape[-1], x=x, z=z, angles=angles,
+                              f_number=cfg["f_number"], out=out, prec=prec)
+    img = tb.das_image(torch.as_tensor(rf).to(DEV, rf_dtype), plan).cpu().numpy()
+    A = np.stack([od.analytic_signal(np.asarray(rf[f], float)) for f in range(rf.shape[0])])
+    ts = plane_t_star(cfg, x, z, angles)
+    ref = np.stack([od.das_image_vectorized(A[f], cfg["fs"], 0.0, x, z, cfg["pitch"], cfg["c"], ts,
+                                            cfg["f_number"], out=out) for f in range(rf.shape[0])])
+    return img, ref, plan
+
+
+def test_cfg1_psf_image_fp32_f64_input():
+    cfg = CFG1
+    rf = osim.synthesize([0.0], [20e-3], [1.0], n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"],
+                         c=cfg["c"], f0=cfg["f0"], fbw=cfg["fbw"], n_samples=cfg["n_samples"],
+                         tx=("plane", 0.0))[None, None]
+    img, ref, _ = _plane_case(cfg, rf, cfg["nz"], cfg["nx"], rf_dtype=torch.float64)
+    assert rel_l2(img[0], ref[0]) <= FP32_TOL
+    # the peak sits at the scatterer
+    iz, ix = np.unravel_index(np.argmax(img[0]), img[0].shape)
+    x, z = grid(cfg)
+    assert abs(z[iz] - 20e-3) < 0.3e-3 and abs(x[ix]) < 0.3e-3
+
+
+def test_cfg1_fp64_instantiation_tight():
+    cfg = CFG1
+    rf = osim.synthesize([1e-3], [18e-3], [1.0], n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"],
+                         c=cfg["c"], f0=cfg["f0"], fbw=cfg["fbw"], n_samples=cfg["n_samples"],
+                         tx=("plane", 0.0))[None, None]
+    img, ref, _ = _plane_case(cfg, rf, 64, 32, prec="f64", rf_dtype=torch.float64)
+    assert rel_l2(img, ref) < 1e-11
+
+
+def test_cfg2_speckle_full_grid():
+    cfg = CFG2
+    rf, _ = speckle_rf(cfg, seed=2)
+    img, ref, _ = _plane_case(cfg, rf[None].astype(np.float32), cfg["nz"], cfg["nx"])
+    assert rel_l2(img, ref) <= FP32_TOL
+
+
+def test_cfg3_coherent_compounding_reduced():
+    cfg = CFG3
+    ang = cfg["angles"]
+    frames = [speckle_rf(cfg, seed=30 + f, n_scat=300, angles=ang)[0] for f in range(2)]
+    rf = np.stack(frames).astype(np.float32)
+    for out in ("coherent", "envelope"):
+        img, ref, _ = _plane_case(cfg, rf, 96, 48, angles=ang, out=out)
+        assert rel_l2(img, ref) <= FP32_TOL, out
+
+
+def test_cfg5_int16_ingest_reduced():
+    cfg = CFG5
+    rng = np.random.default_rng(5)
+    sx, sz, a = osim.speckle(rng, 400, cfg["x"], (8e-3, 55e-3))
+    rf = osim.synthesize(sx, sz, a, n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                         f0=cfg["f0"], fbw=cfg["fbw"], n_samples=cfg["n_samples"], tx=("plane", 0.0))
+    q = osim.quantize_int16(rf, cfg["target_std"])[None, None]
+    img, ref, _ = _plane_case(cfg, q, 64, 64, rf_dtype=torch.int16)
+    assert rel_l2(img, ref) <= FP32_TOL
+
+
+def test_iq_output_and_ragged_grid():
+    cfg = CFG2
+    rf, _ = speckle_rf(cfg, seed=7, n_scat=200)
+    img, ref, _ = _plane_case(cfg, rf[None].astype(np.float32), 37, 53, out="iq")
+    assert img.dtype == np.complex64
+    assert rel_l2(img, ref) <= FP32_TOL
+
+
+def test_frame_batching_is_bitwise_per_frame():
+    """Frames share the time-of-flight work in a CTA; each frame's image is the
+    one it gets alone (worker-count invariance, test_experiments.py:124-131)."""
+    cfg = CFG2
+    rfs = np.stack([speckle_rf(cfg, seed=40 + f, n_scat=150)[0] for f in range(5)]).astype(np.float32)
+    x, z = grid(cfg, 64, 32)
+    plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                              n_samples=cfg["n_samples"], x=x, z=z, f_number=cfg["f_number"])
+    batch = tb.das_image(torch.as_tensor(rfs).to(DEV), plan).cpu().numpy()
+    for f in range(5):
+        alone = tb.das_image(torch.as_tensor(rfs[f:f + 1]).to(DEV), plan).cpu().numpy()[0]
+        assert np.array_equal(batch[f], alone)
+
+
+def test_zero_rf_and_out_of_support_pixels():
+    cfg = CFG1
+    x, z = grid(cfg, 40, 8)
+    z = np.concatenate([z, [200e-3]])  # t* beyond the record -> 0 (np.interp right=0)
+    plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                              n_samples=cfg["n_samples"], x=x, z=z, f_number=cfg["f_number"])
+    zero = torch.zeros((2, 1, cfg["n_el"], cfg["n_samples"]), device=DEV)
+    assert not tb.das_image(zero, plan).any()
+    rf = osim.synthesize([0.0], [20e-3], [1.0], n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"],
+                         c=cfg["c"], f0=cfg["f0"], fbw=cfg["fbw"], n_samples=cfg["n_samples"],
+                         tx=("plane", 0.0))
+    img = tb.das_image(torch.as_tensor(rf[None, None]).to(DEV), plan).cpu().numpy()
+    assert np.all(img[0, -1] == 0.0)
+    assert tb.das_image(torch.zeros((0, 1, cfg["n_el"], cfg["n_samples"]), device=DEV), plan).shape[0] == 0
+
+
+def test_plan_validation():
+    cfg = CFG1
+    x, z = grid(cfg, 8, 8)
+    plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                              n_samples=cfg["n_samples"], x=x, z=z, f_number=cfg["f_number"])
+    with pytest.raises(ValueError):
+        tb.das_from_analytic(torch.zeros((1, 1, 4, 16), dtype=torch.complex64, device=DEV), plan)
