@@ -244,8 +244,9 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
     };
     // --- issue the copies of channel n's window into buffer `slot`
     auto issue = [&](int n, int slot, int lo, int hi) {
+      if (hi < lo) return;  // no live tap in the CTA (lo = INT_MAX, hi = INT_MIN)
       const int W = hi - lo + 1;
-      if (W <= 0 || W > DAS_WMAX) return;
+      if (W > DAS_WMAX) return;
       C* dst = win + (size_t)slot * FB * DAS_WSTRIDE;
       for (int i = tid; i < W * FB; i += DAS_NT) {
         const int b = i / W, e = i - b * W;
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();  // (B) current window resident
-      const int W = cur_hi - cur_lo + 1;
+      const int W = cur_hi >= cur_lo ? cur_hi - cur_lo + 1 : 0;
       if (W > 0) {
         if (W <= DAS_WMAX) {
           const C* wb = win + (size_t)slot * FB * DAS_WSTRIDE;
@@ -373,12 +374,13 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
   return TIDAS_OK;
 }
 
+// A fixed frame-batch width per precision (not chosen from F) keeps every
+// frame's arithmetic independent of how many frames share the launch, so
+// images are bit-identical under any batching or sharding.
 template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   if (sizeof(R) == 8) return launch_das<R, AP, OUT, 1>(p, A, out, st);
-  if (p.F >= 4) return launch_das<R, AP, OUT, 4>(p, A, out, st);
-  if (p.F >= 2) return launch_das<R, AP, OUT, 2>(p, A, out, st);
-  return launch_das<R, AP, OUT, 1>(p, A, out, st);
+  return launch_das<R, AP, OUT, 4>(p, A, out, st);
 }
 
 template <typename R, int AP>

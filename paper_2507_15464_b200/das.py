@@ -258,11 +258,15 @@ def _window_read(traces_d: torch.Tensor, lo, hi, pos, theta) -> np.ndarray:
     L = _lib.lib()
     P, N = traces_d.shape
     out = torch.empty(P, dtype=torch.float64, device=traces_d.device)
+    # keep every argument tensor referenced until the launch is enqueued: a
+    # temporary freed earlier would be handed to the next allocation
     tr = _to_dev(np.arange(P, dtype=np.int32), torch.int32)
     th = _to_dev(np.asarray(theta, float)) if theta is not None else None
+    lo_d = _to_dev(np.asarray(lo, np.int32), torch.int32)
+    hi_d = _to_dev(np.asarray(hi, np.int32), torch.int32)
+    pos_d = _to_dev(np.asarray(pos, float))
     _lib.check(L.tidas_window_envelope_f64(
-        _lib.ptr(traces_d), N, _lib.ptr(tr), _lib.ptr(_to_dev(np.asarray(lo, np.int32), torch.int32)),
-        _lib.ptr(_to_dev(np.asarray(hi, np.int32), torch.int32)), _lib.ptr(_to_dev(np.asarray(pos, float))),
+        _lib.ptr(traces_d), N, _lib.ptr(tr), _lib.ptr(lo_d), _lib.ptr(hi_d), _lib.ptr(pos_d),
         _lib.ptr(th), P, _lib.ptr(out), _lib.stream_handle()))
     return out.cpu().numpy()
 

@@ -228,11 +228,13 @@ def tidas_line(frame: RfFrame, fixed_delays: DelayProfile, thetas: Sequence[floa
     P = len(depths)
     out = torch.empty(P, dtype=torch.float64, device=s_d.device)
     tr = torch.zeros(P, dtype=torch.int32, device=s_d.device)
+    lo_d = _to_dev(lo.astype(np.int32), torch.int32)
+    hi_d = _to_dev(np.maximum(hi, lo).astype(np.int32), torch.int32)
+    pos_d = _to_dev((arrivals - frame.t0) * fs)
+    th_d = _to_dev(thetas)
     _lib.check(L.tidas_window_envelope_f64(
-        _lib.ptr(s_d), N, _lib.ptr(tr), _lib.ptr(_to_dev(lo.astype(np.int32), torch.int32)),
-        _lib.ptr(_to_dev(np.maximum(hi, lo).astype(np.int32), torch.int32)),
-        _lib.ptr(_to_dev((arrivals - frame.t0) * fs)), _lib.ptr(_to_dev(thetas)), P,
-        _lib.ptr(out), _lib.stream_handle()))
+        _lib.ptr(s_d), N, _lib.ptr(tr), _lib.ptr(lo_d), _lib.ptr(hi_d), _lib.ptr(pos_d),
+        _lib.ptr(th_d), P, _lib.ptr(out), _lib.stream_handle()))
     return out.cpu().numpy()
 
 

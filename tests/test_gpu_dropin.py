@@ -142,7 +142,7 @@ def test_fixture_line_csv_das_column():
 
 
 def test_reference_errors():
-    f = T.RfFrame(np.zeros((192, 64)), 50e6, 0.0, 25e-3, np.arange(-10, 10))
+    f = T.RfFrame(np.zeros((192, 2048)), 50e6, 0.0, 25e-3, np.arange(-10, 10))
     with pytest.raises(ValueError):
         T.das_line(f, np.array([10e-3, 9e-3]), PROBE, RX)
     with pytest.raises(ValueError):  # |delay| fs >= n (das.py:87-88)
@@ -153,6 +153,9 @@ def test_reference_errors():
     with pytest.raises(ValueError):
         T.tidas_psf(f, T.rx_delay_profile(25e-3, np.arange(-2, 2), PROBE), float("nan"))
     assert T.das_value(f, (0.0, 25e-3), PROBE, RX) == 0.0
+    short = T.RfFrame(np.zeros((192, 64)), 50e6, 0.0, 25e-3, np.arange(-10, 10))
+    with pytest.raises(ValueError):  # 25 mm F#1 shifts reach 93 samples > 64 (das.py:87-88)
+        T.das_value(short, (0.0, 25e-3), PROBE, RX)
 
 
 def test_fractional_delay_linear_and_spectral(rng):

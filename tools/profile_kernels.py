@@ -1,0 +1,43 @@
+"""Small driver for ncu: one cfg2 DAS chunk (K1 + K2) and one row-operator launch.
+
+  python tools/profile_kernels.py [--iters 2]
+  ncu --set full -k regex:"das_image|analytic_pow2|rowconv_kernel" -c 3 python tools/profile_kernels.py
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2507_15464_b200 as tb  # noqa: E402
+from bench import CFG2, frame_scatterers, grid  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--iters", type=int, default=1)
+ap.add_argument("--frames", type=int, default=8)
+ap.add_argument("--maps", type=int, default=32)
+args = ap.parse_args()
+
+cfg = CFG2
+F = args.frames
+sx, sz, a = frame_scatterers(cfg, range(F))
+rf = tb.synthesize_batch(sx, sz, a, angles=[0.0], n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"],
+                         c=cfg["c"], f0=cfg["f0"], fbw=cfg["fbw"], n_samples=cfg["n_samples"])
+x, z = grid(cfg)
+plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                          n_samples=cfg["n_samples"], x=x, z=z, f_number=cfg["f_number"])
+an = torch.empty((F, 1, cfg["n_el"], cfg["n_samples"]), dtype=torch.complex64, device="cuda")
+img = torch.empty((F, cfg["nz"], cfg["nx"]), device="cuda")
+gen = torch.Generator(device="cuda").manual_seed(1)
+maps = (torch.rand((args.maps, 2048, 1024), device="cuda", generator=gen) < 0.02).float()
+K = torch.randn((2048, 129), device="cuda", generator=gen)
+y = torch.empty_like(maps)
+torch.cuda.synchronize()
+for _ in range(args.iters):
+    tb.rf_analytic(rf, "f32", out=an)
+    tb.das_from_analytic(an, plan, out=img)
+    tb.tidas_rowconv(maps, K, out=y)
+torch.cuda.synchronize()
+print("ok", float(img.sum()), float(y.abs().sum()))
