@@ -61,43 +61,84 @@ template <typename R> __device__ __forceinline__ cplx<R> spectral_op(cplx<R> v, 
   return cmul(v, w);
 }
 
-template <typename R, typename In>
-__global__ void __launch_bounds__(512) analytic_pow2_kernel(const In* __restrict__ rf,
-                                                             int64_t stride, R scale,
-                                                             cplx<R>* __restrict__ out,
-                                                             int logN,
-                                                             int32_t* __restrict__ support,
-                                                             double shift) {
+// Power-of-two rows, Hilbert mode: two channels per CTA. The Hilbert transform
+// is complex-linear, so one complex FFT pair of z = x_a + i x_b gives
+// H(z) = H(x_a) + i H(x_b); the analytic rows are A_a = x_a + i H(x_a) and
+// A_b = x_b + i H(x_b). With scipy's mask h (1 at DC and Nyquist, 2 on positive
+// bins), ifft(fft(x) h) = x + i IFFT(-i sgn(k) X)(k): the real part is the input
+// itself and the imaginary part uses the multiplier -i sgn(k) / N.
+// Delay mode (spectral fractional delay, one row per CTA): out = IFFT(X * ramp).
+template <typename R, typename In, bool DELAY>
+__global__ void __launch_bounds__(512, 1) analytic_pow2_kernel(const In* __restrict__ rf,
+                                                            int64_t stride, R scale,
+                                                            cplx<R>* __restrict__ out,
+                                                            int64_t n_rows, int logN,
+                                                            int32_t* __restrict__ support,
+                                                            double shift) {
   using C = cplx<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
-  __shared__ int first_nz, last_nz;
+  __shared__ int first_nz[2], last_nz[2];
   const int N = 1 << logN;
-  const int64_t row = blockIdx.x;
-  const In* src = rf + row * stride;
-  if (threadIdx.x == 0) { first_nz = N; last_nz = -1; }
-  int lo = N, hi = -1;
+  const int64_t ra = DELAY ? (int64_t)blockIdx.x : 2 * (int64_t)blockIdx.x;
+  const bool has_b = !DELAY && (ra + 1 < n_rows);
+  const In* src_a = rf + ra * stride;
+  const In* src_b = rf + (ra + 1) * stride;
+  if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
-    const R v = R(load_as_double(src + n)) * scale;
-    if (v != R(0)) { lo = min(lo, n); hi = max(hi, n); }
-    C c; c.x = v; c.y = R(0);
-    s[n] = c;
+    const R xa = R(load_as_double(src_a + n)) * scale;
+    const R xb = has_b ? R(load_as_double(src_b + n)) * scale : R(0);
+    if (xa != R(0)) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+    if (xb != R(0)) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    C c; c.x = xa; c.y = xb;
+    s[fpad(n)] = c;
   }
   __syncthreads();
   if (support) {
-    if (lo < N) atomicMin(&first_nz, lo);
-    if (hi >= 0) atomicMax(&last_nz, hi);
+    if (lo_a < N) atomicMin(&first_nz[0], lo_a);
+    if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
+    if (lo_b < N) atomicMin(&first_nz[1], lo_b);
+    if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
   }
   fft_inplace<R, false>(s, logN);
-  for (int k = threadIdx.x; k < N; k += blockDim.x) s[k] = spectral_op<R>(s[k], k, N, shift);
+  const R invN = R(1) / R(N);
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    C v = s[fpad(k)];
+    if (DELAY) {
+      v = spectral_op<R>(v, k, N, shift);
+    } else {
+      C r;  // -i sgn(k) v / N
+      if (k == 0 || k == N / 2) { r.x = R(0); r.y = R(0); }
+      else if (k < N / 2) { r.x = v.y * invN; r.y = -v.x * invN; }
+      else { r.x = -v.y * invN; r.y = v.x * invN; }
+      v = r;
+    }
+    s[fpad(k)] = v;
+  }
   __syncthreads();
   fft_inplace<R, true>(s, logN);
-  C* dst = out + row * (int64_t)N;
-  for (int n = threadIdx.x; n < N; n += blockDim.x) dst[n] = s[n];
+  C* dst_a = out + ra * (int64_t)N;
+  C* dst_b = dst_a + N;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    const C y = s[fpad(n)];
+    if (DELAY) {
+      dst_a[n] = y;
+    } else {
+      C a; a.x = R(load_as_double(src_a + n)) * scale; a.y = y.x;
+      dst_a[n] = a;
+      if (has_b) {
+        C b; b.x = R(load_as_double(src_b + n)) * scale; b.y = y.y;
+        dst_b[n] = b;
+      }
+    }
+  }
   if (support && threadIdx.x == 0) {
-    const bool any = last_nz >= 0;
-    support[2 * row] = any ? first_nz : -1;
-    support[2 * row + 1] = any ? last_nz : -1;
+    for (int c = 0; c < (has_b ? 2 : 1); ++c) {
+      const bool any = last_nz[c] >= 0;
+      support[2 * (ra + c)] = any ? first_nz[c] : -1;
+      support[2 * (ra + c) + 1] = any ? last_nz[c] : -1;
+    }
   }
 }
 
@@ -129,11 +170,11 @@ __global__ void __launch_bounds__(512) chirp_spectrum_kernel(int N, int logM, cp
     C v = cmake<C>(0.0, 0.0);
     if (j < N) v = chirp<R>(j, N, conj_);
     else if (j > M - N) v = chirp<R>(M - j, N, conj_);
-    s[j] = v;
+    s[fpad(j)] = v;
   }
   __syncthreads();
   fft_inplace<R, false>(s, logM);
-  for (int j = threadIdx.x; j < M; j += blockDim.x) B[(int64_t)blockIdx.x * M + j] = s[j];
+  for (int j = threadIdx.x; j < M; j += blockDim.x) B[(int64_t)blockIdx.x * M + j] = s[fpad(j)];
 }
 
 // s holds x (length N, zero beyond); on return s[0..N) = DFT_N(x) (fwd) or
@@ -145,16 +186,16 @@ __device__ void bluestein_dft(cplx<R>* s, int N, int logM, const cplx<R>* __rest
   const int M = 1 << logM;
   for (int j = threadIdx.x; j < M; j += blockDim.x) {
     C v = cmake<C>(0.0, 0.0);
-    if (j < N) v = cmul(s[j], chirp<R>(j, N, !INV));
-    s[j] = v;
+    if (j < N) v = cmul(s[fpad(j)], chirp<R>(j, N, !INV));
+    s[fpad(j)] = v;
   }
   __syncthreads();
   fft_inplace<R, false>(s, logM);
   const R invM = R(1) / R(M);
-  for (int j = threadIdx.x; j < M; j += blockDim.x) s[j] = cscale(cmul(s[j], Bspec[j]), invM);
+  for (int j = threadIdx.x; j < M; j += blockDim.x) s[fpad(j)] = cscale(cmul(s[fpad(j)], Bspec[j]), invM);
   __syncthreads();
   fft_inplace<R, true>(s, logM);
-  for (int k = threadIdx.x; k < N; k += blockDim.x) s[k] = cmul(s[k], chirp<R>(k, N, !INV));
+  for (int k = threadIdx.x; k < N; k += blockDim.x) s[fpad(k)] = cmul(s[fpad(k)], chirp<R>(k, N, !INV));
   __syncthreads();
 }
 
@@ -179,7 +220,7 @@ __global__ void __launch_bounds__(512) analytic_bluestein_kernel(
       if (v != R(0)) { lo = min(lo, n); hi = max(hi, n); }
     }
     C c; c.x = v; c.y = R(0);
-    s[n] = c;
+    s[fpad(n)] = c;
   }
   __syncthreads();
   if (support) {
@@ -188,11 +229,11 @@ __global__ void __launch_bounds__(512) analytic_bluestein_kernel(
   }
   bluestein_dft<R, false>(s, N, logM, Bfwd);
   for (int k = threadIdx.x; k < M; k += blockDim.x)
-    s[k] = k < N ? spectral_op<R>(s[k], k, N, shift) : cmake<C>(0.0, 0.0);
+    s[fpad(k)] = k < N ? spectral_op<R>(s[fpad(k)], k, N, shift) : cmake<C>(0.0, 0.0);
   __syncthreads();
   bluestein_dft<R, true>(s, N, logM, Binv);
   C* dst = out + row * (int64_t)N;
-  for (int n = threadIdx.x; n < N; n += blockDim.x) dst[n] = s[n];
+  for (int n = threadIdx.x; n < N; n += blockDim.x) dst[n] = s[fpad(n)];
   if (support && threadIdx.x == 0) {
     const bool any = last_nz >= 0;
     support[2 * row] = any ? first_nz : -1;
@@ -241,7 +282,7 @@ static int get_chirp_spectra(int device, int N, int logM, const cplx<R>** out) {
   const int M = 1 << logM;
   void* B = nullptr;
   TIDAS_CUDA_CHECK(cudaMalloc(&B, sizeof(C) * 2 * (size_t)M));
-  const size_t smem = sizeof(C) * (size_t)M;
+  const size_t smem = sizeof(C) * (size_t)fft_smem_elems(M);
   auto kern = chirp_spectrum_kernel<R>;
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<2, threads_for<R>(logM), smem>>>(N, logM, reinterpret_cast<C*>(B));
@@ -264,19 +305,22 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
   if (logN >= 0) {
     TIDAS_REQUIRE(logN >= 4 && logN <= FFT_MAX_LOG, "power-of-two n_samples must be in [16, %d]",
                   1 << FFT_MAX_LOG);
-    const size_t smem = sizeof(C) * (size_t)N;
+    const size_t smem = sizeof(C) * (size_t)fft_smem_elems(N);
     TIDAS_REQUIRE(smem <= 227 * 1024, "n_samples=%d too long for the on-chip FFT at this precision", N);
-    auto kern = analytic_pow2_kernel<R, In>;
+    const bool delay = !isnan(shift);
+    auto kern = delay ? analytic_pow2_kernel<R, In, true> : analytic_pow2_kernel<R, In, false>;
     TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)n_rows, threads_for<R>(logN), smem, st>>>(rf, stride, (R)scale,
-                                                                reinterpret_cast<C*>(out), logN, support, shift);
+    TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    const int64_t ctas = delay ? n_rows : (n_rows + 1) / 2;
+    kern<<<(unsigned)ctas, threads_for<R>(logN), smem, st>>>(rf, stride, (R)scale, reinterpret_cast<C*>(out),
+                                                              n_rows, logN, support, shift);
     TIDAS_LAUNCH_CHECK();
     return TIDAS_OK;
   }
   int logM = 0;
   while ((1 << logM) < 2 * N - 1) ++logM;
   logM = logM < 4 ? 4 : logM;
-  const size_t smem = sizeof(C) * ((size_t)1 << logM);
+  const size_t smem = sizeof(C) * (size_t)fft_smem_elems(1 << logM);
   TIDAS_REQUIRE(logM <= FFT_MAX_LOG && smem <= 227 * 1024,
                 "non-power-of-two n_samples=%d needs a %d-point Bluestein grid: too long", N,
                 1 << logM);

@@ -35,7 +35,8 @@ namespace tidas {
 constexpr int DAS_TZ = 32;   // depths per CTA (lanes)
 constexpr int DAS_TX = 8;    // columns per CTA (warps)
 constexpr int DAS_NT = DAS_TZ * DAS_TX;
-constexpr int DAS_WMAX = 448;  // staged window capacity (samples) per frame
+constexpr int DAS_WMAX = 400;  // staged window capacity (samples) per frame
+constexpr int DAS_NBUF = 3;    // channel windows in flight (triple buffer, 1 barrier/channel)
 
 __host__ __device__ constexpr int win_pad(int p) { return p + (p >> 4); }
 constexpr int DAS_WSTRIDE = win_pad(DAS_WMAX) + 2;  // padded per-frame window stride
@@ -154,9 +155,8 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
                                                            void* __restrict__ out_) {
   using C = cplx<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* win = reinterpret_cast<C*>(smem_raw);                 // [2][FB][DAS_WSTRIDE]
-  __shared__ int2 wwin[2][DAS_TX];                         // per-warp tap range per slot
-  __shared__ int ch_lo_s, ch_hi_s;
+  C* win = reinterpret_cast<C*>(smem_raw);  // [DAS_NBUF][FB][DAS_WSTRIDE]
+  __shared__ int red[4];                    // channel range, tap window
 
   const int lane = threadIdx.x, wid = threadIdx.y;
   const int tid = wid * DAS_TZ + lane;
@@ -171,32 +171,41 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
   PixelGeo<R> geo;
   geo.init(p, x, zm);
 
-  // receive aperture (channel range) of this pixel
-  int n_lo = half, n_hi = -half - 1;
+  // receive aperture of this pixel and the largest lateral offset inside it
+  int n_lo = half, n_hi = -half - 1, ap_h = 0;
+  double dxmax = 0.0;
   if (pix) {
     if (AP == TIDAS_AP_HANN) {
       const double a = zm / (2.0 * p.f_number);
-      n_lo = (int)floor((x - a) / p.pitch - 0.5);       // one extra each side: the
-      n_hi = (int)ceil((x + a) / p.pitch - 0.5);        // predicate |dx| < a decides
+      n_lo = (int)floor((x - a) / p.pitch - 0.5);  // one extra each side: the
+      n_hi = (int)ceil((x + a) / p.pitch - 0.5);   // predicate |dx| < a decides
+      dxmax = a;
     } else {
-      const int h = p.ap_half[iz];
-      n_lo = -h;
-      n_hi = h - 1;
+      ap_h = p.ap_half[iz];
+      n_lo = -ap_h;
+      n_hi = ap_h - 1;
     }
     n_lo = max(n_lo, -half);
     n_hi = min(n_hi, half - 1);
+    if (n_lo <= n_hi) {
+      dxmax = fmin(dxmax > 0.0 ? dxmax : 1e300,
+                   fmax(fabs(((double)n_lo + 0.5) * p.pitch - x), fabs(((double)n_hi + 0.5) * p.pitch - x)));
+    }
   }
-  if (tid == 0) { ch_lo_s = INT_MAX; ch_hi_s = INT_MIN; }
+  // most negative receive shift of the pixel (samples): taps j = k0 - m lie in
+  // [k0, k0 - floor(s_min)] for every channel of its aperture
+  const double s_min = (zm - hypot(dxmax, zm)) / p.c * p.fs;
+  const int m_min = (int)floor(s_min) - 1;  // one sample of slack for FP32 rounding
+
+  if (tid == 0) { red[0] = INT_MAX; red[1] = INT_MIN; }
   __syncthreads();
   {
     const int wl = __reduce_min_sync(0xffffffffu, n_lo);
     const int wh = __reduce_max_sync(0xffffffffu, n_hi);
-    if (lane == 0) { atomicMin(&ch_lo_s, wl); atomicMax(&ch_hi_s, wh); }
+    if (lane == 0) { atomicMin(&red[0], wl); atomicMax(&red[1], wh); }
   }
   __syncthreads();
-  const int c_lo = ch_lo_s, c_hi = ch_hi_s;
-  int ap_h = 0;
-  if (AP == TIDAS_AP_REF_BOXCAR && pix) ap_h = p.ap_half[iz];
+  const int c_lo = red[0], c_hi = red[1];
 
   R acc_env[FB];
   C acc_iq[FB];
@@ -218,107 +227,88 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
         fr = (R)(pos - fl);
       }
     }
-    const bool active_px = pix && vpos;
-    if (c_lo > c_hi) continue;
+    const bool active_px = pix && vpos && n_lo <= n_hi;
+    // CTA tap window for this transmit (same for every channel)
+    if (tid == 0) { red[2] = INT_MAX; red[3] = INT_MIN; }
+    __syncthreads();
+    {
+      const int wl = __reduce_min_sync(0xffffffffu, active_px ? k0 - 1 : INT_MAX);
+      const int wh = __reduce_max_sync(0xffffffffu, active_px ? k0 - m_min + 1 : INT_MIN);
+      if (lane == 0) { atomicMin(&red[2], wl); atomicMax(&red[3], wh); }
+    }
+    __syncthreads();
+    const int w_lo = red[2], w_hi = red[3];
+    if (w_hi < w_lo || c_lo > c_hi) continue;  // CTA-uniform
+    const int W = w_hi - w_lo + 1;
+    const bool staged = W <= DAS_WMAX;
 
     C c0[FB], c1[FB];
 #pragma unroll
     for (int b = 0; b < FB; ++b) { c0[b].x = c0[b].y = R(0); c1[b].x = c1[b].y = R(0); }
 
-    // --- stage helper: compute taps of channel n, publish the warp's range
-    auto compute_tap = [&](int n, int slot, Tap<R>& t) {
+    auto row_ptr = [&](int b, int n) {
+      const int fb = min(f0 + b, p.F - 1);
+      return A + (((int64_t)fb * p.A + a) * p.E + (n + half)) * rowN;
+    };
+    auto issue = [&](int n, int slot) {
+      if (n > c_hi) return;
+      C* dst = win + (size_t)slot * FB * DAS_WSTRIDE;
+      for (int e = tid; e < W; e += DAS_NT) {
+        const int src = wrapN(w_lo + e, p.N);
+        const int d = win_pad(e);
+#pragma unroll
+        for (int b = 0; b < FB; ++b) cp_async_elem<R>(dst + b * DAS_WSTRIDE + d, row_ptr(b, n) + src);
+      }
+    };
+    auto accumulate = [&](const Tap<R>& t, int b, C am1, C a0, C ap1) {
+      c0[b].x += t.w0 * a0.x + t.w1 * am1.x;
+      c0[b].y += t.w0 * a0.y + t.w1 * am1.y;
+      c1[b].x += t.w0 * ap1.x + t.w1 * a0.x;
+      c1[b].y += t.w0 * ap1.y + t.w1 * a0.y;
+    };
+
+    if (staged) {
+      issue(c_lo, 0);
+      cp_async_commit();
+      issue(c_lo + 1, 1);
+      cp_async_commit();
+    }
+    int slot = 0;
+    for (int n = c_lo; n <= c_hi; ++n) {
+      Tap<R> t;
       bool in_ap = active_px && n >= n_lo && n <= n_hi;
       if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
       geo.template tap<AP>(p, n, k0, in_ap, t);
       const bool live = in_ap && (t.w0 != R(0) || t.w1 != R(0));
-      const int lo = __reduce_min_sync(0xffffffffu, live ? t.j - 1 : INT_MAX);
-      const int hi = __reduce_max_sync(0xffffffffu, live ? t.j + 1 : INT_MIN);
-      if (lane == 0) wwin[slot][wid] = make_int2(lo, hi);
-      if (!live) { t.w0 = R(0); t.w1 = R(0); }
-    };
-    // --- after a barrier: CTA window of a slot
-    auto window_of = [&](int slot, int& lo, int& hi) {
-      lo = INT_MAX; hi = INT_MIN;
-#pragma unroll
-      for (int w = 0; w < DAS_TX; ++w) { lo = min(lo, wwin[slot][w].x); hi = max(hi, wwin[slot][w].y); }
-    };
-    // --- issue the copies of channel n's window into buffer `slot`
-    auto issue = [&](int n, int slot, int lo, int hi) {
-      if (hi < lo) return;  // no live tap in the CTA (lo = INT_MAX, hi = INT_MIN)
-      const int W = hi - lo + 1;
-      if (W > DAS_WMAX) return;
-      C* dst = win + (size_t)slot * FB * DAS_WSTRIDE;
-      for (int i = tid; i < W * FB; i += DAS_NT) {
-        const int b = i / W, e = i - b * W;
-        const int fb = min(f0 + b, p.F - 1);
-        const C* src = A + (((int64_t)fb * p.A + a) * p.E + (n + half)) * rowN;
-        cp_async_elem<R>(dst + b * DAS_WSTRIDE + win_pad(e), src + wrapN(lo + e, p.N));
-      }
-    };
-
-    Tap<R> cur, nxt;
-    int slot = 0;
-    compute_tap(c_lo, 0, cur);
-    __syncthreads();
-    int cur_lo, cur_hi;
-    window_of(0, cur_lo, cur_hi);
-    issue(c_lo, 0, cur_lo, cur_hi);
-    cp_async_commit();
-
-    for (int n = c_lo; n <= c_hi; ++n) {
-      const bool has_next = n < c_hi;
-      if (has_next) compute_tap(n + 1, slot ^ 1, nxt);
-      __syncthreads();  // (A) next window published; previous gather done
-      int nx_lo = 0, nx_hi = -1;
-      if (has_next) {
-        window_of(slot ^ 1, nx_lo, nx_hi);
-        issue(n + 1, slot ^ 1, nx_lo, nx_hi);
-      }
-      cp_async_commit();
-      cp_async_wait<1>();
-      __syncthreads();  // (B) current window resident
-      const int W = cur_hi >= cur_lo ? cur_hi - cur_lo + 1 : 0;
-      if (W > 0) {
-        if (W <= DAS_WMAX) {
+      if (staged) {
+        cp_async_wait<1>();
+        __syncthreads();  // window n resident for all; slot (n+2)%3 no longer read
+        issue(n + 2, slot == 0 ? 2 : slot - 1);
+        cp_async_commit();
+        if (live) {
           const C* wb = win + (size_t)slot * FB * DAS_WSTRIDE;
-          const int e = cur.j - cur_lo;  // position of tap j-1 is e-1
+          const int e = t.j - w_lo;
 #pragma unroll
-          for (int b = 0; b < FB; ++b) {
-            if (cur.w0 == R(0) && cur.w1 == R(0)) break;
-            const C am1 = wb[b * DAS_WSTRIDE + win_pad(e - 1)];
-            const C a0 = wb[b * DAS_WSTRIDE + win_pad(e)];
-            const C ap1 = wb[b * DAS_WSTRIDE + win_pad(e + 1)];
-            c0[b].x += cur.w0 * a0.x + cur.w1 * am1.x;
-            c0[b].y += cur.w0 * a0.y + cur.w1 * am1.y;
-            c1[b].x += cur.w0 * ap1.x + cur.w1 * a0.x;
-            c1[b].y += cur.w0 * ap1.y + cur.w1 * a0.y;
-          }
-        } else if (cur.w0 != R(0) || cur.w1 != R(0)) {
-          // oversized window (steep geometry): gather straight from global
+          for (int b = 0; b < FB; ++b)
+            accumulate(t, b, wb[b * DAS_WSTRIDE + win_pad(e - 1)], wb[b * DAS_WSTRIDE + win_pad(e)],
+                       wb[b * DAS_WSTRIDE + win_pad(e + 1)]);
+        }
+        slot = slot == DAS_NBUF - 1 ? 0 : slot + 1;
+      } else if (live) {
+        // oversized window (steep geometry): gather straight from global
 #pragma unroll
-          for (int b = 0; b < FB; ++b) {
-            const int fb = min(f0 + b, p.F - 1);
-            const C* src = A + (((int64_t)fb * p.A + a) * p.E + (n + half)) * rowN;
-            const C am1 = src[wrapN(cur.j - 1, p.N)];
-            const C a0 = src[wrapN(cur.j, p.N)];
-            const C ap1 = src[wrapN(cur.j + 1, p.N)];
-            c0[b].x += cur.w0 * a0.x + cur.w1 * am1.x;
-            c0[b].y += cur.w0 * a0.y + cur.w1 * am1.y;
-            c1[b].x += cur.w0 * ap1.x + cur.w1 * a0.x;
-            c1[b].y += cur.w0 * ap1.y + cur.w1 * a0.y;
-          }
+        for (int b = 0; b < FB; ++b) {
+          const C* src = row_ptr(b, n);
+          accumulate(t, b, src[wrapN(t.j - 1, p.N)], src[wrapN(t.j, p.N)], src[wrapN(t.j + 1, p.N)]);
         }
       }
-      cur = nxt;
-      cur_lo = nx_lo;
-      cur_hi = nx_hi;
-      slot ^= 1;
     }
-    cp_async_wait<0>();
-    __syncthreads();
+    if (staged) {
+      cp_async_wait<0>();
+      __syncthreads();
+    }
 
     if (active_px) {
-      const R g = R(1) - fr;
 #pragma unroll
       for (int b = 0; b < FB; ++b) {
         if (OUT == TIDAS_OUT_ENVELOPE) {
@@ -326,6 +316,7 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
           const R e0 = cabs_(c0[b]);
           acc_env[b] += (fr == R(0)) ? e0 : e0 + (cabs_(c1[b]) - e0) * fr;
         } else {
+          const R g = R(1) - fr;
           acc_iq[b].x += g * c0[b].x + fr * c1[b].x;
           acc_iq[b].y += g * c0[b].y + fr * c1[b].y;
         }
@@ -364,7 +355,7 @@ template <typename R, int AP, int OUT, int FB>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
   auto kern = das_image_kernel<R, AP, OUT, FB>;
-  const size_t smem = sizeof(C) * 2 * FB * DAS_WSTRIDE;
+  const size_t smem = sizeof(C) * DAS_NBUF * FB * DAS_WSTRIDE;
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 block(DAS_TZ, DAS_TX);
   dim3 grid((p.nz + DAS_TZ - 1) / DAS_TZ, (p.nx + DAS_TX - 1) / DAS_TX, (p.F + FB - 1) / FB);

@@ -22,65 +22,92 @@
 namespace tidas {
 
 constexpr int RC_THREADS = 256;
+constexpr int RC_OUT = 8;  // consecutive outputs per thread
 
+// Stage ROWS input rows of depth row i (zero halo of H each side) and the row
+// kernel (reversed for the adjoint) in shared memory.
 template <bool ADJ>
+__device__ __forceinline__ void rc_stage(const float* __restrict__ in, const float* __restrict__ K,
+                                         float* Ks, float* G, int i, int64_t b0, int nrows, int rows,
+                                         int nz, int nx, int T, int Tp, int L) {
+  const int H = (T - 1) / 2;
+  for (int k = threadIdx.x; k < Tp + 4; k += blockDim.x)
+    Ks[k] = k < T ? K[(int64_t)i * T + (ADJ ? (T - 1 - k) : k)] : 0.0f;
+  const int nx4 = nx >> 2;
+  const bool vec = (H & 3) == 0;
+  for (int r = 0; r < rows; ++r) {
+    float* Gr = G + r * L;
+    const float4* src = reinterpret_cast<const float4*>(in + ((b0 + r) * nz + i) * (int64_t)nx);
+    for (int q = threadIdx.x; q < nx4; q += blockDim.x) {
+      const float4 v = r < nrows ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (vec) {
+        *reinterpret_cast<float4*>(Gr + H + 4 * q) = v;
+      } else {
+        Gr[H + 4 * q] = v.x; Gr[H + 4 * q + 1] = v.y; Gr[H + 4 * q + 2] = v.z; Gr[H + 4 * q + 3] = v.w;
+      }
+    }
+    for (int e = threadIdx.x; e < H; e += blockDim.x) Gr[e] = 0.0f;
+    for (int e = H + nx + threadIdx.x; e < L; e += blockDim.x) Gr[e] = 0.0f;
+  }
+}
+
+// 8 outputs y[x0..x0+7] += sum_k Ks[k] Gr[x0 + k + (0..7)], k in [0, TP) step 4:
+// per step one broadcast LDS.128 of taps, one LDS.128 of new inputs, 32 FFMA.
+template <int TP>
+__device__ __forceinline__ void rc_dot8(const float* __restrict__ Ks, const float* __restrict__ Gr,
+                                        int tp_rt, float (&acc)[RC_OUT]) {
+  float w[12];
+  {
+    const float4 a = *reinterpret_cast<const float4*>(Gr);
+    const float4 b = *reinterpret_cast<const float4*>(Gr + 4);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+  }
+  const int tp = TP > 0 ? TP : tp_rt;
+#pragma unroll(TP > 0 ? TP / 4 : 2)
+  for (int k = 0; k < tp; k += 4) {
+    const float4 kq = *reinterpret_cast<const float4*>(Ks + k);
+    const float4 nq = *reinterpret_cast<const float4*>(Gr + k + 8);
+    w[8] = nq.x; w[9] = nq.y; w[10] = nq.z; w[11] = nq.w;
+    const float kk[4] = {kq.x, kq.y, kq.z, kq.w};
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+#pragma unroll
+      for (int r = 0; r < RC_OUT; ++r) acc[r] = fmaf(kk[d], w[r + d], acc[r]);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) w[r] = w[r + 4];
+  }
+}
+
+template <bool ADJ, int TP>
 __global__ void __launch_bounds__(RC_THREADS) rowconv_kernel(const float* __restrict__ in,
                                                              const float* __restrict__ K,
                                                              float* __restrict__ out,
                                                              int64_t batch, int nz, int nx,
                                                              int T, int rows, int Tp, int L) {
   extern __shared__ __align__(16) float sm[];
-  float* Ks = sm;        // [Tp + 4]
-  float* G = sm + Tp + 4;  // [rows][L], G[r][x + H] = in row r at x
+  float* Ks = sm;            // [Tp + 4]
+  float* G = sm + Tp + 4;    // [rows][L], G[r][x + H] = input row r at x
   const int i = blockIdx.x % nz;
   const int64_t b0 = (int64_t)(blockIdx.x / nz) * rows;
-  const int H = (T - 1) / 2;
-  for (int k = threadIdx.x; k < Tp + 4; k += blockDim.x) {
-    float v = 0.0f;
-    if (k < T) v = K[(int64_t)i * T + (ADJ ? (T - 1 - k) : k)];
-    Ks[k] = v;
-  }
   const int nrows = (int)((batch - b0) < (int64_t)rows ? (batch - b0) : (int64_t)rows);
-  const int nx4 = nx >> 2;
-  for (int r = 0; r < rows; ++r) {
-    float* Gr = G + r * L;
-    const float4* src = reinterpret_cast<const float4*>(in + ((b0 + r) * nz + i) * (int64_t)nx);
-    // body (16-byte aligned: H + 4q is a multiple of 4 only if H % 4 == 0, so store scalar)
-    for (int q = threadIdx.x; q < nx4; q += blockDim.x) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < nrows) v = src[q];
-      Gr[H + 4 * q + 0] = v.x;
-      Gr[H + 4 * q + 1] = v.y;
-      Gr[H + 4 * q + 2] = v.z;
-      Gr[H + 4 * q + 3] = v.w;
-    }
-    for (int e = threadIdx.x; e < L; e += blockDim.x)
-      if (e < H || e >= H + nx) Gr[e] = 0.0f;
-  }
+  rc_stage<ADJ>(in, K, Ks, G, i, b0, nrows, rows, nz, nx, T, Tp, L);
   __syncthreads();
-  const int quads = nrows * nx4;
-  for (int qi = threadIdx.x; qi < quads; qi += blockDim.x) {
-    const int r = qi / nx4;
-    const int x0 = (qi - r * nx4) * 4;
-    const float* Gr = G + r * L + x0;  // Gr[k + j] = input at x0 + j + k - H
-    float4 w = *reinterpret_cast<const float4*>(Gr);
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < Tp; k += 4) {
-      const float4 kq = *reinterpret_cast<const float4*>(Ks + k);
-      const float4 n = *reinterpret_cast<const float4*>(Gr + k + 4);
-      a0 = fmaf(kq.x, w.x, a0); a1 = fmaf(kq.x, w.y, a1); a2 = fmaf(kq.x, w.z, a2); a3 = fmaf(kq.x, w.w, a3);
-      a0 = fmaf(kq.y, w.y, a0); a1 = fmaf(kq.y, w.z, a1); a2 = fmaf(kq.y, w.w, a2); a3 = fmaf(kq.y, n.x, a3);
-      a0 = fmaf(kq.z, w.z, a0); a1 = fmaf(kq.z, w.w, a1); a2 = fmaf(kq.z, n.x, a2); a3 = fmaf(kq.z, n.y, a3);
-      a0 = fmaf(kq.w, w.w, a0); a1 = fmaf(kq.w, n.x, a1); a2 = fmaf(kq.w, n.y, a2); a3 = fmaf(kq.w, n.z, a3);
-      w = n;
-    }
+  const int per_row = nx / RC_OUT;
+  const int jobs = nrows * per_row;
+  for (int q = threadIdx.x; q < jobs; q += blockDim.x) {
+    const int r = q / per_row;
+    const int x0 = (q - r * per_row) * RC_OUT;
+    float acc[RC_OUT];
+#pragma unroll
+    for (int o = 0; o < RC_OUT; ++o) acc[o] = 0.0f;
+    rc_dot8<TP>(Ks, G + r * L + x0, Tp, acc);
     float4* dst = reinterpret_cast<float4*>(out + ((b0 + r) * nz + i) * (int64_t)nx + x0);
-    *dst = make_float4(a0, a1, a2, a3);
+    dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
 }
 
-// generic fallback for nx % 4 != 0 (one output per thread, taps from shared)
+// generic fallback for nx % 8 != 0 or unaligned maps (one output per thread)
 template <bool ADJ>
 __global__ void rowconv_generic_kernel(const float* __restrict__ in, const float* __restrict__ K,
                                        float* __restrict__ out, int64_t batch, int nz, int nx, int T) {
@@ -109,22 +136,20 @@ static int launch_rowconv(const float* in, const float* K, float* out, int64_t b
   TIDAS_REQUIRE(T >= 1 && (T & 1) && T <= 255, "taps must be odd and in [1, 255]");
   if (batch == 0 || nz == 0 || nx == 0) return TIDAS_OK;
   const bool aligned = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
-  if ((nx & 3) || !aligned) {
+  if ((nx & 7) || !aligned) {
     const int64_t total = batch * nz * (int64_t)nx;
     rowconv_generic_kernel<ADJ><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(in, K, out, batch, nz, nx, T);
     TIDAS_LAUNCH_CHECK();
     return TIDAS_OK;
   }
-  const int H = (T - 1) / 2;
   const int Tp = (T + 3) & ~3;
-  const int L = (nx + Tp + 8 + 3) & ~3;  // halo both sides + slack for the padded taps
-  // rows per CTA: ~1024 outputs per CTA pass
-  int rows = nx >= 1024 ? 1 : 1024 / nx;
+  const int L = (nx + Tp + 12 + 3) & ~3;  // halo both sides + slack for the padded taps
+  // rows per CTA: RC_THREADS * RC_OUT outputs per CTA pass
+  int rows = std::max(1, RC_THREADS * RC_OUT / nx);
   rows = (int)std::min<int64_t>(rows, batch);
   const size_t smem = sizeof(float) * ((size_t)Tp + 4 + (size_t)rows * L);
   TIDAS_REQUIRE(smem <= 200 * 1024, "row too long for the shared-memory row convolution");
-  (void)H;
-  auto kern = rowconv_kernel<ADJ>;
+  auto kern = (T == 129) ? rowconv_kernel<ADJ, 132> : rowconv_kernel<ADJ, 0>;
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t groups = (batch + rows - 1) / rows;
   const int64_t grid = groups * nz;
