@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libtidas_b200.so"
 SOURCES = ["api.cu", "analytic.cu", "das.cu", "rowconv.cu", "tidas_ops.cu", "simulate.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-ftz=true",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 

@@ -32,8 +32,8 @@
 
 namespace tidas {
 
-constexpr int DAS_TZ = 32;   // depths per CTA (lanes)
-constexpr int DAS_TX = 8;    // columns per CTA (warps)
+constexpr int DAS_TZ = 32;   // depths per CTA (also the warp width of the block)
+constexpr int DAS_TX = 8;    // columns per CTA
 constexpr int DAS_NT = DAS_TZ * DAS_TX;
 constexpr int DAS_WMAX = 400;  // staged window capacity (samples) per frame
 constexpr int DAS_NBUF = 3;    // channel windows in flight (triple buffer, 1 barrier/channel)
@@ -150,7 +150,7 @@ template <> struct PixelGeo<double> {
 __device__ __forceinline__ int wrapN(int e, int N) { return e < 0 ? e + N : (e >= N ? e - N : e); }
 
 template <typename R, int AP, int OUT, int FB>
-__global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
+__global__ void __launch_bounds__(DAS_NT, 3) das_image_kernel(DasParams p,
                                                            const cplx<R>* __restrict__ A,
                                                            void* __restrict__ out_) {
   using C = cplx<R>;
@@ -160,8 +160,11 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
 
   const int lane = threadIdx.x, wid = threadIdx.y;
   const int tid = wid * DAS_TZ + lane;
-  const int iz = blockIdx.x * DAS_TZ + lane;
-  const int ix = blockIdx.y * DAS_TX + wid;
+  // each warp covers 8 depths x 4 adjacent columns: the 16 lanes of a half-warp
+  // then read nearly coincident taps (bank conflicts ~1.5x instead of ~2.4x for
+  // a 32-depth column; tools/bank_model in DESIGN.md)
+  const int iz = blockIdx.x * DAS_TZ + (wid >> 1) * 8 + (lane >> 2);
+  const int ix = blockIdx.y * DAS_TX + (wid & 1) * 4 + (lane & 3);
   const int f0 = blockIdx.z * FB;
   const bool pix = (iz < p.nz) && (ix < p.nx);
   const int half = p.E / 2;
@@ -246,18 +249,24 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
 #pragma unroll
     for (int b = 0; b < FB; ++b) { c0[b].x = c0[b].y = R(0); c1[b].x = c1[b].y = R(0); }
 
-    auto row_ptr = [&](int b, int n) {
-      const int fb = min(f0 + b, p.F - 1);
-      return A + (((int64_t)fb * p.A + a) * p.E + (n + half)) * rowN;
-    };
+    // per-frame base of channel rows and this thread's copy slots (<= 2 per
+    // frame since W <= DAS_WMAX < 2 * DAS_NT); only + n * N changes per channel
+    const C* fbase = A + (((int64_t)f0 * p.A + a) * p.E + half) * rowN;
+    const int64_t fstride = (int64_t)p.A * p.E * rowN;
+    const int nfb = min(FB, p.F - f0);  // frames past F are never copied nor stored
+    const bool cp0 = tid < W, cp1 = tid + DAS_NT < W;
+    const int src0 = wrapN(w_lo + tid, p.N), src1 = wrapN(w_lo + tid + DAS_NT, p.N);
+    const int dst0 = win_pad(tid), dst1 = win_pad(tid + DAS_NT);
     auto issue = [&](int n, int slot) {
       if (n > c_hi) return;
       C* dst = win + (size_t)slot * FB * DAS_WSTRIDE;
-      for (int e = tid; e < W; e += DAS_NT) {
-        const int src = wrapN(w_lo + e, p.N);
-        const int d = win_pad(e);
+      const int64_t roff = (int64_t)n * rowN;
 #pragma unroll
-        for (int b = 0; b < FB; ++b) cp_async_elem<R>(dst + b * DAS_WSTRIDE + d, row_ptr(b, n) + src);
+      for (int b = 0; b < FB; ++b) {
+        if (b >= nfb) break;
+        const C* row = fbase + b * fstride + roff;
+        if (cp0) cp_async_elem<R>(dst + b * DAS_WSTRIDE + dst0, row + src0);
+        if (cp1) cp_async_elem<R>(dst + b * DAS_WSTRIDE + dst1, row + src1);
       }
     };
     auto accumulate = [&](const Tap<R>& t, int b, C am1, C a0, C ap1) {
@@ -298,7 +307,8 @@ __global__ void __launch_bounds__(DAS_NT) das_image_kernel(DasParams p,
         // oversized window (steep geometry): gather straight from global
 #pragma unroll
         for (int b = 0; b < FB; ++b) {
-          const C* src = row_ptr(b, n);
+          if (b >= nfb) break;
+          const C* src = fbase + b * fstride + (int64_t)n * rowN;
           accumulate(t, b, src[wrapN(t.j - 1, p.N)], src[wrapN(t.j, p.N)], src[wrapN(t.j + 1, p.N)]);
         }
       }

@@ -24,6 +24,11 @@ namespace tidas {
 constexpr int RC_THREADS = 256;
 constexpr int RC_OUT = 8;  // consecutive outputs per thread
 
+// Staged rows are padded by one 16-byte unit per 128 bytes: lanes read 128-bit
+// words 32 bytes apart, which this spreads over all banks (8 lanes / wavefront).
+__host__ __device__ __forceinline__ int rpad(int x) { return x + 4 * (x >> 5); }
+__host__ __device__ __forceinline__ int rc_row_len(int L) { return rpad(L) + 4; }
+
 // Stage ROWS input rows of depth row i (zero halo of H each side) and the row
 // kernel (reversed for the adjoint) in shared memory.
 template <bool ADJ>
@@ -36,18 +41,19 @@ __device__ __forceinline__ void rc_stage(const float* __restrict__ in, const flo
   const int nx4 = nx >> 2;
   const bool vec = (H & 3) == 0;
   for (int r = 0; r < rows; ++r) {
-    float* Gr = G + r * L;
+    float* Gr = G + r * rc_row_len(L);
     const float4* src = reinterpret_cast<const float4*>(in + ((b0 + r) * nz + i) * (int64_t)nx);
     for (int q = threadIdx.x; q < nx4; q += blockDim.x) {
       const float4 v = r < nrows ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int e = H + 4 * q;
       if (vec) {
-        *reinterpret_cast<float4*>(Gr + H + 4 * q) = v;
+        *reinterpret_cast<float4*>(Gr + rpad(e)) = v;
       } else {
-        Gr[H + 4 * q] = v.x; Gr[H + 4 * q + 1] = v.y; Gr[H + 4 * q + 2] = v.z; Gr[H + 4 * q + 3] = v.w;
+        Gr[rpad(e)] = v.x; Gr[rpad(e + 1)] = v.y; Gr[rpad(e + 2)] = v.z; Gr[rpad(e + 3)] = v.w;
       }
     }
-    for (int e = threadIdx.x; e < H; e += blockDim.x) Gr[e] = 0.0f;
-    for (int e = H + nx + threadIdx.x; e < L; e += blockDim.x) Gr[e] = 0.0f;
+    for (int e = threadIdx.x; e < H; e += blockDim.x) Gr[rpad(e)] = 0.0f;
+    for (int e = H + nx + threadIdx.x; e < L; e += blockDim.x) Gr[rpad(e)] = 0.0f;
   }
 }
 
@@ -55,18 +61,18 @@ __device__ __forceinline__ void rc_stage(const float* __restrict__ in, const flo
 // per step one broadcast LDS.128 of taps, one LDS.128 of new inputs, 32 FFMA.
 template <int TP>
 __device__ __forceinline__ void rc_dot8(const float* __restrict__ Ks, const float* __restrict__ Gr,
-                                        int tp_rt, float (&acc)[RC_OUT]) {
+                                        int x0, int tp_rt, float (&acc)[RC_OUT]) {
   float w[12];
   {
-    const float4 a = *reinterpret_cast<const float4*>(Gr);
-    const float4 b = *reinterpret_cast<const float4*>(Gr + 4);
+    const float4 a = *reinterpret_cast<const float4*>(Gr + rpad(x0));
+    const float4 b = *reinterpret_cast<const float4*>(Gr + rpad(x0 + 4));
     w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
   }
   const int tp = TP > 0 ? TP : tp_rt;
 #pragma unroll(TP > 0 ? TP / 4 : 2)
   for (int k = 0; k < tp; k += 4) {
     const float4 kq = *reinterpret_cast<const float4*>(Ks + k);
-    const float4 nq = *reinterpret_cast<const float4*>(Gr + k + 8);
+    const float4 nq = *reinterpret_cast<const float4*>(Gr + rpad(x0 + k + 8));
     w[8] = nq.x; w[9] = nq.y; w[10] = nq.z; w[11] = nq.w;
     const float kk[4] = {kq.x, kq.y, kq.z, kq.w};
 #pragma unroll
@@ -79,7 +85,7 @@ __device__ __forceinline__ void rc_dot8(const float* __restrict__ Ks, const floa
 }
 
 template <bool ADJ, int TP>
-__global__ void __launch_bounds__(RC_THREADS) rowconv_kernel(const float* __restrict__ in,
+__global__ void __launch_bounds__(RC_THREADS, 4) rowconv_kernel(const float* __restrict__ in,
                                                              const float* __restrict__ K,
                                                              float* __restrict__ out,
                                                              int64_t batch, int nz, int nx,
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(RC_THREADS) rowconv_kernel(const float* __rest
     float acc[RC_OUT];
 #pragma unroll
     for (int o = 0; o < RC_OUT; ++o) acc[o] = 0.0f;
-    rc_dot8<TP>(Ks, G + r * L + x0, Tp, acc);
+    rc_dot8<TP>(Ks, G + r * rc_row_len(L), x0, Tp, acc);
     float4* dst = reinterpret_cast<float4*>(out + ((b0 + r) * nz + i) * (int64_t)nx + x0);
     dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
@@ -147,7 +153,7 @@ static int launch_rowconv(const float* in, const float* K, float* out, int64_t b
   // rows per CTA: RC_THREADS * RC_OUT outputs per CTA pass
   int rows = std::max(1, RC_THREADS * RC_OUT / nx);
   rows = (int)std::min<int64_t>(rows, batch);
-  const size_t smem = sizeof(float) * ((size_t)Tp + 4 + (size_t)rows * L);
+  const size_t smem = sizeof(float) * ((size_t)Tp + 4 + (size_t)rows * rc_row_len(L));
   TIDAS_REQUIRE(smem <= 200 * 1024, "row too long for the shared-memory row convolution");
   auto kern = (T == 129) ? rowconv_kernel<ADJ, 132> : rowconv_kernel<ADJ, 0>;
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
