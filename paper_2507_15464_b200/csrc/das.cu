@@ -17,10 +17,14 @@
 //     for FB frames, so the time-of-flight math (FP32, cancellation-free
 //     s = -dx^2 / (sqrt(dx^2 + z^2) + z) in sample units) is paid once per
 //     (pixel, channel) and reused for FB frames.
-//   * Per channel the CTA's sample window (min..max tap over its 256 pixels,
-//     ~130-200 samples) is copied global->shared with cp.async, double-buffered
-//     one channel ahead, so the 3 taps per pixel are shared-memory reads and the
-//     8 columns reuse one window (lateral reuse of the same channel row).
+//   * The CTA's sample window per transmit (taps of its 256 pixels lie in
+//     [min k0 - 1, max (k0 - floor(s_min)) + 1], ~150-200 samples, the same for
+//     every channel) is copied global->shared per channel by TMA bulk copies
+//     (cp.async.bulk + mbarrier, one issuing thread), triple-buffered two
+//     channels ahead with one barrier per channel; the 3 taps per pixel are
+//     shared-memory reads and the tile's 8 columns reuse one window.
+//   * Warps cover 8 depths x 4 columns so the 16 lanes of a half-warp read
+//     nearly coincident taps (shared-memory wavefronts ~1.5x the minimum).
 //   * t* (one per pixel and transmit) is precomputed in float64 (plane-wave
 //     table kernel or the host's focused-transmit table) and split into an
 //     integer sample index plus an FP32 fraction — the FP32 ulp at index 8192
@@ -36,10 +40,9 @@ constexpr int DAS_TZ = 32;   // depths per CTA (also the warp width of the block
 constexpr int DAS_TX = 8;    // columns per CTA
 constexpr int DAS_NT = DAS_TZ * DAS_TX;
 constexpr int DAS_WMAX = 400;  // staged window capacity (samples) per frame
-constexpr int DAS_NBUF = 3;    // channel windows in flight (triple buffer, 1 barrier/channel)
+constexpr int DAS_NBUF = 4;    // channel windows in flight (producer up to 4 channels ahead)
 
-__host__ __device__ constexpr int win_pad(int p) { return p + (p >> 4); }
-constexpr int DAS_WSTRIDE = win_pad(DAS_WMAX) + 2;  // padded per-frame window stride
+constexpr int DAS_WSTRIDE = DAS_WMAX + 2;  // per-frame window stride (elements, even)
 
 struct DasParams {
   int F, A, E, N, nx, nz;
@@ -50,22 +53,26 @@ struct DasParams {
   const double* zg;
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+// ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-
-template <typename R> __device__ __forceinline__ void cp_async_elem(cplx<R>* s, const cplx<R>* g);
-template <> __device__ __forceinline__ void cp_async_elem<float>(float2* s, const float2* g) { cp_async8(s, g); }
-template <> __device__ __forceinline__ void cp_async_elem<double>(double2* s, const double2* g) { cp_async16(s, g); }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
 // Per-(pixel, channel) interpolation parameters: tap index j (C(k0) reads j, j-1;
 // C(k0+1) reads j+1, j) and the weights w (1 - mu), w mu.
@@ -149,24 +156,34 @@ template <> struct PixelGeo<double> {
 
 __device__ __forceinline__ int wrapN(int e, int N) { return e < 0 ? e + N : (e >= N ? e - N : e); }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised CTA: warps 0..7 own the 32 x 8 pixel tile (consumers),
+// warp 8 lane 0 streams the per-channel sample windows with TMA bulk copies
+// (producer). Buffer b is guarded by full[b] (copy landed, tx-count) and
+// empty[b] (all 8 consumer warps done); consumers never meet at a CTA barrier
+// inside the channel loop, so they drift up to DAS_NBUF channels apart.
 template <typename R, int AP, int OUT, int FB>
-__global__ void __launch_bounds__(DAS_NT, 3) das_image_kernel(DasParams p,
-                                                           const cplx<R>* __restrict__ A,
-                                                           void* __restrict__ out_) {
+__global__ void __launch_bounds__(DAS_NT + 32, 3) das_image_kernel(DasParams p,
+                                                                   const cplx<R>* __restrict__ A,
+                                                                   void* __restrict__ out_) {
   using C = cplx<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* win = reinterpret_cast<C*>(smem_raw);  // [DAS_NBUF][FB][DAS_WSTRIDE]
-  __shared__ int red[4];                    // channel range, tap window
+  __shared__ int red[6];                    // channel range; tap window (x2, by angle parity)
+  __shared__ __align__(8) uint64_t full[DAS_NBUF], empty[DAS_NBUF];
 
   const int lane = threadIdx.x, wid = threadIdx.y;
-  const int tid = wid * DAS_TZ + lane;
-  // each warp covers 8 depths x 4 adjacent columns: the 16 lanes of a half-warp
-  // then read nearly coincident taps (bank conflicts ~1.5x instead of ~2.4x for
-  // a 32-depth column; tools/bank_model in DESIGN.md)
+  const int tid = wid * 32 + lane;
+  const bool producer = wid == DAS_TX;
+  // each consumer warp covers 8 depths x 4 adjacent columns: the 16 lanes of a
+  // half-warp read nearly coincident taps (shared-memory wavefronts ~1.5x min)
   const int iz = blockIdx.x * DAS_TZ + (wid >> 1) * 8 + (lane >> 2);
   const int ix = blockIdx.y * DAS_TX + (wid & 1) * 4 + (lane & 3);
   const int f0 = blockIdx.z * FB;
-  const bool pix = (iz < p.nz) && (ix < p.nx);
+  const bool pix = !producer && (iz < p.nz) && (ix < p.nx);
   const int half = p.E / 2;
 
   const double x = pix ? p.xg[ix] : 0.0;
@@ -195,12 +212,21 @@ __global__ void __launch_bounds__(DAS_NT, 3) das_image_kernel(DasParams p,
                    fmax(fabs(((double)n_lo + 0.5) * p.pitch - x), fabs(((double)n_hi + 0.5) * p.pitch - x)));
     }
   }
-  // most negative receive shift of the pixel (samples): taps j = k0 - m lie in
-  // [k0, k0 - floor(s_min)] for every channel of its aperture
+  // most negative receive shift of the pixel (samples): its taps j = k0 - m lie
+  // in [k0, k0 - floor(s_min)] for every channel of the aperture
   const double s_min = (zm - hypot(dxmax, zm)) / p.c * p.fs;
   const int m_min = (int)floor(s_min) - 1;  // one sample of slack for FP32 rounding
 
-  if (tid == 0) { red[0] = INT_MAX; red[1] = INT_MIN; }
+  if (tid == 0) {
+    red[0] = INT_MAX;
+    red[1] = INT_MIN;
+#pragma unroll
+    for (int b = 0; b < DAS_NBUF; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], DAS_TX);
+    }
+    fence_mbar_init();
+  }
   __syncthreads();
   {
     const int wl = __reduce_min_sync(0xffffffffu, n_lo);
@@ -216,6 +242,7 @@ __global__ void __launch_bounds__(DAS_NT, 3) das_image_kernel(DasParams p,
   for (int b = 0; b < FB; ++b) { acc_env[b] = R(0); acc_iq[b].x = R(0); acc_iq[b].y = R(0); }
 
   const int64_t rowN = p.N;
+  unsigned g0 = 0;  // windows streamed before this transmit (buffer g % NBUF, use g / NBUF)
   for (int a = 0; a < p.A; ++a) {
     // arrival split into integer index + fraction in float64
     int k0 = 0;
@@ -231,107 +258,108 @@ __global__ void __launch_bounds__(DAS_NT, 3) das_image_kernel(DasParams p,
       }
     }
     const bool active_px = pix && vpos && n_lo <= n_hi;
-    // CTA tap window for this transmit (same for every channel)
-    if (tid == 0) { red[2] = INT_MAX; red[3] = INT_MIN; }
+    // CTA tap window of this transmit, the same for every channel
+    int* rw = red + 2 + 2 * (a & 1);
+    if (tid == 0) { rw[0] = INT_MAX; rw[1] = INT_MIN; }
     __syncthreads();
     {
       const int wl = __reduce_min_sync(0xffffffffu, active_px ? k0 - 1 : INT_MAX);
       const int wh = __reduce_max_sync(0xffffffffu, active_px ? k0 - m_min + 1 : INT_MIN);
-      if (lane == 0) { atomicMin(&red[2], wl); atomicMax(&red[3], wh); }
+      if (lane == 0) { atomicMin(&rw[0], wl); atomicMax(&rw[1], wh); }
     }
     __syncthreads();
-    const int w_lo = red[2], w_hi = red[3];
+    const int w_lo = rw[0], w_hi = rw[1];
     if (w_hi < w_lo || c_lo > c_hi) continue;  // CTA-uniform
     const int W = w_hi - w_lo + 1;
     const bool staged = W <= DAS_WMAX;
-
-    C c0[FB], c1[FB];
-#pragma unroll
-    for (int b = 0; b < FB; ++b) { c0[b].x = c0[b].y = R(0); c1[b].x = c1[b].y = R(0); }
-
-    // per-frame base of channel rows and this thread's copy slots (<= 2 per
-    // frame since W <= DAS_WMAX < 2 * DAS_NT); only + n * N changes per channel
+    // element e of a staged window is sample (s0 + e) mod N of the channel row
+    // (s0 even: every bulk copy is 16-byte aligned); per frame one or two
+    // (wrap-around) bulk copies
     const C* fbase = A + (((int64_t)f0 * p.A + a) * p.E + half) * rowN;
     const int64_t fstride = (int64_t)p.A * p.E * rowN;
     const int nfb = min(FB, p.F - f0);  // frames past F are never copied nor stored
-    const bool cp0 = tid < W, cp1 = tid + DAS_NT < W;
-    const int src0 = wrapN(w_lo + tid, p.N), src1 = wrapN(w_lo + tid + DAS_NT, p.N);
-    const int dst0 = win_pad(tid), dst1 = win_pad(tid + DAS_NT);
-    auto issue = [&](int n, int slot) {
-      if (n > c_hi) return;
-      C* dst = win + (size_t)slot * FB * DAS_WSTRIDE;
-      const int64_t roff = (int64_t)n * rowN;
-#pragma unroll
-      for (int b = 0; b < FB; ++b) {
-        if (b >= nfb) break;
-        const C* row = fbase + b * fstride + roff;
-        if (cp0) cp_async_elem<R>(dst + b * DAS_WSTRIDE + dst0, row + src0);
-        if (cp1) cp_async_elem<R>(dst + b * DAS_WSTRIDE + dst1, row + src1);
-      }
-    };
-    auto accumulate = [&](const Tap<R>& t, int b, C am1, C a0, C ap1) {
-      c0[b].x += t.w0 * a0.x + t.w1 * am1.x;
-      c0[b].y += t.w0 * a0.y + t.w1 * am1.y;
-      c1[b].x += t.w0 * ap1.x + t.w1 * a0.x;
-      c1[b].y += t.w0 * ap1.y + t.w1 * a0.y;
-    };
+    const int s0 = w_lo - (w_lo & 1);
+    const int Wc = ((w_hi - s0 + 1) + 1) & ~1;
+    const int n_ch = c_hi - c_lo + 1;
 
-    if (staged) {
-      issue(c_lo, 0);
-      cp_async_commit();
-      issue(c_lo + 1, 1);
-      cp_async_commit();
-    }
-    int slot = 0;
-    for (int n = c_lo; n <= c_hi; ++n) {
-      Tap<R> t;
-      bool in_ap = active_px && n >= n_lo && n <= n_hi;
-      if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
-      geo.template tap<AP>(p, n, k0, in_ap, t);
-      const bool live = in_ap && (t.w0 != R(0) || t.w1 != R(0));
-      if (staged) {
-        cp_async_wait<1>();
-        __syncthreads();  // window n resident for all; slot (n+2)%3 no longer read
-        issue(n + 2, slot == 0 ? 2 : slot - 1);
-        cp_async_commit();
-        if (live) {
-          const C* wb = win + (size_t)slot * FB * DAS_WSTRIDE;
-          const int e = t.j - w_lo;
-#pragma unroll
-          for (int b = 0; b < FB; ++b)
-            accumulate(t, b, wb[b * DAS_WSTRIDE + win_pad(e - 1)], wb[b * DAS_WSTRIDE + win_pad(e)],
-                       wb[b * DAS_WSTRIDE + win_pad(e + 1)]);
+    if (producer) {
+      if (staged && lane == 0) {
+        const int seg0 = s0 < 0 ? s0 + p.N : s0;
+        const int len0 = min(Wc, p.N - seg0);
+        const unsigned bytes = (unsigned)(nfb * Wc * sizeof(C));
+        for (int i = 0; i < n_ch; ++i) {
+          const unsigned g = g0 + i;
+          const int buf = (int)(g % DAS_NBUF);
+          const unsigned use = g / DAS_NBUF;
+          if (use > 0) mbar_wait(&empty[buf], (use - 1) & 1);
+          fence_proxy_async();
+          mbar_expect_tx(&full[buf], bytes);
+          C* dst = win + (size_t)buf * FB * DAS_WSTRIDE;
+          const C* row = fbase + (int64_t)(c_lo + i) * rowN;
+          for (int b = 0; b < nfb; ++b) {
+            const C* rb = row + b * fstride;
+            bulk_g2s(dst + b * DAS_WSTRIDE, rb + seg0, (unsigned)(len0 * sizeof(C)), &full[buf]);
+            if (len0 < Wc)
+              bulk_g2s(dst + b * DAS_WSTRIDE + len0, rb, (unsigned)((Wc - len0) * sizeof(C)), &full[buf]);
+          }
         }
-        slot = slot == DAS_NBUF - 1 ? 0 : slot + 1;
-      } else if (live) {
-        // oversized window (steep geometry): gather straight from global
+      }
+      __syncwarp();
+    } else {
+      C c0[FB], c1[FB];
+#pragma unroll
+      for (int b = 0; b < FB; ++b) { c0[b].x = c0[b].y = R(0); c1[b].x = c1[b].y = R(0); }
+      auto accumulate = [&](const Tap<R>& t, int b, C am1, C a0, C ap1) {
+        c0[b].x = fma(t.w1, am1.x, fma(t.w0, a0.x, c0[b].x));
+        c0[b].y = fma(t.w1, am1.y, fma(t.w0, a0.y, c0[b].y));
+        c1[b].x = fma(t.w1, a0.x, fma(t.w0, ap1.x, c1[b].x));
+        c1[b].y = fma(t.w1, a0.y, fma(t.w0, ap1.y, c1[b].y));
+      };
+      for (int i = 0; i < n_ch; ++i) {
+        const int n = c_lo + i;
+        Tap<R> t;
+        bool in_ap = active_px && n >= n_lo && n <= n_hi;
+        if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
+        geo.template tap<AP>(p, n, k0, in_ap, t);
+        const bool live = in_ap && (t.w0 != R(0) || t.w1 != R(0));
+        if (staged) {
+          const unsigned g = g0 + i;
+          const int buf = (int)(g % DAS_NBUF);
+          mbar_wait(&full[buf], (g / DAS_NBUF) & 1);
+          if (live) {
+            const C* wb = win + (size_t)buf * FB * DAS_WSTRIDE + (t.j - s0);
+#pragma unroll
+            for (int b = 0; b < FB; ++b)
+              if (b < nfb) accumulate(t, b, wb[b * DAS_WSTRIDE - 1], wb[b * DAS_WSTRIDE], wb[b * DAS_WSTRIDE + 1]);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[buf]);
+        } else if (live) {
+          // oversized window (steep geometry): gather straight from global
+#pragma unroll
+          for (int b = 0; b < FB; ++b) {
+            if (b >= nfb) break;
+            const C* src = fbase + b * fstride + (int64_t)n * rowN;
+            accumulate(t, b, src[wrapN(t.j - 1, p.N)], src[wrapN(t.j, p.N)], src[wrapN(t.j + 1, p.N)]);
+          }
+        }
+      }
+      if (active_px) {
 #pragma unroll
         for (int b = 0; b < FB; ++b) {
-          if (b >= nfb) break;
-          const C* src = fbase + b * fstride + (int64_t)n * rowN;
-          accumulate(t, b, src[wrapN(t.j - 1, p.N)], src[wrapN(t.j, p.N)], src[wrapN(t.j + 1, p.N)]);
+          if (OUT == TIDAS_OUT_ENVELOPE) {
+            // np.interp: fp[j] + (fp[j+1] - fp[j]) * f, exact fp[j] at f == 0
+            const R e0 = cabs_(c0[b]);
+            acc_env[b] += (fr == R(0)) ? e0 : e0 + (cabs_(c1[b]) - e0) * fr;
+          } else {
+            const R g = R(1) - fr;
+            acc_iq[b].x += g * c0[b].x + fr * c1[b].x;
+            acc_iq[b].y += g * c0[b].y + fr * c1[b].y;
+          }
         }
       }
     }
-    if (staged) {
-      cp_async_wait<0>();
-      __syncthreads();
-    }
-
-    if (active_px) {
-#pragma unroll
-      for (int b = 0; b < FB; ++b) {
-        if (OUT == TIDAS_OUT_ENVELOPE) {
-          // np.interp: fp[j] + (fp[j+1] - fp[j]) * f, exact fp[j] at f == 0
-          const R e0 = cabs_(c0[b]);
-          acc_env[b] += (fr == R(0)) ? e0 : e0 + (cabs_(c1[b]) - e0) * fr;
-        } else {
-          const R g = R(1) - fr;
-          acc_iq[b].x += g * c0[b].x + fr * c1[b].x;
-          acc_iq[b].y += g * c0[b].y + fr * c1[b].y;
-        }
-      }
-    }
+    if (staged) g0 += n_ch;
   }
 
   if (!pix) return;
@@ -367,7 +395,7 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
   auto kern = das_image_kernel<R, AP, OUT, FB>;
   const size_t smem = sizeof(C) * DAS_NBUF * FB * DAS_WSTRIDE;
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 block(DAS_TZ, DAS_TX);
+  dim3 block(32, DAS_TX + 1);  // 8 consumer warps + 1 producer warp
   dim3 grid((p.nz + DAS_TZ - 1) / DAS_TZ, (p.nx + DAS_TX - 1) / DAS_TX, (p.F + FB - 1) / FB);
   TIDAS_REQUIRE(grid.y <= 65535 && grid.z <= 65535, "pixel grid / frame batch too large");
   kern<<<grid, block, smem, st>>>(p, reinterpret_cast<const C*>(A), out);
