@@ -31,6 +31,7 @@
 //     would otherwise cost 1e-5 relative error.
 #include <math.h>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -40,7 +41,7 @@ constexpr int DAS_TZ = 32;   // depths per CTA (also the warp width of the block
 constexpr int DAS_TX = 8;    // columns per CTA
 constexpr int DAS_NT = DAS_TZ * DAS_TX;
 constexpr int DAS_WMAX = 400;  // staged window capacity (samples) per frame
-constexpr int DAS_NBUF = 4;    // channel windows in flight (producer up to 4 channels ahead)
+constexpr int DAS_NBUF_DEFAULT = 4;  // channel windows in flight (producer lead)
 
 constexpr int DAS_WSTRIDE = DAS_WMAX + 2;  // per-frame window stride (elements, even)
 
@@ -165,8 +166,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // (producer). Buffer b is guarded by full[b] (copy landed, tx-count) and
 // empty[b] (all 8 consumer warps done); consumers never meet at a CTA barrier
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
-template <typename R, int AP, int OUT, int FB>
-__global__ void __launch_bounds__(DAS_NT + 32, 3) das_image_kernel(DasParams p,
+template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false>
+__global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams p,
                                                                    const cplx<R>* __restrict__ A,
                                                                    void* __restrict__ out_) {
   using C = cplx<R>;
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(DAS_NT + 32, 3) das_image_kernel(DasParams p,
     const int w_lo = rw[0], w_hi = rw[1];
     if (w_hi < w_lo || c_lo > c_hi) continue;  // CTA-uniform
     const int W = w_hi - w_lo + 1;
-    const bool staged = W <= DAS_WMAX;
+    const bool staged = !DIRECT && W <= DAS_WMAX;
     // element e of a staged window is sample (s0 + e) mod N of the channel row
     // (s0 even: every bulk copy is 16-byte aligned); per frame one or two
     // (wrap-around) bulk copies
@@ -389,10 +390,10 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
   out[i] = (x[ix] * sn + z[iz] * cs + origin) / c + z[iz] / c;
 }
 
-template <typename R, int AP, int OUT, int FB>
+template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB>;
+  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT>;
   const size_t smem = sizeof(C) * DAS_NBUF * FB * DAS_WSTRIDE;
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 block(32, DAS_TX + 1);  // 8 consumer warps + 1 producer warp
@@ -406,10 +407,33 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // A fixed frame-batch width per precision (not chosen from F) keeps every
 // frame's arithmetic independent of how many frames share the launch, so
 // images are bit-identical under any batching or sharding.
+// Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
+//   0: FB 4, 4 buffers, 4 CTAs/SM (default)   1: FB 4, 6 buffers   2: FB 2, 8 buffers
+//   3: FB 8, 3 buffers   4: FB 4, no staging (L1 gathers)   5: FB 4, 4 buffers, 3 CTAs/SM
+//   6: FB 2, 4 buffers, 4 CTAs/SM
+//   7: FB 4, no staging, 4 CTAs/SM
+static int das_variant() {
+  static int v = [] {
+    const char* e = getenv("TIDAS_DAS_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
-  if (sizeof(R) == 8) return launch_das<R, AP, OUT, 1>(p, A, out, st);
-  return launch_das<R, AP, OUT, 4>(p, A, out, st);
+  if (sizeof(R) == 8) return launch_das<R, AP, OUT, 1, 4>(p, A, out, st);
+  switch (das_variant()) {
+    case 0: return launch_das<R, AP, OUT, 4, 4, 4>(p, A, out, st);  // measured best on B200 (cfg2)
+    case 1: return launch_das<R, AP, OUT, 4, 6>(p, A, out, st);
+    case 2: return launch_das<R, AP, OUT, 2, 8>(p, A, out, st);
+    case 3: return launch_das<R, AP, OUT, 8, 3>(p, A, out, st);
+    case 4: return launch_das<R, AP, OUT, 4, 1, 3, true>(p, A, out, st);
+    case 5: return launch_das<R, AP, OUT, 4, 4, 3>(p, A, out, st);
+    case 6: return launch_das<R, AP, OUT, 2, 4, 4>(p, A, out, st);
+    case 7: return launch_das<R, AP, OUT, 4, 1, 4, true>(p, A, out, st);
+    default: return launch_das<R, AP, OUT, 4, 4>(p, A, out, st);
+  }
 }
 
 template <typename R, int AP>

@@ -2,9 +2,9 @@
 
 ``DasPlan`` holds the frame-invariant geometry on the device (pixel grid,
 per-transmit arrival table t*, aperture), ``das_image`` runs K1 (RF ingest +
-analytic signal) and K2 (fused DAS) over a batch of frames. Frames are
-processed in chunks whose complex analytic RF stays resident in the 126 MB L2
-between the two kernels.
+analytic signal) and K2 (fused DAS) over a batch of frames, in chunks of up to
+256 MB of complex analytic RF (64 cfg2 frames) so each K2 launch spans many
+waves of CTAs.
 
 Semantics: the pixel value is the reference's das_value
 (das.py:181-193) — envelope of the dynamic-focus delayed sum at t*, two-tap
@@ -50,7 +50,7 @@ class DasPlan:
     prec: str = "f32"
     t0: float = 0.0
     ap_half: Optional[torch.Tensor] = None
-    chunk_bytes: int = 32 << 20
+    chunk_bytes: int = 256 << 20
     _desc: Optional[_lib.DasDesc] = field(default=None, repr=False)
 
     @property
@@ -174,7 +174,7 @@ def das_from_analytic(analytic: torch.Tensor, plan: DasPlan, out=None, stream=No
 
 
 class DasWorkspace:
-    """Reusable analytic-RF scratch for ``das_image`` (keeps a chunk L2-sized)."""
+    """Reusable analytic-RF scratch for ``das_image`` (one chunk of frames)."""
 
     def __init__(self, plan: DasPlan, device=None):
         self.plan = plan
