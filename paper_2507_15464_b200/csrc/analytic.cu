@@ -68,8 +68,8 @@ template <typename R> __device__ __forceinline__ cplx<R> spectral_op(cplx<R> v, 
 // bins), ifft(fft(x) h) = x + i IFFT(-i sgn(k) X)(k): the real part is the input
 // itself and the imaginary part uses the multiplier -i sgn(k) / N.
 // Delay mode (spectral fractional delay, one row per CTA): out = IFFT(X * ramp).
-template <typename R, typename In, bool DELAY>
-__global__ void __launch_bounds__(512, 1) analytic_pow2_kernel(const In* __restrict__ rf,
+template <typename R, typename In, bool DELAY, int EPT>
+__global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __restrict__ rf,
                                                             int64_t stride, R scale,
                                                             cplx<R>* __restrict__ out,
                                                             int64_t n_rows, int logN,
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(512, 1) analytic_pow2_kernel(const In* __restr
     if (lo_b < N) atomicMin(&first_nz[1], lo_b);
     if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
   }
-  fft_inplace<R, false>(s, logN);
+  fft_inplace<R, false, EPT>(s, logN);
   const R invN = R(1) / R(N);
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     C v = s[fpad(k)];
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(512, 1) analytic_pow2_kernel(const In* __restr
     s[fpad(k)] = v;
   }
   __syncthreads();
-  fft_inplace<R, true>(s, logN);
+  fft_inplace<R, true, EPT>(s, logN);
   C* dst_a = out + ra * (int64_t)N;
   C* dst_b = dst_a + N;
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
@@ -308,11 +308,15 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
     const size_t smem = sizeof(C) * (size_t)fft_smem_elems(N);
     TIDAS_REQUIRE(smem <= 227 * 1024, "n_samples=%d too long for the on-chip FFT at this precision", N);
     const bool delay = !isnan(shift);
-    auto kern = delay ? analytic_pow2_kernel<R, In, true> : analytic_pow2_kernel<R, In, false>;
+    // FP32: radix-8 passes, 8 elements per thread (<= 64 registers, 4 CTAs / SM);
+    // FP64: radix-16, 16 per thread (fewer passes; FP64 is the drop-in path)
+    constexpr int EPT = sizeof(R) == 4 ? 8 : 16;
+    auto kern = delay ? analytic_pow2_kernel<R, In, true, EPT> : analytic_pow2_kernel<R, In, false, EPT>;
     TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     const int64_t ctas = delay ? n_rows : (n_rows + 1) / 2;
-    kern<<<(unsigned)ctas, threads_for<R>(logN), smem, st>>>(rf, stride, (R)scale, reinterpret_cast<C*>(out),
+    TIDAS_REQUIRE((N / EPT) <= 1024, "n_samples=%d needs too many threads", N);
+    kern<<<(unsigned)ctas, N / EPT, smem, st>>>(rf, stride, (R)scale, reinterpret_cast<C*>(out),
                                                               n_rows, logN, support, shift);
     TIDAS_LAUNCH_CHECK();
     return TIDAS_OK;

@@ -138,16 +138,20 @@ template <int RADIX, typename C> __device__ __forceinline__ void apply_twiddle_p
   v[15] = cmul(v[15], cmul(w12, w3));
 }
 
-// One Stockham pass: N = blockDim * FFT_EPT, Ns = product of earlier radices.
-template <typename R, int RADIX, bool INV>
+// One Stockham pass: N = blockDim * EPT, Ns = product of earlier radices.
+// The group twiddles are fetched before the read barrier so their latency
+// overlaps the shared-memory reads.
+template <typename R, int RADIX, bool INV, int EPT>
 __device__ __forceinline__ void stockham_pass(cplx<R>* s, int N, int Ns, int tw_shift) {
   using C = cplx<R>;
-  constexpr int IT = FFT_EPT / RADIX;
+  constexpr int IT = EPT / RADIX;
   const int G = N / RADIX;
   C v[IT][RADIX];
+  C w[IT];
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const int j = threadIdx.x + it * blockDim.x;
+    if (Ns > 1) w[it] = twiddle<R>((j & (Ns - 1)) << tw_shift);  // exp(-2 pi i jm / (Ns R))
 #pragma unroll
     for (int r = 0; r < RADIX; ++r) v[it][r] = s[fpad(j + r * G)];
   }
@@ -157,9 +161,9 @@ __device__ __forceinline__ void stockham_pass(cplx<R>* s, int N, int Ns, int tw_
     const int j = threadIdx.x + it * blockDim.x;
     const int jm = j & (Ns - 1);
     if (Ns > 1) {
-      C w = twiddle<R>(jm << tw_shift);  // exp(-+ 2 pi i jm / (Ns R))
-      if (INV) w.y = -w.y;
-      apply_twiddle_powers<RADIX>(w, v[it]);
+      C wt = w[it];
+      if (INV) wt.y = -wt.y;
+      apply_twiddle_powers<RADIX>(wt, v[it]);
     }
     if (RADIX == 16) dft16<INV, R>(v[it]);
     if (RADIX == 8) dft8<INV, R>(v[it]);
@@ -174,19 +178,26 @@ __device__ __forceinline__ void stockham_pass(cplx<R>* s, int N, int Ns, int tw_
 }
 
 // Full in-place FFT of the padded s[0..2^logN) (unnormalised; INV: +i exponent).
-// Requires blockDim.x * FFT_EPT == 2^logN and logN <= FFT_MAX_LOG.
-template <typename R, bool INV>
+// Requires blockDim.x * EPT == 2^logN and logN <= FFT_MAX_LOG; radices up to EPT.
+template <typename R, bool INV, int EPT = FFT_EPT>
 __device__ __forceinline__ void fft_inplace(cplx<R>* s, int logN) {
   const int N = 1 << logN;
+  constexpr int MAXBITS = EPT == 16 ? 4 : 3;
   int done = 0;  // log2(Ns)
   while (done < logN) {
     const int left = logN - done;
-    const int rbits = left >= 4 ? 4 : left;
+    const int rbits = left >= MAXBITS ? MAXBITS : left;
     const int tw_shift = TW_LOG - (done + rbits);
-    if (rbits == 4) stockham_pass<R, 16, INV>(s, N, 1 << done, tw_shift);
-    else if (rbits == 3) stockham_pass<R, 8, INV>(s, N, 1 << done, tw_shift);
-    else if (rbits == 2) stockham_pass<R, 4, INV>(s, N, 1 << done, tw_shift);
-    else stockham_pass<R, 2, INV>(s, N, 1 << done, tw_shift);
+    if constexpr (EPT == 16) {
+      if (rbits == 4) {
+        stockham_pass<R, 16, INV, EPT>(s, N, 1 << done, tw_shift);
+        done += rbits;
+        continue;
+      }
+    }
+    if (rbits == 3) stockham_pass<R, 8, INV, EPT>(s, N, 1 << done, tw_shift);
+    else if (rbits == 2) stockham_pass<R, 4, INV, EPT>(s, N, 1 << done, tw_shift);
+    else stockham_pass<R, 2, INV, EPT>(s, N, 1 << done, tw_shift);
     done += rbits;
   }
 }
