@@ -45,6 +45,17 @@ CFG2 = dict(n_el=128, pitch=0.3e-3, f0=5e6, fs=40e6, c=1540.0, fbw=0.6, n_sample
 CFG4 = dict(nz=2048, nx=1024, taps=129, maps=256, density=0.02)
 
 
+def committed_traffic():
+    """DRAM bytes per frame of K1 + K2 from the committed ncu --set full capture
+    (profiles/*/traffic.json, written by tools/traffic_from_ncu.py), or None."""
+    for p in sorted(ROOT.glob("profiles/*/traffic.json"), reverse=True):
+        try:
+            return json.loads(p.read_text())
+        except (OSError, ValueError):
+            continue
+    return None
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -121,8 +132,11 @@ def frame_scatterers(cfg, frames, seed=2025):
     return sx, sz, a
 
 
-def cpu_baseline(budget_pixels: int, workers=None):
-    """Reference algorithm (oracle port) on a bounded pixel sample of one cfg2 frame."""
+def cpu_baseline(budget_pixels: int, workers=None, target_s: float = 0.0):
+    """Reference algorithm (oracle port) on a bounded pixel sample of one cfg2 frame.
+
+    With ``target_s`` > 0 a first small sample sizes a second one to about
+    ``target_s`` seconds of CPU work, which is the one reported."""
     from oracle import cpu_bench, geom, simulate as osim
     cfg = CFG2
     sx, sz, a = frame_scatterers(cfg, [0])
@@ -131,9 +145,12 @@ def cpu_baseline(budget_pixels: int, workers=None):
                          tx=("plane", 0.0)).astype(np.float32).astype(np.float64)
     x, z = grid(cfg)
     ts = geom.plane_wave_expected_arrival(x[None, :], z[:, None], 0.0, cfg["n_el"], cfg["pitch"], cfg["c"])
-    pps, n, dt, w = cpu_bench.pixels_per_second(rf, fs=cfg["fs"], c=cfg["c"], pitch=cfg["pitch"],
-                                                f_number=cfg["f_number"], x=x, z=z, t_star=ts,
-                                                n_pixels=budget_pixels, workers=workers)
+    kw = dict(fs=cfg["fs"], c=cfg["c"], pitch=cfg["pitch"], f_number=cfg["f_number"], x=x, z=z,
+              t_star=ts, workers=workers)
+    pps, n, dt, w = cpu_bench.pixels_per_second(rf, n_pixels=budget_pixels, **kw)
+    if target_s > 0:
+        n2 = int(min(max(budget_pixels, pps * target_s), cfg["nx"] * cfg["nz"]))
+        pps, n, dt, w = cpu_bench.pixels_per_second(rf, n_pixels=n2, seed=1, **kw)
     return pps / (cfg["nx"] * cfg["nz"]), n, dt, w
 
 
@@ -142,7 +159,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     workers = os.cpu_count() or 1
-    px_per_step = max(workers * 24, 64)
+    px_per_step = max(workers * 96, 256)
     vals = []
     for k in range(args.warmup + args.steps):
         fps, n, dt, w = cpu_baseline(px_per_step, workers)
@@ -261,8 +278,11 @@ def main():
     k2 = statistics.median(k2_ms)
     hbm, peak_kind = peaks()
     pipe_gbs = BYTES_PER_FRAME_CFG2 / ((k1 + k2) / 1e3) / 1e9
+    tr = committed_traffic()
+    traffic = tr["das_pipeline_bytes_per_frame"] * chunk if tr else None
     roofline = {"bound": "hbm", "achieved": pipe_gbs, "peak": hbm, "unit": "GB/s",
-                "frac": pipe_gbs / hbm, "traffic": None,
+                "frac": pipe_gbs / hbm, "traffic": traffic,
+                "traffic_source": tr.get("source") if tr else None,
                 "kernel": f"das pipeline per chunk of {chunk} frames: tidas_rf_analytic (K1) + "
                           "das_image_kernel (K2)",
                 "bytes_per_launch": BYTES_PER_FRAME_CFG2 * chunk, "peak_source": peak_kind,
@@ -359,7 +379,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
         n_px = args.cpu_pixels or max(workers * 48, 96)
-        fps, n, dt, w = cpu_baseline(n_px, workers)
+        fps, n, dt, w = cpu_baseline(n_px, workers, target_s=0.0 if args.cpu_pixels else 8.0)
         cpu = {"value": fps, "unit": "frames/s", "cores": w, "kind": "port",
                "sample": f"{n} seeded pixels of one cfg2 frame ({dt:.1f} s over {w} processes), "
                          "reference per-pixel algorithm (full-trace shifts + Hilbert), "
