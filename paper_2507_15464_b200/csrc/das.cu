@@ -102,14 +102,20 @@ template <> struct PixelGeo<float> {
     nref = nr;
     dxref = (float)((((double)nr + 0.5) * p.pitch - x) * k);
   }
+  // dn = n - nref as a float (the caller steps it by 1.0f per channel, exact)
   template <int AP>
-  __device__ __forceinline__ void tap(const DasParams&, int n, int k0, bool in_ap, Tap<float>& t) const {
-    const float dx = fmaf((float)(n - nref), pitch, dxref);  // x_n - x
+  __device__ __forceinline__ void tap(const DasParams&, float dn, int k0, bool in_ap, Tap<float>& t) const {
+    const float dx = fmaf(dn, pitch, dxref);  // x_n - x
     const float q = dx * dx;
     const float rr = q + z2;
     const float r = rr * rsqrtf(rr);
-    const float s = -__fdividef(q, r + z);  // D_n fs, cancellation-free
-    const float m = floorf(s);
+    const float s = -__fdividef(q, r + z);  // D_n fs, cancellation-free, |s| < 2^22
+    // floor(s) on the FMA/ALU pipes instead of FRND + F2I (XU): round to the
+    // nearest integer with the 1.5 * 2^23 magic constant, step down if above s
+    const float tb = s + 12582912.0f;
+    int mi = __float_as_int(tb) - 0x4B400000;
+    float m = tb - 12582912.0f;
+    if (m > s) { m -= 1.0f; --mi; }
     const float mu = s - m;
     float w;
     if (AP == TIDAS_AP_HANN) {
@@ -118,7 +124,7 @@ template <> struct PixelGeo<float> {
       w = 1.0f;
     }
     w = in_ap ? w : 0.0f;
-    t.j = k0 - (int)m;
+    t.j = k0 - mi;
     t.w1 = w * mu;
     t.w0 = w - t.w1;
   }
@@ -316,12 +322,15 @@ __global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams 
         c1[b].x = fma(t.w1, a0.x, fma(t.w0, ap1.x, c1[b].x));
         c1[b].y = fma(t.w1, a0.y, fma(t.w0, ap1.y, c1[b].y));
       };
-      for (int i = 0; i < n_ch; ++i) {
+      float dnf = 0.0f;
+      if constexpr (sizeof(R) == 4) dnf = (float)(c_lo - geo.nref);
+      for (int i = 0; i < n_ch; ++i, dnf += 1.0f) {
         const int n = c_lo + i;
         Tap<R> t;
         bool in_ap = active_px && n >= n_lo && n <= n_hi;
         if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
-        geo.template tap<AP>(p, n, k0, in_ap, t);
+        if constexpr (sizeof(R) == 4) geo.template tap<AP>(p, dnf, k0, in_ap, t);
+        else geo.template tap<AP>(p, n, k0, in_ap, t);
         const bool live = in_ap && (t.w0 != R(0) || t.w1 != R(0));
         if (staged) {
           const unsigned g = g0 + i;
@@ -329,9 +338,15 @@ __global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams 
           mbar_wait(&full[buf], (g / DAS_NBUF) & 1);
           if (live) {
             const C* wb = win + (size_t)buf * FB * DAS_WSTRIDE + (t.j - s0);
+            if (nfb == FB) {  // CTA-uniform: no per-frame bounds in the common case
 #pragma unroll
-            for (int b = 0; b < FB; ++b)
-              if (b < nfb) accumulate(t, b, wb[b * DAS_WSTRIDE - 1], wb[b * DAS_WSTRIDE], wb[b * DAS_WSTRIDE + 1]);
+              for (int b = 0; b < FB; ++b)
+                accumulate(t, b, wb[b * DAS_WSTRIDE - 1], wb[b * DAS_WSTRIDE], wb[b * DAS_WSTRIDE + 1]);
+            } else {
+#pragma unroll
+              for (int b = 0; b < FB; ++b)
+                if (b < nfb) accumulate(t, b, wb[b * DAS_WSTRIDE - 1], wb[b * DAS_WSTRIDE], wb[b * DAS_WSTRIDE + 1]);
+            }
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[buf]);
@@ -410,7 +425,7 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
 //   0: FB 4, 4 buffers, 4 CTAs/SM (default)   1: FB 4, 6 buffers   2: FB 2, 8 buffers
 //   3: FB 8, 3 buffers   4: FB 4, no staging (L1 gathers)   5: FB 4, 4 buffers, 3 CTAs/SM
-//   6: FB 2, 4 buffers, 4 CTAs/SM
+//   6: FB 2, 4 buffers, 4 CTAs/SM   8: FB 8, 4 buffers, 2 CTAs/SM
 //   7: FB 4, no staging, 4 CTAs/SM
 static int das_variant() {
   static int v = [] {
@@ -432,6 +447,7 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
     case 5: return launch_das<R, AP, OUT, 4, 4, 3>(p, A, out, st);
     case 6: return launch_das<R, AP, OUT, 2, 4, 4>(p, A, out, st);
     case 7: return launch_das<R, AP, OUT, 4, 1, 4, true>(p, A, out, st);
+    case 8: return launch_das<R, AP, OUT, 8, 4, 2>(p, A, out, st);
     default: return launch_das<R, AP, OUT, 4, 4>(p, A, out, st);
   }
 }
