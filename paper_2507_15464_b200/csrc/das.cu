@@ -29,17 +29,17 @@
 //     table kernel or the host's focused-transmit table) and split into an
 //     integer sample index plus an FP32 fraction — the FP32 ulp at index 8192
 //     would otherwise cost 1e-5 relative error.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
 namespace tidas {
 
-constexpr int DAS_TZ = 32;   // depths per CTA (also the warp width of the block)
-constexpr int DAS_TX = 8;    // columns per CTA
-constexpr int DAS_NT = DAS_TZ * DAS_TX;
 constexpr int DAS_WMAX = 400;  // staged window capacity (samples) per frame
 constexpr int DAS_NBUF_DEFAULT = 4;  // channel windows in flight (producer lead)
 
@@ -66,11 +66,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware until
+// the phase completes (or the hint expires) instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
-      "WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity), "r"(1000000u) : "memory");
+}
+// one TMA tensor copy: box [FB frames][1 transmit][1 channel][256 samples] of the
+// 4-D analytic tensor [F][A][E][N] (complex64 as 8-byte elements)
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
@@ -118,12 +129,11 @@ template <> struct PixelGeo<float> {
     if (m > s) { m -= 1.0f; --mi; }
     const float mu = s - m;
     float w;
-    if (AP == TIDAS_AP_HANN) {
+    if (AP == TIDAS_AP_HANN) {  // |dx| < a also encodes the aperture and pixel activity
       w = (fabsf(dx) < a) ? fmaf(0.5f, __cosf(dx * pia), 0.5f) : 0.0f;
     } else {
-      w = 1.0f;
+      w = in_ap ? 1.0f : 0.0f;
     }
-    w = in_ap ? w : 0.0f;
     t.j = k0 - mi;
     t.w1 = w * mu;
     t.w0 = w - t.w1;
@@ -166,29 +176,44 @@ __device__ __forceinline__ int wrapN(int e, int N) { return e < 0 ? e + N : (e >
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// shared-window (u32) address forms, hoisted out of the channel loop
+__device__ __forceinline__ void mbar_arrive_u32(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity), "r"(1000000u) : "memory");
+}
 
 // Warp-specialised CTA: warps 0..7 own the 32 x 8 pixel tile (consumers),
 // warp 8 lane 0 streams the per-channel sample windows with TMA bulk copies
 // (producer). Buffer b is guarded by full[b] (copy landed, tx-count) and
 // empty[b] (all 8 consumer warps done); consumers never meet at a CTA barrier
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
-template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false>
-__global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams p,
+template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
+          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false>
+__global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams p,
                                                                    const cplx<R>* __restrict__ A,
-                                                                   void* __restrict__ out_) {
+                                                                   void* __restrict__ out_,
+                                                                   const __grid_constant__ CUtensorMap tmap) {
   using C = cplx<R>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int DAS_WSTRIDE = WCAP + 2;  // per-frame window stride (elements, even)
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   C* win = reinterpret_cast<C*>(smem_raw);  // [DAS_NBUF][FB][DAS_WSTRIDE]
   __shared__ int red[6];                    // channel range; tap window (x2, by angle parity)
   __shared__ __align__(8) uint64_t full[DAS_NBUF], empty[DAS_NBUF];
 
   const int lane = threadIdx.x, wid = threadIdx.y;
   const int tid = wid * 32 + lane;
-  const bool producer = wid == DAS_TX;
+  const bool producer = wid == NW;  // NW consumer warps, then the producer warp
   // each consumer warp covers 8 depths x 4 adjacent columns: the 16 lanes of a
-  // half-warp read nearly coincident taps (shared-memory wavefronts ~1.5x min)
-  const int iz = blockIdx.x * DAS_TZ + (wid >> 1) * 8 + (lane >> 2);
-  const int ix = blockIdx.y * DAS_TX + (wid & 1) * 4 + (lane & 3);
+  // half-warp read nearly coincident taps (shared-memory wavefronts ~1.5x min);
+  // the CTA is DG depth groups x (8 / DG) column groups of warps
+  constexpr int CG = NW / DG;
+  const int iz = blockIdx.x * (8 * DG) + (wid / CG) * 8 + (lane >> 2);
+  const int ix = blockIdx.y * (4 * CG) + (wid % CG) * 4 + (lane & 3);
   const int f0 = blockIdx.z * FB;
   const bool pix = !producer && (iz < p.nz) && (ix < p.nx);
   const int half = p.E / 2;
@@ -230,7 +255,7 @@ __global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams 
 #pragma unroll
     for (int b = 0; b < DAS_NBUF; ++b) {
       mbar_init(&full[b], 1);
-      mbar_init(&empty[b], DAS_TX);
+      mbar_init(&empty[b], NW);  // one arrival per consumer warp
     }
     fence_mbar_init();
   }
@@ -278,7 +303,7 @@ __global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams 
     const int w_lo = rw[0], w_hi = rw[1];
     if (w_hi < w_lo || c_lo > c_hi) continue;  // CTA-uniform
     const int W = w_hi - w_lo + 1;
-    const bool staged = !DIRECT && W <= DAS_WMAX;
+    const bool staged = !DIRECT && W <= WCAP;
     // element e of a staged window is sample (s0 + e) mod N of the channel row
     // (s0 even: every bulk copy is 16-byte aligned); per frame one or two
     // (wrap-around) bulk copies
@@ -290,20 +315,28 @@ __global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams 
     const int n_ch = c_hi - c_lo + 1;
 
     if (producer) {
-      if (staged && lane == 0) {
+      if (staged && lane == 0 && DIAG != 1) {
         const int seg0 = s0 < 0 ? s0 + p.N : s0;
         const int len0 = min(Wc, p.N - seg0);
         const unsigned bytes = (unsigned)(nfb * Wc * sizeof(C));
+        // one tensor copy per channel when the window does not wrap around the row
+        const bool tensor = TMAP && s0 >= 0 && s0 + Wc <= p.N;
         for (int i = 0; i < n_ch; ++i) {
           const unsigned g = g0 + i;
           const int buf = (int)(g % DAS_NBUF);
           const unsigned use = g / DAS_NBUF;
           if (use > 0) mbar_wait(&empty[buf], (use - 1) & 1);
-          fence_proxy_async();
-          mbar_expect_tx(&full[buf], bytes);
+          if (DIAG == 4) { mbar_arrive(&full[buf]); continue; }  // diag: no copy at all
+          if (tensor) {
+            mbar_expect_tx(&full[buf], (unsigned)(FB * DAS_WSTRIDE * sizeof(C)));
+            tma_load_4d(win + (size_t)buf * FB * DAS_WSTRIDE, &tmap, s0, c_lo + i + half, a, f0, &full[buf]);
+            continue;
+          }
+          const int ncopy = DIAG == 3 ? 1 : nfb;                    // diag: one frame only
+          mbar_expect_tx(&full[buf], DIAG == 3 ? (unsigned)(Wc * sizeof(C)) : bytes);
           C* dst = win + (size_t)buf * FB * DAS_WSTRIDE;
           const C* row = fbase + (int64_t)(c_lo + i) * rowN;
-          for (int b = 0; b < nfb; ++b) {
+          for (int b = 0; b < ncopy; ++b) {
             const C* rb = row + b * fstride;
             bulk_g2s(dst + b * DAS_WSTRIDE, rb + seg0, (unsigned)(len0 * sizeof(C)), &full[buf]);
             if (len0 < Wc)
@@ -323,21 +356,33 @@ __global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams 
         c1[b].y = fma(t.w1, a0.y, fma(t.w0, ap1.y, c1[b].y));
       };
       float dnf = 0.0f;
-      if constexpr (sizeof(R) == 4) dnf = (float)(c_lo - geo.nref);
+      if constexpr (sizeof(R) == 4) {
+        dnf = (float)(c_lo - geo.nref);
+        if (AP == TIDAS_AP_HANN && !active_px) geo.a = -1.0f;  // no tap passes |dx| < a
+      }
+      // channels outside every lane's aperture skip the tap math (warp-uniform)
+      const int wn_lo = __reduce_min_sync(0xffffffffu, active_px ? n_lo : INT_MAX);
+      const int wn_hi = __reduce_max_sync(0xffffffffu, active_px ? n_hi : INT_MIN);
+      const unsigned full_u = smem_u32(&full[0]), empty_u = smem_u32(&empty[0]);
+      const C* win_lane = win - s0;  // + buf * FB * WSTRIDE + j
       for (int i = 0; i < n_ch; ++i, dnf += 1.0f) {
         const int n = c_lo + i;
         Tap<R> t;
-        bool in_ap = active_px && n >= n_lo && n <= n_hi;
-        if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
-        if constexpr (sizeof(R) == 4) geo.template tap<AP>(p, dnf, k0, in_ap, t);
-        else geo.template tap<AP>(p, n, k0, in_ap, t);
-        const bool live = in_ap && (t.w0 != R(0) || t.w1 != R(0));
+        bool live = false;
+        if (DIAG < 2 && n >= wn_lo && n <= wn_hi) {
+          bool in_ap = true;
+          if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
+          if (sizeof(R) == 8) in_ap = in_ap && active_px && n >= n_lo && n <= n_hi;
+          if constexpr (sizeof(R) == 4) geo.template tap<AP>(p, dnf, k0, in_ap, t);
+          else geo.template tap<AP>(p, n, k0, in_ap, t);
+          live = (t.w0 != R(0) || t.w1 != R(0));
+        }
         if (staged) {
           const unsigned g = g0 + i;
           const int buf = (int)(g % DAS_NBUF);
-          mbar_wait(&full[buf], (g / DAS_NBUF) & 1);
+          if (DIAG != 1) mbar_wait_u32(full_u + 8u * buf, (g / DAS_NBUF) & 1);
           if (live) {
-            const C* wb = win + (size_t)buf * FB * DAS_WSTRIDE + (t.j - s0);
+            const C* wb = win_lane + (size_t)buf * FB * DAS_WSTRIDE + t.j;
             if (nfb == FB) {  // CTA-uniform: no per-frame bounds in the common case
 #pragma unroll
               for (int b = 0; b < FB; ++b)
@@ -349,7 +394,7 @@ __global__ void __launch_bounds__(DAS_NT + 32, MINB) das_image_kernel(DasParams 
             }
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[buf]);
+          if (DIAG != 1 && lane == 0) mbar_arrive_u32(empty_u + 8u * buf);
         } else if (live) {
           // oversized window (steep geometry): gather straight from global
 #pragma unroll
@@ -405,16 +450,38 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
   out[i] = (x[ix] * sn + z[iz] * cs + origin) / c + z[iz] / c;
 }
 
-template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false>
+template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
+          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT>;
-  const size_t smem = sizeof(C) * DAS_NBUF * FB * DAS_WSTRIDE;
+  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP>;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (TMAP) {
+    static_assert(!TMAP || (sizeof(C) == 8 && WCAP + 2 <= 256), "tensor path: complex64, box <= 256");
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      TIDAS_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q));
+      TIDAS_REQUIRE(q == cudaDriverEntryPointSuccess && encode, "cuTensorMapEncodeTiled unavailable");
+    }
+    const cuuint64_t dims[4] = {(cuuint64_t)p.N, (cuuint64_t)p.E, (cuuint64_t)p.A, (cuuint64_t)p.F};
+    const cuuint64_t strides[3] = {(cuuint64_t)p.N * 8, (cuuint64_t)p.E * p.N * 8,
+                                   (cuuint64_t)p.A * p.E * p.N * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)(WCAP + 2), 1, 1, (cuuint32_t)FB};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(A), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    TIDAS_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  }
+  const size_t smem = sizeof(C) * DAS_NBUF * FB * (WCAP + 2);
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 block(32, DAS_TX + 1);  // 8 consumer warps + 1 producer warp
-  dim3 grid((p.nz + DAS_TZ - 1) / DAS_TZ, (p.nx + DAS_TX - 1) / DAS_TX, (p.F + FB - 1) / FB);
+  dim3 block(32, NW + 1);  // NW consumer warps + 1 producer warp
+  constexpr int TZ = 8 * DG, TXC = 4 * (NW / DG);
+  dim3 grid((p.nz + TZ - 1) / TZ, (p.nx + TXC - 1) / TXC, (p.F + FB - 1) / FB);
   TIDAS_REQUIRE(grid.y <= 65535 && grid.z <= 65535, "pixel grid / frame batch too large");
-  kern<<<grid, block, smem, st>>>(p, reinterpret_cast<const C*>(A), out);
+  kern<<<grid, block, smem, st>>>(p, reinterpret_cast<const C*>(A), out, tmap);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
 }
@@ -423,9 +490,10 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // frame's arithmetic independent of how many frames share the launch, so
 // images are bit-identical under any batching or sharding.
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
-//   0: FB 4, 4 buffers, 4 CTAs/SM (default)   1: FB 4, 6 buffers   2: FB 2, 8 buffers
+//   0: FB 4, 4 buffers, 4 CTAs/SM, TMA tensor windows (default)   27: same with bulk copies   1: FB 4, 6 buffers   2: FB 2, 8 buffers
 //   3: FB 8, 3 buffers   4: FB 4, no staging (L1 gathers)   5: FB 4, 4 buffers, 3 CTAs/SM
 //   6: FB 2, 4 buffers, 4 CTAs/SM   8: FB 8, 4 buffers, 2 CTAs/SM
+//   9/10/11: variant 0 with a 16x16 / 8x32 / 64x4 (depth x column) tile
 //   7: FB 4, no staging, 4 CTAs/SM
 static int das_variant() {
   static int v = [] {
@@ -439,7 +507,9 @@ template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   if (sizeof(R) == 8) return launch_das<R, AP, OUT, 1, 4>(p, A, out, st);
   switch (das_variant()) {
-    case 0: return launch_das<R, AP, OUT, 4, 4, 4>(p, A, out, st);  // measured best on B200 (cfg2)
+    case 0:  // measured best on B200 (cfg2): TMA tensor windows, 4 buffers, 4 CTAs/SM
+      return launch_das<R, AP, OUT, 4, 4, 4, false, 4, 254, 0, 8, sizeof(R) == 4>(p, A, out, st);
+    case 27: return launch_das<R, AP, OUT, 4, 4, 4>(p, A, out, st);  // previous default (bulk copies)
     case 1: return launch_das<R, AP, OUT, 4, 6>(p, A, out, st);
     case 2: return launch_das<R, AP, OUT, 2, 8>(p, A, out, st);
     case 3: return launch_das<R, AP, OUT, 8, 3>(p, A, out, st);
@@ -448,6 +518,24 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
     case 6: return launch_das<R, AP, OUT, 2, 4, 4>(p, A, out, st);
     case 7: return launch_das<R, AP, OUT, 4, 1, 4, true>(p, A, out, st);
     case 8: return launch_das<R, AP, OUT, 8, 4, 2>(p, A, out, st);
+    case 9: return launch_das<R, AP, OUT, 4, 4, 4, false, 2>(p, A, out, st);
+    case 10: return launch_das<R, AP, OUT, 4, 4, 4, false, 1>(p, A, out, st);
+    case 11: return launch_das<R, AP, OUT, 4, 4, 4, false, 8>(p, A, out, st);
+    case 12: return launch_das<R, AP, OUT, 4, 8, 4, false, 4, 208>(p, A, out, st);
+    case 13: return launch_das<R, AP, OUT, 4, 6, 4, false, 4, 208>(p, A, out, st);
+    case 14: return launch_das<R, AP, OUT, 4, 8, 4, false, 2, 208>(p, A, out, st);
+    case 15: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, DAS_WMAX, 1>(p, A, out, st);  // diag: compute only
+    case 16: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, DAS_WMAX, 2>(p, A, out, st);  // diag: data only
+    case 17: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, DAS_WMAX, 0, 16>(p, A, out, st);  // 32 x 16 tile
+    case 18: return launch_das<R, AP, OUT, 4, 4, 2, false, 2, DAS_WMAX, 0, 16>(p, A, out, st);  // 16 x 32 tile
+    case 19: return launch_das<R, AP, OUT, 4, 4, 1, false, 4, DAS_WMAX, 0, 32>(p, A, out, st);  // 32 x 32 tile
+    case 20: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, DAS_WMAX, 2, 16>(p, A, out, st);  // diag data-only 32x16
+    case 21: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, DAS_WMAX, 3>(p, A, out, st);  // diag: data-only, 1 copy
+    case 22: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, DAS_WMAX, 4>(p, A, out, st);  // diag: barriers only
+    case 23: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, 254, 0, 8, sizeof(R) == 4>(p, A, out, st);  // TMA tensor
+    case 24: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, 254, 2, 8, sizeof(R) == 4>(p, A, out, st);  // ... data only
+    case 25: return launch_das<R, AP, OUT, 4, 6, 4, false, 4, 254, 0, 8, sizeof(R) == 4>(p, A, out, st);
+    case 26: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, sizeof(R) == 4>(p, A, out, st);
     default: return launch_das<R, AP, OUT, 4, 4>(p, A, out, st);
   }
 }
