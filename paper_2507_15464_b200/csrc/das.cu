@@ -193,7 +193,7 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
 // empty[b] (all 8 consumer warps done); consumers never meet at a CTA barrier
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
-          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false>
+          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1>
 __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams p,
                                                                    const cplx<R>* __restrict__ A,
                                                                    void* __restrict__ out_,
@@ -314,33 +314,40 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
     const int Wc = ((w_hi - s0 + 1) + 1) & ~1;
     const int n_ch = c_hi - c_lo + 1;
 
+    // channel blocks of CPB channels share one buffer (one TMA box, one wait)
+    const int n_blk = (n_ch + CPB - 1) / CPB;
+    constexpr int SLOT = FB * CPB * DAS_WSTRIDE;  // elements per buffer: [FB][CPB][WSTRIDE]
+
     if (producer) {
       if (staged && lane == 0 && DIAG != 1) {
         const int seg0 = s0 < 0 ? s0 + p.N : s0;
         const int len0 = min(Wc, p.N - seg0);
-        const unsigned bytes = (unsigned)(nfb * Wc * sizeof(C));
-        // one tensor copy per channel when the window does not wrap around the row
+        // one tensor copy per block when the window does not wrap around the row
         const bool tensor = TMAP && s0 >= 0 && s0 + Wc <= p.N;
-        for (int i = 0; i < n_ch; ++i) {
-          const unsigned g = g0 + i;
+        for (int kb = 0; kb < n_blk; ++kb) {
+          const unsigned g = g0 + kb;
           const int buf = (int)(g % DAS_NBUF);
           const unsigned use = g / DAS_NBUF;
           if (use > 0) mbar_wait(&empty[buf], (use - 1) & 1);
+          const int n0 = c_lo + kb * CPB;
+          C* dst = win + (size_t)buf * SLOT;
           if (DIAG == 4) { mbar_arrive(&full[buf]); continue; }  // diag: no copy at all
           if (tensor) {
-            mbar_expect_tx(&full[buf], (unsigned)(FB * DAS_WSTRIDE * sizeof(C)));
-            tma_load_4d(win + (size_t)buf * FB * DAS_WSTRIDE, &tmap, s0, c_lo + i + half, a, f0, &full[buf]);
+            mbar_expect_tx(&full[buf], (unsigned)(SLOT * sizeof(C)));
+            tma_load_4d(dst, &tmap, s0, n0 + half, a, f0, &full[buf]);
             continue;
           }
-          const int ncopy = DIAG == 3 ? 1 : nfb;                    // diag: one frame only
-          mbar_expect_tx(&full[buf], DIAG == 3 ? (unsigned)(Wc * sizeof(C)) : bytes);
-          C* dst = win + (size_t)buf * FB * DAS_WSTRIDE;
-          const C* row = fbase + (int64_t)(c_lo + i) * rowN;
-          for (int b = 0; b < ncopy; ++b) {
-            const C* rb = row + b * fstride;
-            bulk_g2s(dst + b * DAS_WSTRIDE, rb + seg0, (unsigned)(len0 * sizeof(C)), &full[buf]);
-            if (len0 < Wc)
-              bulk_g2s(dst + b * DAS_WSTRIDE + len0, rb, (unsigned)((Wc - len0) * sizeof(C)), &full[buf]);
+          const int nc = min(CPB, c_hi - n0 + 1);
+          const int ncopy = DIAG == 3 ? 1 : nfb;  // diag: one frame only
+          mbar_expect_tx(&full[buf], (unsigned)(nc * ncopy * Wc * sizeof(C)));
+          for (int c = 0; c < nc; ++c) {
+            const C* row = fbase + (int64_t)(n0 + c) * rowN;
+            for (int b = 0; b < ncopy; ++b) {
+              const C* rb = row + b * fstride;
+              C* d = dst + (b * CPB + c) * DAS_WSTRIDE;
+              bulk_g2s(d, rb + seg0, (unsigned)(len0 * sizeof(C)), &full[buf]);
+              if (len0 < Wc) bulk_g2s(d + len0, rb, (unsigned)((Wc - len0) * sizeof(C)), &full[buf]);
+            }
           }
         }
       }
@@ -364,45 +371,54 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
       const int wn_lo = __reduce_min_sync(0xffffffffu, active_px ? n_lo : INT_MAX);
       const int wn_hi = __reduce_max_sync(0xffffffffu, active_px ? n_hi : INT_MIN);
       const unsigned full_u = smem_u32(&full[0]), empty_u = smem_u32(&empty[0]);
-      const C* win_lane = win - s0;  // + buf * FB * WSTRIDE + j
-      for (int i = 0; i < n_ch; ++i, dnf += 1.0f) {
-        const int n = c_lo + i;
-        Tap<R> t;
-        bool live = false;
-        if (DIAG < 2 && n >= wn_lo && n <= wn_hi) {
-          bool in_ap = true;
-          if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
-          if (sizeof(R) == 8) in_ap = in_ap && active_px && n >= n_lo && n <= n_hi;
-          if constexpr (sizeof(R) == 4) geo.template tap<AP>(p, dnf, k0, in_ap, t);
-          else geo.template tap<AP>(p, n, k0, in_ap, t);
-          live = (t.w0 != R(0) || t.w1 != R(0));
-        }
-        if (staged) {
-          const unsigned g = g0 + i;
-          const int buf = (int)(g % DAS_NBUF);
-          if (DIAG != 1) mbar_wait_u32(full_u + 8u * buf, (g / DAS_NBUF) & 1);
-          if (live) {
-            const C* wb = win_lane + (size_t)buf * FB * DAS_WSTRIDE + t.j;
+      const C* win_lane = win - s0;  // + buf * SLOT + (b * CPB + c) * WSTRIDE + j
+      for (int kb = 0; kb < n_blk; ++kb) {
+        const unsigned g = g0 + kb;
+        const int buf = (int)(g % DAS_NBUF);
+        if (staged && DIAG != 1) mbar_wait_u32(full_u + 8u * buf, (g / DAS_NBUF) & 1);
+#pragma unroll
+        for (int c = 0; c < CPB; ++c, dnf += 1.0f) {
+          const int n = c_lo + kb * CPB + c;
+          if (n > c_hi) break;
+          Tap<R> t;
+          bool live = false;
+          if (DIAG < 2 && n >= wn_lo && n <= wn_hi) {
+            bool in_ap = true;
+            if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
+            if (sizeof(R) == 8) in_ap = in_ap && active_px && n >= n_lo && n <= n_hi;
+            if constexpr (sizeof(R) == 4) geo.template tap<AP>(p, dnf, k0, in_ap, t);
+            else geo.template tap<AP>(p, n, k0, in_ap, t);
+            live = (t.w0 != R(0) || t.w1 != R(0));
+          }
+          if (!live) continue;
+          if (staged) {
+            const C* wb = win_lane + (size_t)buf * SLOT + c * DAS_WSTRIDE + t.j;
             if (nfb == FB) {  // CTA-uniform: no per-frame bounds in the common case
 #pragma unroll
-              for (int b = 0; b < FB; ++b)
-                accumulate(t, b, wb[b * DAS_WSTRIDE - 1], wb[b * DAS_WSTRIDE], wb[b * DAS_WSTRIDE + 1]);
+              for (int b = 0; b < FB; ++b) {
+                const C* q = wb + b * CPB * DAS_WSTRIDE;
+                accumulate(t, b, q[-1], q[0], q[1]);
+              }
             } else {
 #pragma unroll
-              for (int b = 0; b < FB; ++b)
-                if (b < nfb) accumulate(t, b, wb[b * DAS_WSTRIDE - 1], wb[b * DAS_WSTRIDE], wb[b * DAS_WSTRIDE + 1]);
+              for (int b = 0; b < FB; ++b) {
+                const C* q = wb + b * CPB * DAS_WSTRIDE;
+                if (b < nfb) accumulate(t, b, q[-1], q[0], q[1]);
+              }
+            }
+          } else {
+            // oversized window (steep geometry): gather straight from global
+#pragma unroll
+            for (int b = 0; b < FB; ++b) {
+              if (b >= nfb) break;
+              const C* src = fbase + b * fstride + (int64_t)n * rowN;
+              accumulate(t, b, src[wrapN(t.j - 1, p.N)], src[wrapN(t.j, p.N)], src[wrapN(t.j + 1, p.N)]);
             }
           }
+        }
+        if (staged) {
           __syncwarp();
           if (DIAG != 1 && lane == 0) mbar_arrive_u32(empty_u + 8u * buf);
-        } else if (live) {
-          // oversized window (steep geometry): gather straight from global
-#pragma unroll
-          for (int b = 0; b < FB; ++b) {
-            if (b >= nfb) break;
-            const C* src = fbase + b * fstride + (int64_t)n * rowN;
-            accumulate(t, b, src[wrapN(t.j - 1, p.N)], src[wrapN(t.j, p.N)], src[wrapN(t.j + 1, p.N)]);
-          }
         }
       }
       if (active_px) {
@@ -420,7 +436,7 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
         }
       }
     }
-    if (staged) g0 += n_ch;
+    if (staged) g0 += (c_hi - c_lo + 1 + CPB - 1) / CPB;
   }
 
   if (!pix) return;
@@ -451,10 +467,10 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
 }
 
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
-          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false>
+          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP>;
+  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (TMAP) {
@@ -468,14 +484,14 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
     const cuuint64_t dims[4] = {(cuuint64_t)p.N, (cuuint64_t)p.E, (cuuint64_t)p.A, (cuuint64_t)p.F};
     const cuuint64_t strides[3] = {(cuuint64_t)p.N * 8, (cuuint64_t)p.E * p.N * 8,
                                    (cuuint64_t)p.A * p.E * p.N * 8};
-    const cuuint32_t box[4] = {(cuuint32_t)(WCAP + 2), 1, 1, (cuuint32_t)FB};
+    const cuuint32_t box[4] = {(cuuint32_t)(WCAP + 2), (cuuint32_t)CPB, 1, (cuuint32_t)FB};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(A), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     TIDAS_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   }
-  const size_t smem = sizeof(C) * DAS_NBUF * FB * (WCAP + 2);
+  const size_t smem = sizeof(C) * DAS_NBUF * FB * CPB * (WCAP + 2);
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 block(32, NW + 1);  // NW consumer warps + 1 producer warp
   constexpr int TZ = 8 * DG, TXC = 4 * (NW / DG);
@@ -490,7 +506,8 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // frame's arithmetic independent of how many frames share the launch, so
 // images are bit-identical under any batching or sharding.
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
-//   0: FB 4, 4 buffers, 4 CTAs/SM, TMA tensor windows (default)   27: same with bulk copies   1: FB 4, 6 buffers   2: FB 2, 8 buffers
+//   0: FB 8, 2-channel TMA tensor boxes, 3 buffers, 2 CTAs/SM (default; = 34)
+//   27: FB 4, bulk copies (earlier default)   1: FB 4, 6 buffers   2: FB 2, 8 buffers
 //   3: FB 8, 3 buffers   4: FB 4, no staging (L1 gathers)   5: FB 4, 4 buffers, 3 CTAs/SM
 //   6: FB 2, 4 buffers, 4 CTAs/SM   8: FB 8, 4 buffers, 2 CTAs/SM
 //   9/10/11: variant 0 with a 16x16 / 8x32 / 64x4 (depth x column) tile
@@ -507,9 +524,24 @@ template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   if (sizeof(R) == 8) return launch_das<R, AP, OUT, 1, 4>(p, A, out, st);
   switch (das_variant()) {
-    case 0:  // measured best on B200 (cfg2): TMA tensor windows, 4 buffers, 4 CTAs/SM
-      return launch_das<R, AP, OUT, 4, 4, 4, false, 4, 254, 0, 8, sizeof(R) == 4>(p, A, out, st);
+    case 0:  // measured best on B200 (cfg2): 8 frames per thread, TMA tensor boxes of
+             // [8 frames][2 channels][256 samples], 3 buffers, 2 CTAs/SM (6.3 us/frame)
+      return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
     case 27: return launch_das<R, AP, OUT, 4, 4, 4>(p, A, out, st);  // previous default (bulk copies)
+    case 28: return launch_das<R, AP, OUT, 4, 3, 4, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
+    case 29: return launch_das<R, AP, OUT, 4, 2, 4, false, 4, 254, 0, 8, sizeof(R) == 4, 4>(p, A, out, st);
+    case 30: return launch_das<R, AP, OUT, 4, 3, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 4>(p, A, out, st);
+    case 31: return launch_das<R, AP, OUT, 4, 4, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
+    case 32: return launch_das<R, AP, OUT, 4, 6, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
+    case 33: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 4>(p, A, out, st);
+    case 34: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
+    case 35: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, sizeof(R) == 4, 2>(p, A, out, st);
+    case 36: return launch_das<R, AP, OUT, 4, 3, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 3>(p, A, out, st);
+    case 37: return launch_das<R, AP, OUT, 8, 4, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 1>(p, A, out, st);
+    case 38: return launch_das<R, AP, OUT, 8, 2, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
+    case 39: return launch_das<R, AP, OUT, 8, 2, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 3>(p, A, out, st);
+    case 40: return launch_das<R, AP, OUT, 8, 3, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 1>(p, A, out, st);
+    case 41: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 16, sizeof(R) == 4, 1>(p, A, out, st);
     case 1: return launch_das<R, AP, OUT, 4, 6>(p, A, out, st);
     case 2: return launch_das<R, AP, OUT, 2, 8>(p, A, out, st);
     case 3: return launch_das<R, AP, OUT, 8, 3>(p, A, out, st);
