@@ -86,12 +86,23 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
   const In* src_b = rf + (ra + 1) * stride;
   if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
   int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
-    const R xa = R(load_as_double(src_a + n)) * scale;
-    const R xb = has_b ? R(load_as_double(src_b + n)) * scale : R(0);
-    if (xa != R(0)) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
-    if (xb != R(0)) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
-    C c; c.x = xa; c.y = xb;
+  // N == blockDim.x * EPT: every thread owns EPT samples per row; all loads are
+  // issued before the first use so their latencies overlap
+  R xa[EPT], xb[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int n = threadIdx.x + k * blockDim.x;
+    xa[k] = R(load_as_double(src_a + n));
+    xb[k] = has_b ? R(load_as_double(src_b + n)) : R(0);
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int n = threadIdx.x + k * blockDim.x;
+    xa[k] *= scale;
+    xb[k] *= scale;
+    if (xa[k] != R(0)) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+    if (xb[k] != R(0)) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    C c; c.x = xa[k]; c.y = xb[k];
     s[fpad(n)] = c;
   }
   __syncthreads();
@@ -120,15 +131,26 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
   fft_inplace<R, true, EPT>(s, logN);
   C* dst_a = out + ra * (int64_t)N;
   C* dst_b = dst_a + N;
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+  // real parts = the inputs, re-read (L2) with all loads in flight first
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int n = threadIdx.x + k * blockDim.x;
+    if (!DELAY) {
+      xa[k] = R(load_as_double(src_a + n)) * scale;
+      xb[k] = has_b ? R(load_as_double(src_b + n)) * scale : R(0);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int n = threadIdx.x + k * blockDim.x;
     const C y = s[fpad(n)];
     if (DELAY) {
       dst_a[n] = y;
     } else {
-      C a; a.x = R(load_as_double(src_a + n)) * scale; a.y = y.x;
+      C a; a.x = xa[k]; a.y = y.x;
       dst_a[n] = a;
       if (has_b) {
-        C b; b.x = R(load_as_double(src_b + n)) * scale; b.y = y.y;
+        C b; b.x = xb[k]; b.y = y.y;
         dst_b[n] = b;
       }
     }
