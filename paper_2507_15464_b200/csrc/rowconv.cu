@@ -16,6 +16,8 @@
 // reading 4 new inputs and 4 taps per 4 steps as conflict-free 128-bit shared
 // loads (tap loads are warp broadcasts). 129 taps -> 16 FMA per shared load.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -135,12 +137,30 @@ __global__ void rowconv_generic_kernel(const float* __restrict__ in, const float
 }
 
 template <bool ADJ>
+int launch_rowconv_tc(const float* in, const float* K, float* out, int64_t batch, int nz, int nx, int T,
+                      cudaStream_t st);
+
+// TIDAS_ROWCONV_PATH=simt forces the CUDA-core kernel (tests compare both paths)
+static bool rowconv_tc_enabled() {
+  static int v = [] {
+    const char* e = getenv("TIDAS_ROWCONV_PATH");
+    return (e && std::string(e) == "simt") ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+template <bool ADJ>
 static int launch_rowconv(const float* in, const float* K, float* out, int64_t batch, int nz, int nx,
                           int T, cudaStream_t st) {
   TIDAS_REQUIRE(in && K && out, "null pointer");
   TIDAS_REQUIRE(batch >= 0 && nz >= 0 && nx >= 0, "bad sizes");
   TIDAS_REQUIRE(T >= 1 && (T & 1) && T <= 255, "taps must be odd and in [1, 255]");
   if (batch == 0 || nz == 0 || nx == 0) return TIDAS_OK;
+  // tensor cores (tcgen05, 3xTF32) for batches that fill the 128-map MMA tile
+  if (rowconv_tc_enabled() && batch >= 32) {
+    const int rc = launch_rowconv_tc<ADJ>(in, K, out, batch, nz, nx, T, st);
+    if (rc != TIDAS_EUNSUPPORTED) return rc;
+  }
   const bool aligned = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
   if ((nx & 7) || !aligned) {
     const int64_t total = batch * nz * (int64_t)nx;

@@ -1,0 +1,406 @@
+// K6 / K7 on the 5th-generation tensor cores (tcgen05 + TMEM), float32-exact
+// through a 3xTF32 split.
+//
+// For one depth row i the row operator is a GEMM with a banded Toeplitz matrix:
+//   Y[b, x] = sum_u G[b, u] T[u, x],  T[u, x] = K'[u - x + 64]  (0 <= u - x + 64 <= 128)
+// where K' is the row kernel zero-padded to 129 taps around its centre (any odd
+// T <= 129; the adjoint uses the reversed kernel). For an output block of 32
+// columns x in [32j, 32j + 32) only inputs u in [32j - 64, 32j + 96) contribute,
+// and the 32 x 160 block of T is the same for every j: it is built ONCE per row
+// in shared memory (hi and lo TF32 halves, K-major, 128B-swizzled) and reused
+// by every output block and map block of that row.
+//
+//   MMA (M = 128 maps, N = 32 outputs, K = 8 inputs per instruction):
+//     D[128 maps][32 outputs] (TMEM, fp32) +=
+//         A_hi B_hi + A_hi B_lo + A_lo B_hi      (A = maps, B = Toeplitz taps)
+//   A streams through TMEM: the 4 converter warps (thread = map = TMEM lane)
+//   load 32-input chunks with 128-bit loads, split them into TF32 hi / lo
+//   (cvt.rna) and tcgen05.st them into a 6-chunk ring (hi: columns 0..191,
+//   lo: 192..383); block j reads chunks j .. j+4. D is double-buffered
+//   (columns 384..447) so the epilogue of block j-1 overlaps the MMAs of block j.
+//   One elected thread of warp 4 issues the 60 tcgen05.mma of a block and
+//   commits them to an mbarrier.
+//
+// Precision: a = hi + lo with hi = rna_tf32(a), lo = rna_tf32(a - hi); the
+// dropped lo*lo term and the rounding of lo are ~2^-22 relative per product.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace tidas {
+
+namespace tc {
+
+constexpr int MAPS = 128;      // M: maps per block (TMEM lanes)
+constexpr int NOUT = 32;       // N: outputs per block
+constexpr int HALO = 64;       // taps each side (padded kernel of 129)
+constexpr int KSPAN = NOUT + 2 * HALO;   // 160 inputs per output block
+constexpr int CH = 32;         // inputs per chunk (one 128B swizzle atom of K)
+constexpr int CHB = KSPAN / CH;          // 5 chunks per block
+constexpr int RING = 6;        // chunk slots in TMEM
+constexpr int COL_HI = 0, COL_LO = RING * CH, COL_D = 2 * RING * CH;  // 0, 192, 384
+constexpr int TMEM_COLS = 512;
+constexpr int B_ATOM = NOUT * 128;       // bytes per K-atom of B (32 rows x 128 B)
+constexpr int B_BYTES = CHB * B_ATOM;    // 20 KB per half
+constexpr int NTHREADS = 192;            // 4 converter/epilogue warps + MMA warp + TMA warp
+constexpr int NSTAGE = 4;                // A chunk stages in shared memory (TMA ring)
+constexpr int A_STAGE = MAPS * CH * 4;   // 16 KB: [128 maps][32 inputs], 128B-swizzled
+
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, unsigned n) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1, %2;\n"
+      " @!p bra W_%=;\n}\n" ::"r"(su32(b)), "r"(parity), "r"(1000000u) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+// 3-D TMA tile [128 maps][1 row][32 inputs] of the maps tensor; OOB -> zeros
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int row, int m0,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(row), "r"(m0), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int row, int m0) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(su32(src)), "r"(x), "r"(row), "r"(m0)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ unsigned tf32_rna(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ void tmem_st32(unsigned taddr, const unsigned (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n"
+      ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+        "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+        "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, float (&v)[32]) {
+  unsigned r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+// K-major, 128B-swizzled shared-memory matrix descriptor (sm_100 "version 1"):
+// start >> 4, LBO 0 (one K-atom per MMA), SBO 1024 (8-row core groups).
+__device__ __forceinline__ uint64_t smem_desc_sw128(unsigned saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, both K-major, N = 32, M = 128
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NOUT >> 3) << 17) |
+                           ((uint32_t)(MAPS >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(unsigned d_tmem, unsigned a_tmem, uint64_t b_desc, int accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(IDESC), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+               ::"r"(su32(bar)) : "memory");
+}
+
+// byte offset of B element (row r = output x', column u' in [0, 160)) in the
+// K-major SW128 layout: atoms of 32 rows x 128 B along K
+__device__ __forceinline__ int b_offset(int r, int u) {
+  const int atom = u >> 5, c = u & 31;
+  return atom * B_ATOM + (r >> 3) * 1024 + (r & 7) * 128 + ((((c >> 2) ^ (r & 7))) << 4) + ((c & 3) << 2);
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                 const __grid_constant__ CUtensorMap omap,
+                                                                 const float* __restrict__ K,
+                                                                 float* __restrict__ out, int batch,
+                                                                 int nz, int nx, int T) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // B halves, 1024-aligned (swizzle atoms)
+  unsigned char* sbase = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
+  unsigned char* B_hi = sbase;
+  unsigned char* B_lo = sbase + B_BYTES;
+  unsigned char* A_st = sbase + 2 * B_BYTES;  // [NSTAGE][16 KB], 1024-aligned
+  unsigned char* O_st = A_st + NSTAGE * A_STAGE;  // [4 warps][2][32 maps][32 outputs], 128B-swizzled
+  __shared__ __align__(8) uint64_t block_ready[2], mma_done[2], d_empty[2];
+  __shared__ __align__(8) uint64_t a_full[NSTAGE], a_empty[NSTAGE];
+  __shared__ unsigned tmem_base_s;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_mb = (batch + MAPS - 1) / MAPS;
+  const int n_xb = (nx + NOUT - 1) / NOUT;
+  const int H = (T - 1) / 2;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                 ::"r"(su32(&tmem_base_s)), "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (threadIdx.x == 32) {
+    for (int k = 0; k < 2; ++k) {
+      bar_init(&block_ready[k], 4);
+      bar_init(&mma_done[k], 1);
+      bar_init(&d_empty[k], 4);
+    }
+    for (int k = 0; k < NSTAGE; ++k) {
+      bar_init(&a_full[k], 1);
+      bar_init(&a_empty[k], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const unsigned tmem = tmem_base_s;
+
+  // rows of this CTA: i = blockIdx.x + r * gridDim.x; blocks per row = n_mb * n_xb
+  const int rows_mine = (nz - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const long long total_blocks = (long long)rows_mine * n_mb * n_xb;
+
+  if (warp < 4) {
+    // ===== converter + epilogue warps: thread = map m = TMEM lane (32 warp + lane)
+    const int m = warp * 32 + lane;
+    const unsigned lane_addr = (unsigned)(warp * 32) << 16;
+    long long b = 0;
+    long long gq = 0;  // A chunks consumed (same order the TMA warp produces them)
+    auto write_chunk = [&](int row, int mb, int q) {
+      // chunk q of the row (inputs u in [32 q - 64, 32 q - 32)) from its TMA stage
+      const int slot = q % RING;
+      const int st = (int)(gq % NSTAGE);
+      bar_wait(&a_full[st], (unsigned)((gq / NSTAGE) & 1));
+      const unsigned char* rowp = A_st + st * A_STAGE + m * 128;
+      float v[32];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // 16-byte chunk k of this map's 128-byte row, swizzled
+        const float4 w = *reinterpret_cast<const float4*>(rowp + ((k ^ (m & 7)) << 4));
+        v[4 * k] = w.x; v[4 * k + 1] = w.y; v[4 * k + 2] = w.z; v[4 * k + 3] = w.w;
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&a_empty[st]);
+      ++gq;
+      (void)row; (void)mb;
+      unsigned hi[32], lo[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        hi[k] = tf32_rna(v[k]);
+        lo[k] = tf32_rna(v[k] - __uint_as_float(hi[k]));
+      }
+      tmem_st32(tmem + lane_addr + COL_HI + slot * CH, hi);
+      tmem_st32(tmem + lane_addr + COL_LO + slot * CH, lo);
+    };
+    long long ne = 0;  // epilogues done by this warp (staging slot = ne & 1)
+    auto epilogue = [&](long long bb, int row, int mb, int j) {
+      const int dbuf = (int)(bb & 1);
+      bar_wait(&mma_done[dbuf], (unsigned)((bb >> 1) & 1));
+      fence_after();
+      float v[32];
+      tmem_ld32(tmem + lane_addr + COL_D + dbuf * NOUT, v);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        bar_arrive(&d_empty[dbuf]);
+        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");  // slot's previous store read out
+      }
+      __syncwarp();
+      unsigned char* slab = O_st + (warp * 2 + (int)(ne & 1)) * 4096;
+      unsigned char* rowp = slab + lane * 128;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        *reinterpret_cast<float4*>(rowp + ((k ^ (lane & 7)) << 4)) =
+            make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      // TMA clips maps >= batch and outputs >= nx
+      if (lane == 0) tma_store_3d(&omap, slab, j * NOUT, row, mb * MAPS + warp * 32);
+      ++ne;
+    };
+    int prev_row = -1, prev_mb = 0, prev_j = 0;
+    for (int r = 0; r < rows_mine; ++r) {
+      const int row = (int)blockIdx.x + r * (int)gridDim.x;
+      for (int mb = 0; mb < n_mb; ++mb) {
+        for (int j = 0; j < n_xb; ++j, ++b) {
+          if (j == 0) {
+            // new (row, map block): every MMA of the previous one must be done
+            // before the TMEM ring (and, on a new row, B) is overwritten
+            if (b >= 1) {
+              bar_wait(&mma_done[(b - 1) & 1], (unsigned)(((b - 1) >> 1) & 1));
+              fence_after();
+            }
+            if (mb == 0) {
+              // Toeplitz taps of this row: B[x'][u'] = K'[u' - x'], hi / lo halves
+              for (int e = threadIdx.x; e < NOUT * KSPAN; e += 128) {
+                const int rr = e / KSPAN, u = e - rr * KSPAN;
+                const int k = u - rr;           // padded tap index in [0, 128]
+                const int kt = k - (HALO - H);  // original tap
+                float w = 0.f;
+                if (k >= 0 && k <= 2 * HALO && kt >= 0 && kt < T)
+                  w = K[(long long)row * T + (ADJ ? (T - 1 - kt) : kt)];
+                const unsigned h = tf32_rna(w);
+                const unsigned l = tf32_rna(w - __uint_as_float(h));
+                const int off = b_offset(rr, u);
+                *reinterpret_cast<unsigned*>(B_hi + off) = h;
+                *reinterpret_cast<unsigned*>(B_lo + off) = l;
+              }
+              asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            }
+            for (int q = 0; q < CHB - 1; ++q) write_chunk(row, mb, q);
+          } else if (b >= 2 && j >= 2) {
+            // the slot of chunk j + 4 last held chunk j - 2, read by block j - 2
+            bar_wait(&mma_done[(b - 2) & 1], (unsigned)(((b - 2) >> 1) & 1));
+            fence_after();
+          } else if (j == 1 && b >= 2) {
+            bar_wait(&mma_done[(b - 2) & 1], (unsigned)(((b - 2) >> 1) & 1));
+            fence_after();
+          }
+          write_chunk(row, mb, j + CHB - 1);
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+          fence_before();
+          __syncwarp();
+          if (lane == 0) bar_arrive(&block_ready[b & 1]);
+          // epilogue of the previous block overlaps this block's MMAs
+          if (b >= 1) epilogue(b - 1, prev_row, prev_mb, prev_j);
+          prev_row = row; prev_mb = mb; prev_j = j;
+        }
+      }
+    }
+    if (b >= 1) epilogue(b - 1, prev_row, prev_mb, prev_j);
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+  } else if (warp == 5) {
+    // ===== TMA producer: A chunks in consumption order, NSTAGE ahead
+    if (lane == 0) {
+      long long gp = 0;
+      for (int r = 0; r < rows_mine; ++r) {
+        const int row = (int)blockIdx.x + r * (int)gridDim.x;
+        for (int mb = 0; mb < n_mb; ++mb) {
+          for (int q = 0; q < n_xb + CHB - 1; ++q, ++gp) {
+            const int st = (int)(gp % NSTAGE);
+            if (gp >= NSTAGE) bar_wait(&a_empty[st], (unsigned)(((gp / NSTAGE) - 1) & 1));
+            bar_expect_tx(&a_full[st], A_STAGE);
+            tma_load_3d(A_st + st * A_STAGE, &tmap, q * CH - HALO, row, mb * MAPS, &a_full[st]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    // ===== MMA issuer (one elected thread)
+    const unsigned bh = su32(B_hi), bl = su32(B_lo);
+    long long b = 0;
+    for (int r = 0; r < rows_mine; ++r) {
+      for (int mb = 0; mb < n_mb; ++mb) {
+        for (int j = 0; j < n_xb; ++j, ++b) {
+          bar_wait(&block_ready[b & 1], (unsigned)((b >> 1) & 1));
+          if (b >= 2) bar_wait(&d_empty[b & 1], (unsigned)(((b - 2) >> 1) & 1));
+          fence_after();
+          if (lane == 0) {
+            const unsigned d = tmem + COL_D + (unsigned)(b & 1) * NOUT;
+#pragma unroll 4
+            for (int s = 0; s < KSPAN / 8; ++s) {  // 20 K-steps of 8 inputs
+              const int slot = (j + (s >> 2)) % RING;
+              const unsigned ac = (unsigned)(slot * CH + (s & 3) * 8);
+              const unsigned boff = (unsigned)((s >> 2) * B_ATOM + (s & 3) * 32);
+              const uint64_t dbh = smem_desc_sw128(bh + boff), dbl = smem_desc_sw128(bl + boff);
+              mma_tf32(d, tmem + COL_HI + ac, dbh, s > 0);
+              mma_tf32(d, tmem + COL_HI + ac, dbl, 1);
+              mma_tf32(d, tmem + COL_LO + ac, dbh, 1);
+            }
+            mma_commit(&mma_done[b & 1]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
+}  // namespace tc
+
+// host side: returns TIDAS_EUNSUPPORTED when the shape is outside the tensor path
+template <bool ADJ>
+int launch_rowconv_tc(const float* in, const float* K, float* out, int64_t batch, int nz, int nx, int T,
+                      cudaStream_t st) {
+  using namespace tc;
+  if (T > 2 * HALO + 1 || (nx & 3) || batch > (int64_t(1) << 30) ||
+      ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15))
+    return TIDAS_EUNSUPPORTED;
+  int dev = 0, sms = 0;
+  TIDAS_CUDA_CHECK(cudaGetDevice(&dev));
+  TIDAS_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    TIDAS_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q));
+    TIDAS_REQUIRE(q == cudaDriverEntryPointSuccess && encode, "cuTensorMapEncodeTiled unavailable");
+  }
+  CUtensorMap tmap;
+  const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)nz, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)nx * 4, (cuuint64_t)nz * nx * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)CH, 1, (cuuint32_t)MAPS};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return TIDAS_EUNSUPPORTED;
+  CUtensorMap omap;
+  const cuuint32_t obox[3] = {(cuuint32_t)NOUT, 1, 32};
+  const CUresult r2 = encode(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out, dims, strides, obox, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r2 != CUDA_SUCCESS) return TIDAS_EUNSUPPORTED;
+  // ask for more shared memory than two CTAs could share, so each SM holds one
+  // CTA and its 512 TMEM columns are never contended
+  const size_t smem = 2 * B_BYTES + NSTAGE * A_STAGE + 8 * 4096 + 1024;
+  auto kern = rowconv_tc_kernel<ADJ>;
+  TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = nz < sms ? nz : sms;
+  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, out, (int)batch, nz, nx, T);
+  TIDAS_LAUNCH_CHECK();
+  return TIDAS_OK;
+}
+
+template int launch_rowconv_tc<false>(const float*, const float*, float*, int64_t, int, int, int, cudaStream_t);
+template int launch_rowconv_tc<true>(const float*, const float*, float*, int64_t, int, int, int, cudaStream_t);
+
+}  // namespace tidas
