@@ -132,6 +132,19 @@ __device__ __forceinline__ void mma_tf32(unsigned d_tmem, unsigned a_tmem, uint6
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(IDESC), "r"(accumulate));
 }
+// issued by the whole (converged) warp with warp-uniform operands; one lane is
+// elected inside the asm so no per-MMA waterfall over lanes is generated
+__device__ __forceinline__ void mma_tf32_warp(unsigned d_tmem, unsigned a_tmem, uint64_t b_desc, int accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(IDESC), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+               " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n"
+               ::"r"(su32(bar)) : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
                ::"r"(su32(bar)) : "memory");
@@ -328,19 +341,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc_kernel(const __grid_co
           bar_wait(&block_ready[b & 1], (unsigned)((b >> 1) & 1));
           if (b >= 2) bar_wait(&d_empty[b & 1], (unsigned)(((b - 2) >> 1) & 1));
           fence_after();
-          if (lane == 0) {
+          {
             const unsigned d = tmem + COL_D + (unsigned)(b & 1) * NOUT;
-#pragma unroll 4
-            for (int s = 0; s < KSPAN / 8; ++s) {  // 20 K-steps of 8 inputs
-              const int slot = (j + (s >> 2)) % RING;
-              const unsigned ac = (unsigned)(slot * CH + (s & 3) * 8);
-              const unsigned boff = (unsigned)((s >> 2) * B_ATOM + (s & 3) * 32);
-              const uint64_t dbh = smem_desc_sw128(bh + boff), dbl = smem_desc_sw128(bl + boff);
-              mma_tf32(d, tmem + COL_HI + ac, dbh, s > 0);
-              mma_tf32(d, tmem + COL_HI + ac, dbl, 1);
-              mma_tf32(d, tmem + COL_LO + ac, dbh, 1);
+            const uint64_t dbh0 = smem_desc_sw128(bh), dbl0 = smem_desc_sw128(bl);
+#pragma unroll
+            for (int c = 0; c < CHB; ++c) {  // 32-input chunk c of the K span (TMEM ring slot)
+              const int slot = (j + c) % RING;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {  // K-steps of 8 inputs
+                const unsigned ac = (unsigned)(slot * CH + t * 8);
+                const uint64_t boff = (uint64_t)((c * B_ATOM + t * 32) >> 4);  // descriptor start field
+                mma_tf32_warp(d, tmem + COL_HI + ac, dbh0 + boff, (c | t) != 0);
+                mma_tf32_warp(d, tmem + COL_HI + ac, dbl0 + boff, 1);
+                mma_tf32_warp(d, tmem + COL_LO + ac, dbh0 + boff, 1);
+              }
             }
-            mma_commit(&mma_done[b & 1]);
+            mma_commit_warp(&mma_done[b & 1]);
           }
           __syncwarp();
         }
