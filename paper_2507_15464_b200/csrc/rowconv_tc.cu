@@ -13,16 +13,24 @@
 //   MMA (M = 128 maps, N = 32 outputs, K = 8 inputs per instruction):
 //     D[128 maps][32 outputs] (TMEM, fp32) +=
 //         A_hi B_hi + A_hi B_lo + A_lo B_hi      (A = maps, B = Toeplitz taps)
-//   A streams through TMEM: the 4 converter warps (thread = map = TMEM lane)
-//   load 32-input chunks with 128-bit loads, split them into TF32 hi / lo
-//   (cvt.rna) and tcgen05.st them into a 6-chunk ring (hi: columns 0..191,
-//   lo: 192..383); block j reads chunks j .. j+4. D is double-buffered
-//   (columns 384..447) so the epilogue of block j-1 overlaps the MMAs of block j.
-//   One elected thread of warp 4 issues the 60 tcgen05.mma of a block and
-//   commits them to an mbarrier.
+//   Warp roles (one CTA per SM, 320 threads):
+//     warp 9    TMA producer: 32-input x 128-map chunks of the maps tensor
+//               (3-D tensor map, 128B swizzle, OOB zero fill = the row halo)
+//               into a 4-stage shared-memory ring;
+//     warps 0-3 converters (thread = map = TMEM lane): Toeplitz taps of each
+//               row into a double-buffered B, and every A chunk split into
+//               TF32 hi / lo (cvt.rna) and tcgen05.st into a 6-slot TMEM ring
+//               (hi: columns 0..191, lo: 192..383); block j reads chunks j..j+4;
+//     warp 8    MMA issuer: 60 tcgen05.mma per block (whole warp, elect.sync),
+//               commits to the accumulator, chunk-free and row-done barriers;
+//     warps 4-7 epilogue: tcgen05.ld of the double-buffered pair of
+//               accumulators (columns 384..511), summed -> swizzled smem slab -> TMA tensor store.
+//   Every hand-off is an mbarrier ring, so conversion, MMA and epilogue of
+//   consecutive blocks (and rows) overlap.
 //
 // Precision: a = hi + lo with hi = rna_tf32(a), lo = rna_tf32(a - hi); the
 // dropped lo*lo term and the rounding of lo are ~2^-22 relative per product.
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -40,12 +48,14 @@ constexpr int CH = 32;         // inputs per chunk (one 128B swizzle atom of K)
 constexpr int CHB = KSPAN / CH;          // 5 chunks per block
 constexpr int RING = 6;        // chunk slots in TMEM
 constexpr int COL_HI = 0, COL_LO = RING * CH, COL_D = 2 * RING * CH;  // 0, 192, 384
+constexpr int NCHAIN = 2;      // independent accumulators per block (MMAs alternate)
 constexpr int TMEM_COLS = 512;
 constexpr int B_ATOM = NOUT * 128;       // bytes per K-atom of B (32 rows x 128 B)
 constexpr int B_BYTES = CHB * B_ATOM;    // 20 KB per half
-constexpr int NTHREADS = 192;            // 4 converter/epilogue warps + MMA warp + TMA warp
+constexpr int NTHREADS = 320;            // 4 converter + 4 epilogue warps, MMA warp, TMA warp
 constexpr int NSTAGE = 4;                // A chunk stages in shared memory (TMA ring)
 constexpr int A_STAGE = MAPS * CH * 4;   // 16 KB: [128 maps][32 inputs], 128B-swizzled
+constexpr int OSLAB = 4;                 // output slabs (TMA stores in flight) per epilogue warp
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(uint64_t* b, unsigned n) {
@@ -60,6 +70,26 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, unsigned parity) {
       "W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1, %2;\n"
       " @!p bra W_%=;\n}\n" ::"r"(su32(b)), "r"(parity), "r"(1000000u) : "memory");
 }
+#ifdef TIDAS_RC_PROF
+__device__ unsigned long long g_rc_prof[16][16];  // [warp][wait site] cycles (lane 0 of each warp)
+#define RC_PROF_DECL unsigned long long rc_prof[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}; \
+  const long long rc_t_begin = clock64();
+#define RC_WAIT(site, bar, par)                 \
+  do {                                          \
+    const long long t_ = clock64();             \
+    bar_wait(bar, par);                         \
+    rc_prof[site] += (unsigned long long)(clock64() - t_); \
+  } while (0)
+#define RC_PROF_FLUSH(warp)                                                        \
+  if ((threadIdx.x & 31) == 0) {                                                   \
+    for (int k_ = 0; k_ < 9; ++k_) atomicAdd(&g_rc_prof[warp][k_], rc_prof[k_]);  \
+    atomicAdd(&g_rc_prof[warp][9], (unsigned long long)(clock64() - rc_t_begin)); \
+  }
+#else
+#define RC_PROF_DECL
+#define RC_WAIT(site, bar, par) bar_wait(bar, par)
+#define RC_PROF_FLUSH(warp)
+#endif
 __device__ __forceinline__ void bar_expect_tx(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
@@ -140,6 +170,16 @@ __device__ __forceinline__ void mma_tf32_warp(unsigned d_tmem, unsigned a_tmem, 
       " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(IDESC), "r"(accumulate));
 }
+// same, with the B descriptor passed as its two 32-bit halves (only the low
+// word - the start address - varies between instructions)
+__device__ __forceinline__ void mma_tf32_warp2(unsigned d_tmem, unsigned a_tmem, unsigned b_lo, unsigned b_hi,
+                                               bool accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n .reg .b64 bd;\n setp.ne.b32 p, %5, 0;\n mov.b64 bd, {%2, %3};\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bd, %4, p;\n}\n"
+      ::"r"(d_tmem), "r"(a_tmem), "r"(b_lo), "r"(b_hi), "n"(IDESC), "r"((unsigned)accumulate));
+}
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
   asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
                " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n"
@@ -160,23 +200,26 @@ __device__ __forceinline__ int b_offset(int r, int u) {
 template <bool ADJ>
 __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                  const __grid_constant__ CUtensorMap omap,
-                                                                 const float* __restrict__ K,
-                                                                 float* __restrict__ out, int batch,
-                                                                 int nz, int nx, int T) {
+                                                                 const float* __restrict__ K, int batch,
+                                                                 int nz, int nx, int T, int rows_per,
+                                                                 int diag) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // B halves, 1024-aligned (swizzle atoms)
   unsigned char* sbase = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
-  unsigned char* B_hi = sbase;
-  unsigned char* B_lo = sbase + B_BYTES;
-  unsigned char* A_st = sbase + 2 * B_BYTES;  // [NSTAGE][16 KB], 1024-aligned
-  unsigned char* O_st = A_st + NSTAGE * A_STAGE;  // [4 warps][2][32 maps][32 outputs], 128B-swizzled
-  __shared__ __align__(8) uint64_t block_ready[2], mma_done[2], d_empty[2];
-  __shared__ __align__(8) uint64_t a_full[NSTAGE], a_empty[NSTAGE];
+  unsigned char* B_st = sbase;                        // [2 rows][hi, lo][20 KB], 1024-aligned atoms
+  unsigned char* A_st = sbase + 4 * B_BYTES;          // [NSTAGE][16 KB]
+  unsigned char* O_st = A_st + NSTAGE * A_STAGE;      // [4 quarters][OSLAB][32 maps][32 outputs]
+  __shared__ __align__(8) uint64_t a_full[NSTAGE], a_empty[NSTAGE];  // TMA ring
+  __shared__ __align__(8) uint64_t c_full[RING], c_free[RING];       // TMEM chunk ring
+  __shared__ __align__(8) uint64_t mma_done[2], d_empty[2];          // accumulators
+  __shared__ __align__(8) uint64_t row_done[2];                      // Toeplitz buffers
   __shared__ unsigned tmem_base_s;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0: role branches become warp-uniform, so the
+  // MMA operands stay in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int n_mb = (batch + MAPS - 1) / MAPS;
   const int n_xb = (nx + NOUT - 1) / NOUT;
+  const int S = n_xb + CHB - 1;  // chunks per (row, map block) segment
   const int H = (T - 1) / 2;
 
   if (warp == 0) {
@@ -185,14 +228,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc_kernel(const __grid_co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (threadIdx.x == 32) {
-    for (int k = 0; k < 2; ++k) {
-      bar_init(&block_ready[k], 4);
-      bar_init(&mma_done[k], 1);
-      bar_init(&d_empty[k], 4);
-    }
     for (int k = 0; k < NSTAGE; ++k) {
       bar_init(&a_full[k], 1);
       bar_init(&a_empty[k], 4);
+    }
+    for (int k = 0; k < RING; ++k) {
+      bar_init(&c_full[k], 4);
+      bar_init(&c_free[k], 1);
+    }
+    for (int k = 0; k < 2; ++k) {
+      bar_init(&mma_done[k], 1);
+      bar_init(&d_empty[k], 4);
+      bar_init(&row_done[k], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -200,130 +247,125 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc_kernel(const __grid_co
   __syncthreads();
   fence_after();
   const unsigned tmem = tmem_base_s;
+  if (tmem != 0) __trap();  // a full 512-column allocation always starts at column 0
+  RC_PROF_DECL
 
-  // rows of this CTA: i = blockIdx.x + r * gridDim.x; blocks per row = n_mb * n_xb
-  const int rows_mine = (nz - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const long long total_blocks = (long long)rows_mine * n_mb * n_xb;
+  // a contiguous band of rows per CTA: each map is then read and written as
+  // one sequential stream per CTA
+  const int row0 = (int)blockIdx.x * rows_per;
+  const int rows_mine = max(0, min(rows_per, nz - row0));
 
   if (warp < 4) {
-    // ===== converter + epilogue warps: thread = map m = TMEM lane (32 warp + lane)
-    const int m = warp * 32 + lane;
+    // ===== converters: Toeplitz taps per row, A chunks -> TF32 hi/lo -> TMEM ring
+    const int m = warp * 32 + lane;  // map within the block = TMEM lane
     const unsigned lane_addr = (unsigned)(warp * 32) << 16;
-    long long b = 0;
-    long long gq = 0;  // A chunks consumed (same order the TMA warp produces them)
-    auto write_chunk = [&](int row, int mb, int q) {
-      // chunk q of the row (inputs u in [32 q - 64, 32 q - 32)) from its TMA stage
-      const int slot = q % RING;
-      const int st = (int)(gq % NSTAGE);
-      bar_wait(&a_full[st], (unsigned)((gq / NSTAGE) & 1));
-      const unsigned char* rowp = A_st + st * A_STAGE + m * 128;
-      float v[32];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {  // 16-byte chunk k of this map's 128-byte row, swizzled
-        const float4 w = *reinterpret_cast<const float4*>(rowp + ((k ^ (m & 7)) << 4));
-        v[4 * k] = w.x; v[4 * k + 1] = w.y; v[4 * k + 2] = w.z; v[4 * k + 3] = w.w;
+    long long gc = 0;  // chunks converted (TMA order)
+    for (int r = 0; r < rows_mine; ++r) {
+      const int row = row0 + r;
+      // B[r & 1] was last read by the MMAs of row r - 2
+      if (r >= 2) RC_WAIT(0, &row_done[r & 1], (unsigned)(((r - 2) >> 1) & 1));
+      unsigned char* Bh = B_st + (r & 1) * 2 * B_BYTES;
+      unsigned char* Bl = Bh + B_BYTES;
+      for (int e = threadIdx.x; e < NOUT * KSPAN; e += 128) {
+        const int rr = e / KSPAN, u = e - rr * KSPAN;
+        const int k = u - rr;           // padded tap index in [0, 128]
+        const int kt = k - (HALO - H);  // original tap
+        float w = 0.f;
+        if (k >= 0 && k <= 2 * HALO && kt >= 0 && kt < T) w = K[(long long)row * T + (ADJ ? (T - 1 - kt) : kt)];
+        const unsigned h = tf32_rna(w);
+        const unsigned l = tf32_rna(w - __uint_as_float(h));
+        const int off = b_offset(rr, u);
+        *reinterpret_cast<unsigned*>(Bh + off) = h;
+        *reinterpret_cast<unsigned*>(Bl + off) = l;
       }
-      __syncwarp();
-      if (lane == 0) bar_arrive(&a_empty[st]);
-      ++gq;
-      (void)row; (void)mb;
-      unsigned hi[32], lo[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        hi[k] = tf32_rna(v[k]);
-        lo[k] = tf32_rna(v[k] - __uint_as_float(hi[k]));
-      }
-      tmem_st32(tmem + lane_addr + COL_HI + slot * CH, hi);
-      tmem_st32(tmem + lane_addr + COL_LO + slot * CH, lo);
-    };
-    long long ne = 0;  // epilogues done by this warp (staging slot = ne & 1)
-    auto epilogue = [&](long long bb, int row, int mb, int j) {
-      const int dbuf = (int)(bb & 1);
-      bar_wait(&mma_done[dbuf], (unsigned)((bb >> 1) & 1));
-      fence_after();
-      float v[32];
-      tmem_ld32(tmem + lane_addr + COL_D + dbuf * NOUT, v);
-      fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        bar_arrive(&d_empty[dbuf]);
-        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");  // slot's previous store read out
-      }
-      __syncwarp();
-      unsigned char* slab = O_st + (warp * 2 + (int)(ne & 1)) * 4096;
-      unsigned char* rowp = slab + lane * 128;
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        *reinterpret_cast<float4*>(rowp + ((k ^ (lane & 7)) << 4)) =
-            make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
-      // TMA clips maps >= batch and outputs >= nx
-      if (lane == 0) tma_store_3d(&omap, slab, j * NOUT, row, mb * MAPS + warp * 32);
-      ++ne;
-    };
-    int prev_row = -1, prev_mb = 0, prev_j = 0;
+      for (int q = 0; q < n_mb * S; ++q, ++gc) {
+        const int slot = (int)(gc % RING);
+        if (gc >= RING) {
+          RC_WAIT(1, &c_free[slot], (unsigned)(((gc / RING) - 1) & 1));
+          fence_after();
+        }
+        const int st = (int)(gc % NSTAGE);
+        RC_WAIT(2, &a_full[st], (unsigned)((gc / NSTAGE) & 1));
+        const unsigned char* rowp = A_st + st * A_STAGE + m * 128;
+        float v[32];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // 16-byte chunk k of this map's 128-byte row, swizzled
+          const float4 w = *reinterpret_cast<const float4*>(rowp + ((k ^ (m & 7)) << 4));
+          v[4 * k] = w.x; v[4 * k + 1] = w.y; v[4 * k + 2] = w.z; v[4 * k + 3] = w.w;
+        }
+        __syncwarp();
+        if (lane == 0) bar_arrive(&a_empty[st]);
+        unsigned hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          hi[k] = tf32_rna(v[k]);
+          lo[k] = tf32_rna(v[k] - __uint_as_float(hi[k]));
+        }
+        tmem_st32(tmem + lane_addr + COL_HI + slot * CH, hi);
+        tmem_st32(tmem + lane_addr + COL_LO + slot * CH, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(&c_full[slot]);
+      }
+    }
+  } else if (warp < 8) {
+    // ===== epilogue: TMEM accumulator -> swizzled smem slab -> TMA store
+    const int qw = warp & 3;  // TMEM lane quarter this warp may access
+    const unsigned lane_addr = (unsigned)(qw * 32) << 16;
+    long long b = 0;
     for (int r = 0; r < rows_mine; ++r) {
-      const int row = (int)blockIdx.x + r * (int)gridDim.x;
+      const int row = row0 + r;
       for (int mb = 0; mb < n_mb; ++mb) {
         for (int j = 0; j < n_xb; ++j, ++b) {
-          if (j == 0) {
-            // new (row, map block): every MMA of the previous one must be done
-            // before the TMEM ring (and, on a new row, B) is overwritten
-            if (b >= 1) {
-              bar_wait(&mma_done[(b - 1) & 1], (unsigned)(((b - 1) >> 1) & 1));
-              fence_after();
-            }
-            if (mb == 0) {
-              // Toeplitz taps of this row: B[x'][u'] = K'[u' - x'], hi / lo halves
-              for (int e = threadIdx.x; e < NOUT * KSPAN; e += 128) {
-                const int rr = e / KSPAN, u = e - rr * KSPAN;
-                const int k = u - rr;           // padded tap index in [0, 128]
-                const int kt = k - (HALO - H);  // original tap
-                float w = 0.f;
-                if (k >= 0 && k <= 2 * HALO && kt >= 0 && kt < T)
-                  w = K[(long long)row * T + (ADJ ? (T - 1 - kt) : kt)];
-                const unsigned h = tf32_rna(w);
-                const unsigned l = tf32_rna(w - __uint_as_float(h));
-                const int off = b_offset(rr, u);
-                *reinterpret_cast<unsigned*>(B_hi + off) = h;
-                *reinterpret_cast<unsigned*>(B_lo + off) = l;
-              }
-              asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            }
-            for (int q = 0; q < CHB - 1; ++q) write_chunk(row, mb, q);
-          } else if (b >= 2 && j >= 2) {
-            // the slot of chunk j + 4 last held chunk j - 2, read by block j - 2
-            bar_wait(&mma_done[(b - 2) & 1], (unsigned)(((b - 2) >> 1) & 1));
-            fence_after();
-          } else if (j == 1 && b >= 2) {
-            bar_wait(&mma_done[(b - 2) & 1], (unsigned)(((b - 2) >> 1) & 1));
-            fence_after();
-          }
-          write_chunk(row, mb, j + CHB - 1);
-          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+          const int dbuf = (int)(b & 1);
+          RC_WAIT(3, &mma_done[dbuf], (unsigned)((b >> 1) & 1));
+          fence_after();
+          float v[32], v1[32];
+          tmem_ld32(tmem + lane_addr + COL_D + dbuf * (NCHAIN * NOUT), v);
+          tmem_ld32(tmem + lane_addr + COL_D + dbuf * (NCHAIN * NOUT) + NOUT, v1);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] += v1[k];
           fence_before();
           __syncwarp();
-          if (lane == 0) bar_arrive(&block_ready[b & 1]);
-          // epilogue of the previous block overlaps this block's MMAs
-          if (b >= 1) epilogue(b - 1, prev_row, prev_mb, prev_j);
-          prev_row = row; prev_mb = mb; prev_j = j;
+          if (lane == 0) {
+            bar_arrive(&d_empty[dbuf]);
+#ifdef TIDAS_RC_PROF
+            const long long t_ = clock64();
+#endif
+            asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(OSLAB - 1) : "memory");  // slab free
+#ifdef TIDAS_RC_PROF
+            rc_prof[7] += (unsigned long long)(clock64() - t_);
+#endif
+          }
+          __syncwarp();
+          unsigned char* slab = O_st + (qw * OSLAB + (int)(b % OSLAB)) * 4096;
+          unsigned char* rowp = slab + lane * 128;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<float4*>(rowp + ((k ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          __syncwarp();
+          // TMA clips maps >= batch and outputs >= nx
+          if (lane == 0) tma_store_3d(&omap, slab, j * NOUT, row, mb * MAPS + qw * 32);
         }
       }
     }
-    if (b >= 1) epilogue(b - 1, prev_row, prev_mb, prev_j);
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ===== TMA producer: A chunks in consumption order, NSTAGE ahead
     if (lane == 0) {
       long long gp = 0;
       for (int r = 0; r < rows_mine; ++r) {
-        const int row = (int)blockIdx.x + r * (int)gridDim.x;
+        const int row = row0 + r;
         for (int mb = 0; mb < n_mb; ++mb) {
-          for (int q = 0; q < n_xb + CHB - 1; ++q, ++gp) {
+          for (int q = 0; q < S; ++q, ++gp) {
             const int st = (int)(gp % NSTAGE);
-            if (gp >= NSTAGE) bar_wait(&a_empty[st], (unsigned)(((gp / NSTAGE) - 1) & 1));
+            if (gp >= NSTAGE) RC_WAIT(4, &a_empty[st], (unsigned)(((gp / NSTAGE) - 1) & 1));
             bar_expect_tx(&a_full[st], A_STAGE);
             tma_load_3d(A_st + st * A_STAGE, &tmap, q * CH - HALO, row, mb * MAPS, &a_full[st]);
           }
@@ -331,38 +373,55 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc_kernel(const __grid_co
       }
     }
     __syncwarp();
-  } else if (warp == 4) {
-    // ===== MMA issuer (one elected thread)
-    const unsigned bh = su32(B_hi), bl = su32(B_lo);
+  } else {
+    // ===== MMA issuer (warp 8; one lane elected per instruction inside the asm)
     long long b = 0;
     for (int r = 0; r < rows_mine; ++r) {
+      const unsigned bh = su32(B_st + (r & 1) * 2 * B_BYTES), bl = bh + B_BYTES;
+      const uint64_t dbh0 = smem_desc_sw128(bh), dbl0 = smem_desc_sw128(bl);
+      const unsigned bh_lo = (unsigned)dbh0, bl_lo = (unsigned)dbl0, b_hi = (unsigned)(dbh0 >> 32);
       for (int mb = 0; mb < n_mb; ++mb) {
+        const long long g0 = ((long long)r * n_mb + mb) * S;
         for (int j = 0; j < n_xb; ++j, ++b) {
-          bar_wait(&block_ready[b & 1], (unsigned)((b >> 1) & 1));
-          if (b >= 2) bar_wait(&d_empty[b & 1], (unsigned)(((b - 2) >> 1) & 1));
-          fence_after();
-          {
-            const unsigned d = tmem + COL_D + (unsigned)(b & 1) * NOUT;
-            const uint64_t dbh0 = smem_desc_sw128(bh), dbl0 = smem_desc_sw128(bl);
-#pragma unroll
-            for (int c = 0; c < CHB; ++c) {  // 32-input chunk c of the K span (TMEM ring slot)
-              const int slot = (j + c) % RING;
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {  // K-steps of 8 inputs
-                const unsigned ac = (unsigned)(slot * CH + t * 8);
-                const uint64_t boff = (uint64_t)((c * B_ATOM + t * 32) >> 4);  // descriptor start field
-                mma_tf32_warp(d, tmem + COL_HI + ac, dbh0 + boff, (c | t) != 0);
-                mma_tf32_warp(d, tmem + COL_HI + ac, dbl0 + boff, 1);
-                mma_tf32_warp(d, tmem + COL_LO + ac, dbh0 + boff, 1);
-              }
-            }
-            mma_commit_warp(&mma_done[b & 1]);
+          for (int c = (j == 0 ? 0 : CHB - 1); c < CHB; ++c) {
+            const long long g = g0 + j + c;
+            RC_WAIT(5, &c_full[(int)(g % RING)], (unsigned)((g / RING) & 1));
           }
+          if (b >= 2) RC_WAIT(6, &d_empty[b & 1], (unsigned)(((b - 2) >> 1) & 1));
+          fence_after();
+          // all 512 columns are allocated, so the TMEM base is column 0 (checked
+          // above); constant addresses keep the MMA operands in uniform registers
+          // two accumulators per block, MMAs alternating between them, so
+          // consecutive MMAs do not wait on each other's accumulator
+          const unsigned d0 = COL_D + (unsigned)(b & 1) * (NCHAIN * NOUT), d1 = d0 + NOUT;
+          const int s0 = (int)((g0 + j) % RING);
+          int slot = s0;
+#pragma unroll 1
+          for (int c = 0; c < (diag ? 0 : CHB); ++c) {  // 32-input chunk c of the K span
+            const unsigned a_hi = COL_HI + (unsigned)slot * CH, a_lo = COL_LO + (unsigned)slot * CH;
+            const unsigned bo = (unsigned)c * (B_ATOM >> 4);
+            const bool first = (c == 0);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {  // K-steps of 8 inputs: 12 MMAs alternate d0 / d1
+              const unsigned kb = bo + (unsigned)t * 2;  // +32 bytes of K per step
+              mma_tf32_warp2((3 * t) & 1 ? d1 : d0, a_hi + t * 8, bh_lo + kb, b_hi, !(first && t == 0));
+              mma_tf32_warp2((3 * t + 1) & 1 ? d1 : d0, a_hi + t * 8, bl_lo + kb, b_hi, !(first && t == 0));
+              mma_tf32_warp2((3 * t + 2) & 1 ? d1 : d0, a_lo + t * 8, bh_lo + kb, b_hi, true);
+            }
+            slot = (slot + 1 == RING) ? 0 : slot + 1;
+          }
+          mma_commit_warp(&mma_done[b & 1]);
+          // chunk g0 + j has no later reader; the last block frees the segment's tail
+          mma_commit_warp(&c_free[s0]);
+          if (j == n_xb - 1)
+            for (int c = 1; c < CHB; ++c) mma_commit_warp(&c_free[(s0 + c) % RING]);
           __syncwarp();
         }
       }
+      mma_commit_warp(&row_done[r & 1]);
     }
   }
+  RC_PROF_FLUSH(warp)
   fence_before();
   __syncthreads();
   fence_after();
@@ -407,11 +466,13 @@ int launch_rowconv_tc(const float* in, const float* K, float* out, int64_t batch
   if (r2 != CUDA_SUCCESS) return TIDAS_EUNSUPPORTED;
   // ask for more shared memory than two CTAs could share, so each SM holds one
   // CTA and its 512 TMEM columns are never contended
-  const size_t smem = 2 * B_BYTES + NSTAGE * A_STAGE + 8 * 4096 + 1024;
+  const size_t smem = 4 * B_BYTES + NSTAGE * A_STAGE + 4 * OSLAB * 4096 + 1024;
   auto kern = rowconv_tc_kernel<ADJ>;
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = nz < sms ? nz : sms;
-  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, out, (int)batch, nz, nx, T);
+  const int rows_per = (nz + sms - 1) / sms;
+  const int grid = (nz + rows_per - 1) / rows_per;  // every CTA gets a band of rows_per rows (last: fewer)
+    static const int diag = getenv("TIDAS_ROWCONV_DIAG") ? atoi(getenv("TIDAS_ROWCONV_DIAG")) : 0;  // 1: data only
+  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, (int)batch, nz, nx, T, rows_per, diag);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
 }

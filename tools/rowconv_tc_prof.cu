@@ -1,0 +1,44 @@
+// Wait-time breakdown of the tcgen05 row operator per warp role (cfg4 forward).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DTIDAS_RC_PROF -I paper_2507_15464_b200/csrc \
+//        -o tools/bin/rowconv_tc_prof tools/rowconv_tc_prof.cu \
+//        paper_2507_15464_b200/csrc/api.cu -lcuda
+#include "../paper_2507_15464_b200/csrc/rowconv_tc.cu"
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+int main(int argc, char** argv) {
+  const int B = 256, nz = 2048, nx = 1024, T = 129;
+  float *in, *K, *out;
+  cudaMalloc(&in, (size_t)B * nz * nx * 4);
+  cudaMalloc(&out, (size_t)B * nz * nx * 4);
+  cudaMalloc(&K, (size_t)nz * T * 4);
+  cudaMemset(in, 0, (size_t)B * nz * nx * 4);
+  cudaMemset(K, 0, (size_t)nz * T * 4);
+  for (int i = 0; i < 2; ++i) tidas::launch_rowconv_tc<false>(in, K, out, B, nz, nx, T, 0);
+  cudaDeviceSynchronize();
+  unsigned long long z[16][16];
+  memset(z, 0, sizeof(z));
+  cudaMemcpyToSymbol(tidas::tc::g_rc_prof, z, sizeof(z));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  const int rc = tidas::launch_rowconv_tc<false>(in, K, out, B, nz, nx, T, 0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaMemcpyFromSymbol(z, tidas::tc::g_rc_prof, sizeof(z));
+  printf("rc=%d  %.3f ms  (%s)\n", rc, ms, cudaGetErrorString(cudaGetLastError()));
+  const char* site[10] = {"row_done", "c_free", "a_full", "mma_done", "a_empty", "c_full", "d_empty", "st_read", "-", "TOTAL"};
+  const char* role[10] = {"conv0", "conv1", "conv2", "conv3", "epi0", "epi1", "epi2", "epi3", "mma", "tma"};
+  for (int w = 0; w < 10; ++w) {
+    printf("%-6s", role[w]);
+    const double tot = (double)z[w][9];
+    for (int k = 0; k < 8; ++k)
+      if (z[w][k]) printf("  %s %4.1f%%", site[k], 100.0 * z[w][k] / tot);
+    printf("  | total %.0f cyc/CTA\n", tot / 147);
+  }
+  return 0;
+}
