@@ -142,11 +142,9 @@ int launch_rowconv_tc(const float* in, const float* K, float* out, int64_t batch
 
 // TIDAS_ROWCONV_PATH=simt forces the CUDA-core kernel (tests compare both paths)
 static bool rowconv_tc_enabled() {
-  static int v = [] {
-    const char* e = getenv("TIDAS_ROWCONV_PATH");
-    return (e && std::string(e) == "simt") ? 0 : 1;
-  }();
-  return v != 0;
+  // read per call (cheap next to a launch) so one process can compare both paths
+  const char* e = getenv("TIDAS_ROWCONV_PATH");
+  return !(e && std::string(e) == "simt");
 }
 
 template <bool ADJ>

@@ -55,6 +55,67 @@ def test_rowconv_cfg4_map_size_and_adjoint_identity(rng):
     assert abs(lhs - rhs) / scale < 1e-6
 
 
+# tensor-core path (tcgen05 3xTF32, batch >= 32): ragged map blocks (B not a
+# multiple of 128), ragged column blocks (nx not a multiple of 32), short and
+# full-width kernels. Tolerance: 2e-6 relative L2 vs the float64 oracle (the
+# split drops the lo*lo term, ~2^-22 relative per product).
+@pytest.mark.parametrize("shape", [(128, 3, 256), (40, 5, 100), (33, 2, 36), (200, 3, 1024), (257, 2, 64)])
+@pytest.mark.parametrize("taps", [129, 31, 1])
+def test_rowconv_tensor_core_path_vs_oracle(shape, taps, rng):
+    B, nz, nx = shape
+    g = sparse_maps(rng, B, nz, nx, 0.2)
+    K = rng.standard_normal((nz, taps)).astype(np.float32)
+    Kd, gd = torch.as_tensor(K).to(DEV), torch.as_tensor(g).to(DEV)
+    y = tb.tidas_rowconv(gd, Kd).cpu().numpy()
+    assert od.rel_l2(y, ot.rowconv_fwd(g, K)) < 2e-6
+    a = tb.tidas_rowconv_adjoint(gd, Kd).cpu().numpy()
+    assert od.rel_l2(a, ot.rowconv_adj(g, K)) < 2e-6
+
+
+def test_rowconv_tensor_core_matches_cuda_core_path(rng, monkeypatch):
+    B, nz, nx, T = 96, 16, 512, 129
+    g = torch.as_tensor(sparse_maps(rng, B, nz, nx, 0.05)).to(DEV)
+    K = torch.as_tensor(rng.standard_normal((nz, T)).astype(np.float32) / 8).to(DEV)
+    y_tc, a_tc = tb.tidas_rowconv(g, K), tb.tidas_rowconv_adjoint(g, K)
+    monkeypatch.setenv("TIDAS_ROWCONV_PATH", "simt")
+    y_s, a_s = tb.tidas_rowconv(g, K), tb.tidas_rowconv_adjoint(g, K)
+    for u, v in ((y_tc, y_s), (a_tc, a_s)):
+        assert (torch.linalg.norm((u - v).double()) / torch.linalg.norm(v.double())).item() < 2e-6
+
+
+@pytest.mark.parametrize("shape,taps", [((64, 3, 30), 129), ((64, 2, 256), 131)])
+def test_rowconv_shapes_outside_tensor_path_fall_back(shape, taps, rng):
+    # nx % 4 != 0 (TMA row pitch) and taps > 129 run on the CUDA-core kernels
+    B, nz, nx = shape
+    g = sparse_maps(rng, B, nz, nx, 0.2)
+    K = rng.standard_normal((nz, taps)).astype(np.float32)
+    y = tb.tidas_rowconv(torch.as_tensor(g).to(DEV), torch.as_tensor(K).to(DEV)).cpu().numpy()
+    assert od.rel_l2(y, ot.rowconv_fwd(g, K)) < 1e-6
+
+
+def test_rowconv_cfg4_full_batch_tensor_core_adjoint_identity():
+    # all 256 cfg4 maps through the tensor path: <A g, y> = <g, A^T y>
+    cfg = CFG4
+    B, nz, nx, T = 256, cfg["nz"], cfg["nx"], cfg["taps"]
+    gen = torch.Generator(device=DEV).manual_seed(3)
+    g = (torch.rand((B, nz, nx), device=DEV, generator=gen) < cfg["density"]).float() * \
+        torch.randn((B, nz, nx), device=DEV, generator=gen)
+    yv = torch.randn((B, nz, nx), device=DEV, generator=gen)
+    K = torch.randn((nz, T), device=DEV, generator=gen) / 8
+    Ag = tb.tidas_rowconv(g, K)
+    lhs = torch.sum(Ag.double() * yv.double()).item()
+    del Ag
+    Aty = tb.tidas_rowconv_adjoint(yv, K)
+    rhs = torch.sum(g.double() * Aty.double()).item()
+    scale = torch.linalg.norm(g.double()).item() * torch.linalg.norm(yv.double()).item() * \
+        torch.linalg.norm(K.double()).item()
+    assert abs(lhs - rhs) / scale < 1e-6
+    # one map against the oracle at full size
+    g0 = g[:1].cpu().numpy()
+    y0 = tb.tidas_rowconv(g, K)[:1].cpu().numpy()
+    assert od.rel_l2(y0, ot.rowconv_fwd(g0, K.cpu().numpy())) < 2e-6
+
+
 def test_rowconv_rejects_bad_taps():
     with pytest.raises(ValueError):
         tb.tidas_rowconv(torch.zeros((1, 2, 8), device=DEV), torch.zeros((2, 4), device=DEV))
