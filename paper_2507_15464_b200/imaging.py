@@ -213,3 +213,87 @@ def das_image(rf: torch.Tensor, plan: DasPlan, *, scale: float = 1.0, out=None,
 def launches_per_call(F: int, plan: DasPlan, workspace: DasWorkspace) -> int:
     """Number of library kernels ``das_image`` launches for F frames."""
     return 2 * ((F + workspace.chunk - 1) // workspace.chunk)
+
+
+class HostPipeline:
+    """Host-to-host DAS with copy/compute overlap (the ingest path of a scanner).
+
+    RF frames arrive in pinned host memory and images go back to pinned host
+    memory. Three CUDA streams (host->device, compute, device->host) work on
+    double-buffered chunks of ``chunk`` frames, ordered only by events, so the
+    PCIe upload of chunk i+1, the K1 + K2 kernels of chunk i and the download of
+    chunk i-1 run concurrently - within one call and across consecutive calls.
+    ``run`` returns once the work is enqueued; ``synchronize`` (or ``join`` on a
+    stream) waits for it.
+    """
+
+    def __init__(self, plan: DasPlan, *, chunk: int = 16, rf_dtype=torch.float32, device=None):
+        device = torch.device(device) if device is not None else plan.x.device
+        self.plan, self.chunk = plan, int(chunk)
+        out_dt = _COMPLEX[plan.prec_code] if plan.out == "iq" else _REAL[plan.prec_code]
+        self.rf_dev = [torch.empty((self.chunk, plan.n_angles, plan.n_el, plan.n_samples), dtype=rf_dtype,
+                                   device=device) for _ in range(2)]
+        self.img_dev = [torch.empty((self.chunk, plan.nz, plan.nx), dtype=out_dt, device=device)
+                        for _ in range(2)]
+        self.ws = DasWorkspace(plan, device)
+        self.s_in, self.s_cmp, self.s_out = (torch.cuda.Stream(device) for _ in range(3))
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]
+        self.ev_cmp = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.n = 0  # chunks issued so far (buffer = n % 2)
+
+    def wait_for(self, stream) -> None:
+        """Order the pipeline's next work after everything already on ``stream``."""
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        for s in (self.s_in, self.s_cmp, self.s_out):
+            s.wait_event(ev)
+
+    def join(self, stream) -> None:
+        """Make ``stream`` wait for all pipeline work issued so far."""
+        for s in (self.s_in, self.s_cmp, self.s_out):
+            ev = torch.cuda.Event()
+            ev.record(s)
+            stream.wait_event(ev)
+
+    def synchronize(self) -> None:
+        for s in (self.s_in, self.s_cmp, self.s_out):
+            s.synchronize()
+
+    def run(self, rf_host: torch.Tensor, out_host: torch.Tensor, *, scale: float = 1.0) -> torch.Tensor:
+        """rf_host [F][A][E][N] (pinned) -> out_host [F][nz][nx] (pinned), asynchronously."""
+        if rf_host.dim() == 3:
+            rf_host = rf_host.unsqueeze(1)
+        if rf_host.is_cuda or out_host.is_cuda:
+            raise ValueError("HostPipeline.run takes host tensors (use das_image for device tensors)")
+        if rf_host.dtype != self.rf_dev[0].dtype:
+            raise ValueError(f"rf dtype {rf_host.dtype} != pipeline rf dtype {self.rf_dev[0].dtype}")
+        F = int(rf_host.shape[0])
+        if tuple(rf_host.shape[1:]) != tuple(self.rf_dev[0].shape[1:]) or \
+                tuple(out_host.shape) != (F, self.plan.nz, self.plan.nx):
+            raise ValueError(f"rf {tuple(rf_host.shape)} / out {tuple(out_host.shape)} do not match the plan "
+                             f"([F]{tuple(self.rf_dev[0].shape[1:])} -> [F][{self.plan.nz}][{self.plan.nx}])")
+        for f0 in range(0, F, self.chunk):
+            f1 = min(F, f0 + self.chunk)
+            k, b = f1 - f0, self.n % 2
+            if self.n >= 2:
+                self.s_in.wait_event(self.ev_cmp[b])      # rf_dev[b] consumed by chunk n-2
+                self.s_cmp.wait_event(self.ev_out[b])     # img_dev[b] downloaded
+            with torch.cuda.stream(self.s_in):
+                self.rf_dev[b][:k].copy_(rf_host[f0:f1], non_blocking=True)
+            self.ev_in[b].record(self.s_in)
+            self.s_cmp.wait_event(self.ev_in[b])
+            das_image(self.rf_dev[b][:k], self.plan, scale=scale, out=self.img_dev[b][:k], workspace=self.ws,
+                      stream=self.s_cmp)
+            self.ev_cmp[b].record(self.s_cmp)
+            self.s_out.wait_event(self.ev_cmp[b])
+            with torch.cuda.stream(self.s_out):
+                out_host[f0:f1].copy_(self.img_dev[b][:k], non_blocking=True)
+            self.ev_out[b].record(self.s_out)
+            self.n += 1
+        return out_host
+
+    def launches(self, F: int) -> int:
+        """Library kernels one ``run`` of F frames launches."""
+        per = launches_per_call(min(F, self.chunk), self.plan, self.ws)
+        return per * ((F + self.chunk - 1) // self.chunk)
