@@ -12,19 +12,23 @@
 //   value = (1-f) |C(k0)| + f |C(k0+1)|
 // so each (pixel, channel) reads three consecutive complex samples.
 //
-// Layout / schedule (B200):
-//   * CTA = 32 depths (lanes) x 8 columns (warps); each thread owns one pixel
-//     for FB frames, so the time-of-flight math (FP32, cancellation-free
+// Layout / schedule (B200, default variant — case 0 of the variant table):
+//   * CTA = 8 consumer warps + 1 producer warp, 2 CTAs per SM. The consumers
+//     cover 32 depths x 8 columns; a warp covers 8 depths x 4 columns so the
+//     16 lanes of a half-warp read nearly coincident taps (shared-memory
+//     wavefronts ~1.5x the minimum). Each thread owns one pixel for FB = 8
+//     frames, so the time-of-flight math (FP32, cancellation-free
 //     s = -dx^2 / (sqrt(dx^2 + z^2) + z) in sample units) is paid once per
-//     (pixel, channel) and reused for FB frames.
+//     (pixel, channel) and reused for 8 frames.
 //   * The CTA's sample window per transmit (taps of its 256 pixels lie in
-//     [min k0 - 1, max (k0 - floor(s_min)) + 1], ~150-200 samples, the same for
-//     every channel) is copied global->shared per channel by TMA bulk copies
-//     (cp.async.bulk + mbarrier, one issuing thread), triple-buffered two
-//     channels ahead with one barrier per channel; the 3 taps per pixel are
-//     shared-memory reads and the tile's 8 columns reuse one window.
-//   * Warps cover 8 depths x 4 columns so the 16 lanes of a half-warp read
-//     nearly coincident taps (shared-memory wavefronts ~1.5x the minimum).
+//     [min k0 - 1, max (k0 - floor(s_min)) + 1], <= 256 samples, the same for
+//     every channel) is fetched by the producer warp as ONE TMA tensor copy
+//     per 2 channels: a box [8 frames][2 channels][256 samples] of the 4-D
+//     tensor map over the analytic RF [F][A][E][N] (complex64 as 8-byte
+//     elements). Three such buffers rotate under full / empty mbarriers (the
+//     consumers arrive per warp on "empty"), so no CTA-wide barrier sits in
+//     the channel loop and the copy of channels c+2, c+3 overlaps the gather
+//     of channels c, c+1.
 //   * t* (one per pixel and transmit) is precomputed in float64 (plane-wave
 //     table kernel or the host's focused-transmit table) and split into an
 //     integer sample index plus an FP32 fraction — the FP32 ulp at index 8192

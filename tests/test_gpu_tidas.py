@@ -55,11 +55,12 @@ def test_rowconv_cfg4_map_size_and_adjoint_identity(rng):
     assert abs(lhs - rhs) / scale < 1e-6
 
 
-# tensor-core path (tcgen05 3xTF32, batch >= 32): ragged map blocks (B not a
-# multiple of 128), ragged column blocks (nx not a multiple of 32), short and
-# full-width kernels. Tolerance: 2e-6 relative L2 vs the float64 oracle (the
-# split drops the lo*lo term, ~2^-22 relative per product).
-@pytest.mark.parametrize("shape", [(128, 3, 256), (40, 5, 100), (33, 2, 36), (200, 3, 1024), (257, 2, 64)])
+# tensor-core path (tcgen05 3xTF32, batch >= 32, nx % 32 == 0): ragged map
+# blocks (B not a multiple of 64), ragged column blocks (nx not a multiple of
+# the 64-output block), short and full-width kernels. Tolerance: 2e-6 relative
+# L2 vs the float64 oracle (the split drops the lo*lo term and truncates lo,
+# ~2^-21 relative per product).
+@pytest.mark.parametrize("shape", [(128, 3, 256), (40, 5, 96), (33, 2, 32), (200, 3, 1024), (257, 2, 64)])
 @pytest.mark.parametrize("taps", [129, 31, 1])
 def test_rowconv_tensor_core_path_vs_oracle(shape, taps, rng):
     B, nz, nx = shape
@@ -83,9 +84,9 @@ def test_rowconv_tensor_core_matches_cuda_core_path(rng, monkeypatch):
         assert (torch.linalg.norm((u - v).double()) / torch.linalg.norm(v.double())).item() < 2e-6
 
 
-@pytest.mark.parametrize("shape,taps", [((64, 3, 30), 129), ((64, 2, 256), 131)])
+@pytest.mark.parametrize("shape,taps", [((64, 3, 30), 129), ((40, 5, 100), 129), ((64, 2, 256), 131)])
 def test_rowconv_shapes_outside_tensor_path_fall_back(shape, taps, rng):
-    # nx % 4 != 0 (TMA row pitch) and taps > 129 run on the CUDA-core kernels
+    # nx % 32 != 0 (whole 32-input chunks) and taps > 129 run on the CUDA-core kernels
     B, nz, nx = shape
     g = sparse_maps(rng, B, nz, nx, 0.2)
     K = rng.standard_normal((nz, taps)).astype(np.float32)

@@ -32,8 +32,10 @@ int main(int argc, char** argv) {
   cudaMemcpyFromSymbol(z, tidas::tc::g_rc_prof, sizeof(z));
   printf("rc=%d  %.3f ms  (%s)\n", rc, ms, cudaGetErrorString(cudaGetLastError()));
   const char* site[10] = {"row_done", "c_free", "a_full", "mma_done", "a_empty", "c_full", "d_empty", "st_read", "-", "TOTAL"};
-  const char* role[10] = {"conv0", "conv1", "conv2", "conv3", "epi0", "epi1", "epi2", "epi3", "mma", "tma"};
-  for (int w = 0; w < 10; ++w) {
+  const char* role[16] = {"conv0", "conv1", "conv2", "conv3", "epi0", "epi1", "epi2", "epi3", "mma", "tma",
+                          "idle", "idle", "conv4", "conv5", "conv6", "conv7"};
+  for (int w = 0; w < 16; ++w) {
+    if (w == 10 || w == 11) continue;
     printf("%-6s", role[w]);
     const double tot = (double)z[w][9];
     for (int k = 0; k < 8; ++k)
