@@ -222,3 +222,55 @@ def test_build_row_kernels_theta_identity():
     r = ot.neighbourhood_reference_rows(10, 4)
     assert list(r) == [2, 2, 2, 2, 6, 6, 6, 6, 9, 9]
     assert th4[2] == pytest.approx(1.0) and th4[6] == pytest.approx(1.0)
+
+
+# ------------------------------------------------ FFT theta estimator (§8(f)1)
+
+from oracle import theta as oth  # noqa: E402
+
+
+def read_matrix_csv(name):
+    """Depth-indexed matrix written by save_matrix_csv (tidas.py:105-117)."""
+    rows = list(csv.reader(open(GOLDEN / "fixtures" / name)))
+    cols = np.array([float(v) for v in rows[0][1:]])
+    refs = np.array([float(r[0]) for r in rows[1:]])
+    vals = np.array([[float(v) for v in r[1:]] for r in rows[1:]])
+    return refs, cols, vals
+
+
+def assert_matches_9g(ours, csv_vals):
+    """Equal to the CSV's 9 significant digits, NaN pattern identical."""
+    assert np.array_equal(np.isnan(ours), np.isnan(csv_vals))
+    ok = ~np.isnan(csv_vals)
+    np.testing.assert_allclose(ours[ok], csv_vals[ok], rtol=1e-8, atol=0.0)
+
+
+def test_oracle_error_sweep_reproduces_fixtures(ref_vectors):
+    """theta_matrix / error_local / error_global / error_mask CSVs of
+    run_error_sweep (experiments.py:334-361) at the fixture config: 40 depths
+    5-42 mm, 7 MHz, Tx focus 25 mm, Kossoff 0.6, F#1, eps from the focal FWHM."""
+    refs, cols, th_csv = read_matrix_csv("theta_matrix.csv")
+    _, _, loc_csv = read_matrix_csv("error_local.csv")
+    _, _, glo_csv = read_matrix_csv("error_global.csv")
+    _, _, mask_csv = read_matrix_csv("error_mask.csv")
+    depths = np.linspace(0.005, 0.042, 40)
+    np.testing.assert_allclose(cols, depths, rtol=1e-8)
+    th, loc, glo = oth.error_sweep(depths, depths, REF_PROBE, tx_focus=25e-3,
+                                   half_width=float(ref_vectors["eps"]))
+    assert_matches_9g(th, th_csv)
+    assert_matches_9g(loc, loc_csv)
+    assert_matches_9g(glo, glo_csv)
+    mask = np.where(np.isfinite(loc), (loc < 0.05).astype(float), np.nan)
+    assert np.array_equal(mask, mask_csv, equal_nan=True)
+
+
+@pytest.mark.parametrize("form,key", [("beamsum", "F_theta_sweep"), ("per_element", "F_theta_sweep_pe")])
+def test_oracle_theta_matrix_sweep_golden(ref_vectors, form, key):
+    """theta_matrix_sweep (tidas.py:394-425), both estimator forms, vs the reference."""
+    d = ref_vectors["F_depths"]
+    ours = oth.theta_matrix_sweep(d, REF_PROBE, tx_focus=25e-3, half_width=float(ref_vectors["eps"]),
+                                  form=form)
+    ref = ref_vectors[key]
+    assert np.array_equal(np.isnan(ours), np.isnan(ref))
+    ok = ~np.isnan(ref)
+    np.testing.assert_allclose(ours[ok], ref[ok], rtol=1e-11, atol=1e-13)
