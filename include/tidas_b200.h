@@ -174,6 +174,47 @@ int tidas_synthesize(const double* sx, const double* sz, const double* amp, cons
                      int32_t spreading, int32_t n_samples, void* out, int out_dtype,
                      void* stream);
 
+/* ------------------------------------------------------------------------
+ * FFT theta estimator and theta / error sweeps, float64.
+ * ------------------------------------------------------------------------ */
+
+/* Zero frames [n_frames][n_rows][n_samples] outside [lo[f], hi[f]) in place and
+ * report per row the first / last nonzero sample inside (-1 if none).
+ * Replaces: window_signals (tidas.py:150-168) + the support scan of
+ * _windowed_spectra (tidas.py:214-218). */
+int tidas_window_frames_f64(double* frames, int32_t n_frames, int32_t n_rows, int32_t n_samples,
+                            const int32_t* lo, const int32_t* hi, int32_t* first, int32_t* last,
+                            void* stream);
+
+/* One-sided spectra, bins [0, nfft/2) (Nyquist dropped), of the segments
+ * frames[pair_frame[p]][rows[p][e]][pair_lo[p], pair_hi[p]) zero-padded to
+ * pair_nfft[p]; written as complex128 to spectra[(pair_off[p] + e) * kmax + k].
+ * Replaces: the rfft of _windowed_spectra (tidas.py:198-234). */
+int tidas_window_spectra_f64(const double* frames, int32_t n_rows, int32_t n_samples, int32_t n_pairs,
+                             const int32_t* pair_frame, const int32_t* pair_lo, const int32_t* pair_hi,
+                             const int32_t* pair_nfft, const int64_t* pair_off, const int32_t* rows,
+                             int32_t max_rows, const int32_t* count, int32_t kmax, void* spectra,
+                             void* stream);
+
+/* theta per cell from the cached spectra of its pair; d_fixed / d_true [cell][max_rows]
+ * are the rebased delays in samples; form 0 = beamsum, 1 = per_element; status 1
+ * = zero denominator (the reference's ZeroDivisionError), theta NaN.
+ * Replaces: estimate_theta (tidas.py:237-283) incl. _delay_phases (tidas.py:180-195). */
+int tidas_theta_cells_f64(const void* spectra, int32_t n_cells, const int32_t* cell_pair,
+                          const int64_t* pair_off, const int32_t* pair_nfft, const int32_t* count,
+                          int32_t kmax, const double* d_fixed, const double* d_true, int32_t max_rows,
+                          int32_t form, double* theta, int32_t* status, void* stream);
+
+/* Per cell c: cand = theta[c] * sums[c][k] on [crop_lo[c], crop_hi[c]) (0 elsewhere),
+ * ref = refs[cell_col[c]][k]; out[c] = {sum_win (cand-ref)^2, sum_win ref^2,
+ * sum_all (cand-ref)^2, sum_all ref^2}, window [win_lo, win_hi) and length n_len
+ * of the column. Replaces: local_error / global_error (metrics.py:92-112) of
+ * the error sweep (experiments.py:320-328). */
+int tidas_psf_errors_f64(const double* sums, int32_t n_samples, const double* theta, const double* refs,
+                         int32_t n_cells, const int32_t* cell_col, const int32_t* crop_lo,
+                         const int32_t* crop_hi, const int32_t* n_len, const int32_t* win_lo,
+                         const int32_t* win_hi, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@ from .metrics import (MetricsReport, envelope, fwhm, global_error, local_error, 
 from .tidas import (ThetaMatrix, TimeWindow, build_row_kernels, estimate_theta_aligned,
                     fwhm_window, lateral_psfs, rasterize, theta_row_aligned, tidas_line,
                     tidas_psf, tidas_rowconv, tidas_rowconv_adjoint, window_signals)
+from .sweep import error_sweep, estimate_theta, theta_matrix_sweep
 from .imaging import (DasPlan, DasWorkspace, HostPipeline, das_from_analytic, das_image, plane_wave_plan,
                       rf_analytic, table_plan)
 

@@ -47,6 +47,11 @@ SIGNATURES = {
     "tidas_window_dots_f64": ([_P, _P, _I32, _P, _P, _I32, _P, _P], C.c_int),
     "tidas_rowconv_fwd_f32": ([_P, _P, _P, _I64, _I32, _I32, _I32, _P], C.c_int),
     "tidas_rowconv_adj_f32": ([_P, _P, _P, _I64, _I32, _I32, _I32, _P], C.c_int),
+    "tidas_window_frames_f64": ([_P, _I32, _I32, _I32, _P, _P, _P, _P, _P], C.c_int),
+    "tidas_window_spectra_f64": ([_P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _I32, _P, _P],
+                                 C.c_int),
+    "tidas_theta_cells_f64": ([_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _P], C.c_int),
+    "tidas_psf_errors_f64": ([_P, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "tidas_synthesize": ([_P, _P, _P, _P, _I32, _I32, _I32, _I32, _D, _D, _D, _D, _D, _I32,
                           _I32, _P, C.c_int, _P], C.c_int),
 }

@@ -1,0 +1,331 @@
+"""FFT theta estimator and the theta / error sweeps on the GPU.
+
+Drop-ins for the reference's
+  estimate_theta      tidas.py:237-283 (with _windowed_spectra / _delay_phases)
+  theta_matrix_sweep  tidas.py:394-425 (one single-scatterer frame per column)
+and ``error_sweep``, the (theta, local error, global error) matrices that
+``run_error_sweep`` (experiments.py:299-361) writes as theta_matrix.csv,
+error_local.csv, error_global.csv and error_mask.csv.
+
+All columns of a sweep are simulated in one launch (tidas_synthesize, FP64),
+windowed and support-scanned in one launch, their window spectra computed once
+per (column, FFT length) and cached in HBM, and every cell's theta computed by
+one CTA (tidas_theta_cells_f64). The error sweep adds the true-profile PSF per
+column and the cropped fixed-profile PSF per cell (K3, bit-identical to numpy)
+and one reduction per cell (tidas_psf_errors_f64). Host work is the geometry
+(apertures, delay profiles, FFT lengths) in float64 — O(cells x aperture).
+Failure cases become NaN cells exactly as in the reference.
+"""
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import das as _das
+from .geometry import (ApertureRule, DelayProfile, ProbeConfig, element_positions, rx_aperture,
+                       rx_delay_profile, tx_aperture)
+from .metrics import window_bounds
+from .simulate import RfFrame, _focused_arrivals, _synth_device, make_pulse
+
+FORMS = {"beamsum": 0, "per_element": 1}
+_COL_BATCH = 96  # columns per device batch (bounds the spectra / PSF scratch)
+
+
+def _next_pow2(n: int) -> int:
+    return 1 << max(int(n) - 1, 0).bit_length()
+
+
+def _dev():
+    _lib.lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _i32(a, dev):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32)).to(dev)
+
+
+def _f64(a, dev):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+
+class _Columns:
+    """Single on-axis scatterer frames (one per target depth), windowed on the device."""
+
+    def __init__(self, targets, config: ProbeConfig, tx_rule: ApertureRule, tx_focus: float,
+                 half_width: float, spreading: bool):
+        dev = _dev()
+        self.targets = np.asarray(targets, float)
+        T = len(self.targets)
+        c, fs, n_el = config.sound_speed, config.sampling_frequency, config.element_count
+        self.fs, self.n_el = fs, n_el
+        pulse = make_pulse(config)
+        ap = tx_aperture(tx_focus, tx_rule, config)
+        arr = _focused_arrivals(np.zeros(T), self.targets, tx_focus, ap, config)  # [T]
+        xs = element_positions(np.arange(-n_el // 2, n_el // 2), config)
+        dist = np.hypot(xs[None, :], self.targets[:, None])
+        # frame length of synthesize_frame (simulate.py:229)
+        self.n_len = (np.ceil(((arr[:, None] + dist / c).max(axis=1) + pulse.duration) * fs)).astype(np.int64) + 1
+        self.N = int(self.n_len.max())
+        frames = _synth_device(np.zeros((T, 1)), self.targets[:, None], np.ones((T, 1)), arr[:, None, None],
+                               n_frames=T, n_angles=1, n_el=n_el, pitch=config.pitch, c=c, fs=fs,
+                               f0=pulse.center_frequency, fbw=pulse.fractional_bandwidth,
+                               n_samples=self.N, spreading=spreading, dtype=torch.float64, device=dev)
+        # one extra all-zero row at the end: padding target for K3 profiles
+        flat = torch.zeros((T * n_el + 1, self.N), dtype=torch.float64, device=dev)
+        flat[: T * n_el] = frames.reshape(T * n_el, self.N)
+        del frames
+        self.flat = flat
+        self.zero_row = T * n_el
+        # window per column (tidas.py:150-168 / experiments.py:305-313): centred on
+        # the focused-transmit arrival + z / c (das.expected_arrival_time, and
+        # tx_arrival_times(...)[0] + z / c in tidas.py:369-371 — the same value)
+        centers = arr + self.targets / c
+        self.centers = centers
+        self.ok = np.ones(T, bool)
+        self.wlo = np.zeros(T, np.int32)
+        self.whi = np.zeros(T, np.int32)
+        for t in range(T):
+            n = int(self.n_len[t])
+            t_end = (n - 1) / fs
+            lo, hi = window_bounds(n, 0.0, fs, float(centers[t]), half_width)
+            if centers[t] - half_width < 0.0 or centers[t] + half_width > t_end or hi <= lo:
+                self.ok[t] = False
+                lo = hi = 0
+            self.wlo[t], self.whi[t] = lo, hi
+        first = torch.empty((T, n_el), dtype=torch.int32, device=dev)
+        last = torch.empty((T, n_el), dtype=torch.int32, device=dev)
+        lo_d, hi_d = _i32(self.wlo, dev), _i32(self.whi, dev)
+        L = _lib.lib()
+        for t0 in range(0, T, 65535):
+            t1 = min(T, t0 + 65535)
+            _lib.check(L.tidas_window_frames_f64(_lib.ptr(flat[t0 * n_el:]), t1 - t0, n_el, self.N,
+                                                 _lib.ptr(lo_d[t0:]), _lib.ptr(hi_d[t0:]),
+                                                 _lib.ptr(first[t0:]), _lib.ptr(last[t0:]),
+                                                 _lib.stream_handle()))
+        f, l_ = first.cpu().numpy(), last.cpu().numpy()
+        has = l_ >= 0
+        self.s_lo = np.where(has.any(1), np.where(has, f, np.iinfo(np.int32).max).min(1), 0).astype(np.int64)
+        self.s_hi = np.where(has.any(1), l_.max(1) + 1, 0).astype(np.int64)
+        self.has_support = has.any(1)
+
+
+def _theta_cells(cols: _Columns, cell_col: np.ndarray, idx_of_col, d_fix_of_cell, d_true_of_col,
+                 form: str) -> Tuple[np.ndarray, np.ndarray]:
+    """theta for cells (column, fixed delays) over their column's true profile.
+
+    idx_of_col[t]: element indices of the column's aperture; d_fix_of_cell[c] /
+    d_true_of_col[t]: delays in seconds. Returns (theta, nfft) per cell; NaN
+    where the reference raises (no support, zero denominator)."""
+    if form not in FORMS:
+        raise ValueError(f"unknown estimator form {form!r}")
+    dev = _dev()
+    L = _lib.lib()
+    C = len(cell_col)
+    fs = cols.fs
+    theta = np.full(C, np.nan)
+    nffts = np.zeros(C, np.int64)
+    good = np.array([cols.ok[t] and cols.has_support[t] for t in cell_col], bool)
+    A = max(len(idx_of_col[t]) for t in set(cell_col.tolist()))
+    dfx = np.zeros((C, A))
+    dtr = np.zeros((C, A))
+    for c in range(C):
+        t = int(cell_col[c])
+        df, dt = np.asarray(d_fix_of_cell[c], float), np.asarray(d_true_of_col[t], float)
+        off = min(df.min(), dt.min())
+        df, dt = df - off, dt - off
+        width = int(cols.s_hi[t] - cols.s_lo[t])
+        span = int(np.ceil(float(max(df.max(), dt.max())) * fs)) + 4
+        nffts[c] = _next_pow2(max(2 * width, width + span))
+        dfx[c, :len(df)] = df * fs
+        dtr[c, :len(dt)] = dt * fs
+    sel = np.flatnonzero(good)
+    if sel.size == 0:
+        return theta, nffts
+    # spectra pairs: distinct (column, nfft) among the good cells
+    keys = sorted({(int(cell_col[c]), int(nffts[c])) for c in sel})
+    pid = {k: i for i, k in enumerate(keys)}
+    P = len(keys)
+    kmax = max(n // 2 for _, n in keys)
+    rows = np.zeros((P, A), np.int32)
+    count = np.zeros(P, np.int32)
+    for i, (t, n) in enumerate(keys):
+        idx = np.asarray(idx_of_col[t], int)
+        rows[i, :len(idx)] = idx + cols.n_el // 2  # frame-relative row
+        count[i] = len(idx)
+    pair_frame = np.array([t for t, _ in keys], np.int32)
+    pair_lo = cols.s_lo[pair_frame].astype(np.int32)
+    pair_hi = cols.s_hi[pair_frame].astype(np.int32)
+    pair_nfft = np.array([n for _, n in keys], np.int32)
+    pair_off = (np.arange(P, dtype=np.int64) * A)
+    S = torch.empty((P * A, kmax), dtype=torch.complex128, device=dev)
+    keep = [_i32(pair_frame, dev), _i32(pair_lo, dev), _i32(pair_hi, dev), _i32(pair_nfft, dev),
+            torch.as_tensor(pair_off).to(dev), _i32(rows, dev), _i32(count, dev)]
+    for p0 in range(0, P, 65535):
+        p1 = min(P, p0 + 65535)
+        _lib.check(L.tidas_window_spectra_f64(
+            _lib.ptr(cols.flat), cols.n_el, cols.N, p1 - p0, _lib.ptr(keep[0][p0:]), _lib.ptr(keep[1][p0:]),
+            _lib.ptr(keep[2][p0:]), _lib.ptr(keep[3][p0:]), _lib.ptr(keep[4][p0:]), _lib.ptr(keep[5][p0:]),
+            A, _lib.ptr(keep[6][p0:]), kmax, _lib.ptr(S), _lib.stream_handle()))
+    cell_pair = np.array([pid[(int(cell_col[c]), int(nffts[c]))] for c in sel], np.int32)
+    th_d = torch.empty(sel.size, dtype=torch.float64, device=dev)
+    st_d = torch.empty(sel.size, dtype=torch.int32, device=dev)
+    cp_d, df_d, dt_d = _i32(cell_pair, dev), _f64(dfx[sel], dev), _f64(dtr[sel], dev)
+    _lib.check(L.tidas_theta_cells_f64(_lib.ptr(S), int(sel.size), _lib.ptr(cp_d), _lib.ptr(keep[4]),
+                                       _lib.ptr(keep[3]), _lib.ptr(keep[6]), kmax, _lib.ptr(df_d),
+                                       _lib.ptr(dt_d), A, FORMS[form], _lib.ptr(th_d), _lib.ptr(st_d),
+                                       _lib.stream_handle()))
+    theta[sel] = th_d.cpu().numpy()
+    return theta, nffts
+
+
+def _profiles(targets, refs, config, rx_rule):
+    idx_of_col, d_true, d_fix = [], [], []
+    for z in targets:
+        ap = rx_aperture(float(z), rx_rule, config)
+        idx_of_col.append(np.asarray(ap, int))
+        d_true.append(rx_delay_profile(float(z), ap, config).delays)
+        d_fix.append([rx_delay_profile(float(r), ap, config).delays for r in refs])
+    return idx_of_col, d_true, d_fix
+
+
+def theta_matrix_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, rx_rule: ApertureRule, *,
+                       tx_focus_depth: float, window_half_width: float,
+                       reference_depths: Optional[np.ndarray] = None, form: str = "beamsum",
+                       spreading: bool = True, workers: int = 1):
+    """theta for every (reference profile, single-scatterer depth) pair — tidas.py:394-425.
+
+    ``workers`` is accepted for signature compatibility (the GPU batches all cells)."""
+    from .tidas import ThetaMatrix
+    targets = np.asarray(depth_grid, dtype=float)
+    refs = targets if reference_depths is None else np.asarray(reference_depths, dtype=float)
+    values = np.full((len(refs), len(targets)), np.nan)
+    for b0 in range(0, len(targets), _COL_BATCH):
+        tb = targets[b0:b0 + _COL_BATCH]
+        cols = _Columns(tb, config, tx_rule, tx_focus_depth, window_half_width, spreading)
+        idx, d_true, d_fix = _profiles(tb, refs, config, rx_rule)
+        cell_col = np.repeat(np.arange(len(tb)), len(refs))
+        fix_cells = [d for t in range(len(tb)) for d in d_fix[t]]
+        th, _ = _theta_cells(cols, cell_col, idx, fix_cells, d_true, form)
+        values[:, b0:b0 + len(tb)] = th.reshape(len(tb), len(refs)).T
+        del cols
+    return ThetaMatrix(reference_depths=refs, target_depths=targets, values=values)
+
+
+def error_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, rx_rule: ApertureRule, *,
+                tx_focus_depth: float, window_half_width: float,
+                reference_depths: Optional[np.ndarray] = None, form: str = "beamsum",
+                spreading: bool = True, delay_method: str = "linear"):
+    """(theta, local error, global error) [reference][scatterer depth] matrices of
+    run_error_sweep (experiments.py:299-361); the below-5% mask is
+    ``np.where(np.isfinite(local), local < 0.05, nan)``."""
+    if delay_method != "linear":
+        raise NotImplementedError("the GPU error sweep implements delay_method='linear'")
+    dev = _dev()
+    L = _lib.lib()
+    targets = np.asarray(depth_grid, dtype=float)
+    refs = targets if reference_depths is None else np.asarray(reference_depths, dtype=float)
+    R, T = len(refs), len(targets)
+    th_m, loc_m, glo_m = (np.full((R, T), np.nan) for _ in range(3))
+    fs = config.sampling_frequency
+    for b0 in range(0, T, _COL_BATCH):
+        tb = targets[b0:b0 + _COL_BATCH]
+        Tb = len(tb)
+        cols = _Columns(tb, config, tx_rule, tx_focus_depth, window_half_width, spreading)
+        idx, d_true, d_fix = _profiles(tb, refs, config, rx_rule)
+        A = max(len(i) for i in idx)
+        half = config.element_count // 2
+        # true-profile PSF per column (das_psf of the windowed frame), K3
+        rows_t = np.full((Tb, A), cols.zero_row, np.int64)
+        sh_t = np.zeros((Tb, A))
+        for t in range(Tb):
+            n = len(idx[t])
+            rows_t[t, :n] = t * config.element_count + idx[t] + half
+            sh_t[t, :n] = np.asarray(d_true[t]) * fs
+        _das._count(int(sum(len(i) for i in idx)))
+        refs_d = _das._delayed_sums_dev(cols.flat, rows_t, sh_t)
+        cell_col = np.repeat(np.arange(Tb), R)
+        fix_cells = [d for t in range(Tb) for d in d_fix[t]]
+        th, _ = _theta_cells(cols, cell_col, idx, fix_cells, d_true, form)
+        th_m[:, b0:b0 + Tb] = th.reshape(Tb, R).T
+        sel = np.flatnonzero(np.isfinite(th))
+        if sel.size == 0:
+            continue
+        # fixed-profile sums on each cell's crop [lo - span, hi + 2) (tidas.py:336-349), K3
+        C = sel.size
+        rows_c = np.full((C, A), cols.zero_row, np.int64)
+        sh_c = np.zeros((C, A))
+        clo = np.zeros(C, np.int32)
+        chi = np.zeros(C, np.int32)
+        for j, c in enumerate(sel):
+            t = int(cell_col[c])
+            n = len(idx[t])
+            d = np.asarray(fix_cells[c], float)
+            rows_c[j, :n] = t * config.element_count + idx[t] + half
+            sh_c[j, :n] = d * fs
+            span = int(np.ceil(-d.min() * fs)) + 2
+            clo[j] = max(int(cols.wlo[t]) - span, 0)
+            chi[j] = min(int(cols.whi[t]) + 2, int(cols.n_len[t]))
+        _das._count(int(sum(len(idx[int(cell_col[c])]) for c in sel)))
+        sums = _das._delayed_sums_dev(cols.flat, rows_c, sh_c, lo=clo, hi=chi)
+        th_d = _f64(th[sel], dev)
+        cc_d = _i32(cell_col[sel], dev)
+        clo_d, chi_d = _i32(clo, dev), _i32(chi, dev)
+        n_d, wlo_d, whi_d = _i32(cols.n_len, dev), _i32(cols.wlo, dev), _i32(cols.whi, dev)
+        out = torch.empty((C, 4), dtype=torch.float64, device=dev)
+        _lib.check(L.tidas_psf_errors_f64(_lib.ptr(sums), cols.N, _lib.ptr(th_d), _lib.ptr(refs_d), C,
+                                          _lib.ptr(cc_d), _lib.ptr(clo_d), _lib.ptr(chi_d), _lib.ptr(n_d),
+                                          _lib.ptr(wlo_d), _lib.ptr(whi_d), _lib.ptr(out), _lib.stream_handle()))
+        e = out.cpu().numpy()
+        with np.errstate(divide="ignore", invalid="ignore"):
+            loc = np.where(e[:, 1] > 0.0, e[:, 0] / np.where(e[:, 1] > 0.0, e[:, 1], 1.0), np.nan)
+            glo = np.where(e[:, 3] > 0.0, e[:, 2] / np.where(e[:, 3] > 0.0, e[:, 3], 1.0), np.nan)
+        # a failing local_error (experiments.py:327) leaves the global error unset
+        glo = np.where(np.isfinite(loc), glo, np.nan)
+        r_idx, t_idx = sel % R, sel // R
+        loc_m[r_idx, b0 + t_idx] = loc
+        glo_m[r_idx, b0 + t_idx] = glo
+        del cols, sums, refs_d
+    return th_m, loc_m, glo_m
+
+
+def estimate_theta(windowed_frame: RfFrame, fixed_delays: DelayProfile, true_delays: DelayProfile,
+                   form: str = "beamsum", support: Optional[Tuple[int, int]] = None) -> float:
+    """Least-squares scaling weight over the window spectrum — tidas.py:237-283."""
+    if len(fixed_delays) != len(true_delays) or np.any(
+            np.asarray(fixed_delays.element_indices) != np.asarray(true_delays.element_indices)):
+        raise ValueError("fixed and true profiles must cover the same aperture")
+    if form not in FORMS:
+        raise ValueError(f"unknown estimator form {form!r}")
+    dev = _dev()
+    L = _lib.lib()
+    tr = np.asarray(windowed_frame.traces, float)
+    n_el, n = tr.shape
+    lo, hi = (0, n) if support is None else (int(support[0]), int(support[1]))
+
+    class _One:  # a one-column stand-in for _Columns
+        pass
+
+    one = _One()
+    one.fs, one.n_el, one.N = windowed_frame.sampling_frequency, n_el, n
+    one.flat = _f64(tr, dev)
+    first = torch.empty((1, n_el), dtype=torch.int32, device=dev)
+    last = torch.empty((1, n_el), dtype=torch.int32, device=dev)
+    scan = one.flat.clone()  # the scan zeroes outside [lo, hi): keep the caller's samples
+    lo_d, hi_d = _i32([lo], dev), _i32([hi], dev)  # alive until the launch is enqueued
+    _lib.check(L.tidas_window_frames_f64(_lib.ptr(scan), 1, n_el, n, _lib.ptr(lo_d), _lib.ptr(hi_d),
+                                         _lib.ptr(first), _lib.ptr(last), _lib.stream_handle()))
+    f, l_ = first.cpu().numpy()[0], last.cpu().numpy()[0]
+    if not (l_ >= 0).any():
+        raise ZeroDivisionError("window missed the echo: frame is zero inside the window")
+    one.s_lo = np.array([f[l_ >= 0].min()])
+    one.s_hi = np.array([l_.max() + 1])
+    one.ok = np.array([True])
+    one.has_support = np.array([True])
+    idx = np.asarray(fixed_delays.element_indices, int)
+    th, _ = _theta_cells(one, np.array([0]), [idx], [fixed_delays.delays], [true_delays.delays], form)
+    if not np.isfinite(th[0]):
+        raise ZeroDivisionError("window missed the echo: fixed-profile sum has no energy")
+    return float(th[0])
