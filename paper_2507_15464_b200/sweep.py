@@ -112,54 +112,67 @@ class _Columns:
         self.has_support = has.any(1)
 
 
-def _theta_cells(cols: _Columns, cell_col: np.ndarray, idx_of_col, d_fix_of_cell, d_true_of_col,
-                 form: str) -> Tuple[np.ndarray, np.ndarray]:
-    """theta for cells (column, fixed delays) over their column's true profile.
+def _next_pow2_vec(n: np.ndarray) -> np.ndarray:
+    """1 << bit_length(n - 1), elementwise (frexp gives the exact bit length)."""
+    _, e = np.frexp(np.maximum(np.asarray(n, np.int64) - 1, 0).astype(np.float64))
+    return np.left_shift(np.int64(1), e.astype(np.int64))
 
-    idx_of_col[t]: element indices of the column's aperture; d_fix_of_cell[c] /
-    d_true_of_col[t]: delays in seconds. Returns (theta, nfft) per cell; NaN
-    where the reference raises (no support, zero denominator)."""
+
+def _cell_geometry(cols, t: int, idx, d_fix: np.ndarray, d_true: np.ndarray):
+    """Rebased delays in samples and FFT lengths of the cells (t, every fixed
+    profile row of d_fix) — tidas.py:254-265 (offset, span, nfft)."""
+    fs = cols.fs
+    off = np.minimum(d_fix.min(axis=1), d_true.min())
+    df = d_fix - off[:, None]
+    dt = d_true[None, :] - off[:, None]
+    width = int(cols.s_hi[t] - cols.s_lo[t])
+    span = np.ceil(np.maximum(df.max(axis=1), dt.max(axis=1)) * fs).astype(np.int64) + 4
+    nfft = _next_pow2_vec(np.maximum(2 * width, width + span))
+    return df * fs, dt * fs, nfft
+
+
+def _theta_cells(cols, idx_of_col, d_fix_of_col, d_true_of_col, form: str) -> np.ndarray:
+    """theta [t][r] for every column t and fixed profile row r of d_fix_of_col[t]
+    (an (R, n_t) array of delays in seconds) against the column's true profile.
+    NaN where the reference raises (window outside the frame, no support, zero
+    denominator)."""
     if form not in FORMS:
         raise ValueError(f"unknown estimator form {form!r}")
     dev = _dev()
     L = _lib.lib()
-    C = len(cell_col)
-    fs = cols.fs
-    theta = np.full(C, np.nan)
-    nffts = np.zeros(C, np.int64)
-    good = np.array([cols.ok[t] and cols.has_support[t] for t in cell_col], bool)
-    A = max(len(idx_of_col[t]) for t in set(cell_col.tolist()))
+    T = len(idx_of_col)
+    R = d_fix_of_col[0].shape[0]
+    theta = np.full((T, R), np.nan)
+    good_cols = [t for t in range(T) if cols.ok[t] and cols.has_support[t]]
+    if not good_cols:
+        return theta
+    A = max(len(idx_of_col[t]) for t in good_cols)
+    C = len(good_cols) * R
     dfx = np.zeros((C, A))
     dtr = np.zeros((C, A))
-    for c in range(C):
-        t = int(cell_col[c])
-        df, dt = np.asarray(d_fix_of_cell[c], float), np.asarray(d_true_of_col[t], float)
-        off = min(df.min(), dt.min())
-        df, dt = df - off, dt - off
-        width = int(cols.s_hi[t] - cols.s_lo[t])
-        span = int(np.ceil(float(max(df.max(), dt.max())) * fs)) + 4
-        nffts[c] = _next_pow2(max(2 * width, width + span))
-        dfx[c, :len(df)] = df * fs
-        dtr[c, :len(dt)] = dt * fs
-    sel = np.flatnonzero(good)
-    if sel.size == 0:
-        return theta, nffts
-    # spectra pairs: distinct (column, nfft) among the good cells
-    keys = sorted({(int(cell_col[c]), int(nffts[c])) for c in sel})
-    pid = {k: i for i, k in enumerate(keys)}
+    nffts = np.zeros(C, np.int64)
+    cell_t = np.repeat(np.asarray(good_cols, np.int64), R)
+    for j, t in enumerate(good_cols):
+        n = len(idx_of_col[t])
+        df, dt, nf = _cell_geometry(cols, t, idx_of_col[t], d_fix_of_col[t], np.asarray(d_true_of_col[t], float))
+        dfx[j * R:(j + 1) * R, :n] = df
+        dtr[j * R:(j + 1) * R, :n] = dt
+        nffts[j * R:(j + 1) * R] = nf
+    # spectra pairs: distinct (column, nfft)
+    keys, cell_pair = np.unique(cell_t * (1 << 32) + nffts, return_inverse=True)
+    pair_frame = (keys >> 32).astype(np.int32)
+    pair_nfft = (keys & ((1 << 32) - 1)).astype(np.int32)
     P = len(keys)
-    kmax = max(n // 2 for _, n in keys)
+    kmax = int(pair_nfft.max()) // 2
     rows = np.zeros((P, A), np.int32)
     count = np.zeros(P, np.int32)
-    for i, (t, n) in enumerate(keys):
-        idx = np.asarray(idx_of_col[t], int)
+    for i in range(P):
+        idx = np.asarray(idx_of_col[int(pair_frame[i])], int)
         rows[i, :len(idx)] = idx + cols.n_el // 2  # frame-relative row
         count[i] = len(idx)
-    pair_frame = np.array([t for t, _ in keys], np.int32)
     pair_lo = cols.s_lo[pair_frame].astype(np.int32)
     pair_hi = cols.s_hi[pair_frame].astype(np.int32)
-    pair_nfft = np.array([n for _, n in keys], np.int32)
-    pair_off = (np.arange(P, dtype=np.int64) * A)
+    pair_off = np.arange(P, dtype=np.int64) * A
     S = torch.empty((P * A, kmax), dtype=torch.complex128, device=dev)
     keep = [_i32(pair_frame, dev), _i32(pair_lo, dev), _i32(pair_hi, dev), _i32(pair_nfft, dev),
             torch.as_tensor(pair_off).to(dev), _i32(rows, dev), _i32(count, dev)]
@@ -169,25 +182,29 @@ def _theta_cells(cols: _Columns, cell_col: np.ndarray, idx_of_col, d_fix_of_cell
             _lib.ptr(cols.flat), cols.n_el, cols.N, p1 - p0, _lib.ptr(keep[0][p0:]), _lib.ptr(keep[1][p0:]),
             _lib.ptr(keep[2][p0:]), _lib.ptr(keep[3][p0:]), _lib.ptr(keep[4][p0:]), _lib.ptr(keep[5][p0:]),
             A, _lib.ptr(keep[6][p0:]), kmax, _lib.ptr(S), _lib.stream_handle()))
-    cell_pair = np.array([pid[(int(cell_col[c]), int(nffts[c]))] for c in sel], np.int32)
-    th_d = torch.empty(sel.size, dtype=torch.float64, device=dev)
-    st_d = torch.empty(sel.size, dtype=torch.int32, device=dev)
-    cp_d, df_d, dt_d = _i32(cell_pair, dev), _f64(dfx[sel], dev), _f64(dtr[sel], dev)
-    _lib.check(L.tidas_theta_cells_f64(_lib.ptr(S), int(sel.size), _lib.ptr(cp_d), _lib.ptr(keep[4]),
-                                       _lib.ptr(keep[3]), _lib.ptr(keep[6]), kmax, _lib.ptr(df_d),
-                                       _lib.ptr(dt_d), A, FORMS[form], _lib.ptr(th_d), _lib.ptr(st_d),
-                                       _lib.stream_handle()))
-    theta[sel] = th_d.cpu().numpy()
-    return theta, nffts
+    th_d = torch.empty(C, dtype=torch.float64, device=dev)
+    st_d = torch.empty(C, dtype=torch.int32, device=dev)
+    cp_d, df_d, dt_d = _i32(cell_pair, dev), _f64(dfx, dev), _f64(dtr, dev)
+    _lib.check(L.tidas_theta_cells_f64(_lib.ptr(S), C, _lib.ptr(cp_d), _lib.ptr(keep[4]), _lib.ptr(keep[3]),
+                                       _lib.ptr(keep[6]), kmax, _lib.ptr(df_d), _lib.ptr(dt_d), A, FORMS[form],
+                                       _lib.ptr(th_d), _lib.ptr(st_d), _lib.stream_handle()))
+    theta[np.asarray(good_cols)] = th_d.cpu().numpy().reshape(len(good_cols), R)
+    return theta
 
 
 def _profiles(targets, refs, config, rx_rule):
+    """Per column: aperture (element indices), true delays (n_t,), fixed delays
+    (R, n_t) — rx_aperture / rx_delay_profile (geometry.py:169-199), vectorised
+    over the reference depths: D_n = (z - hypot(x_n, z)) / c."""
+    refs = np.asarray(refs, float)[:, None]
+    c = config.sound_speed
     idx_of_col, d_true, d_fix = [], [], []
     for z in targets:
-        ap = rx_aperture(float(z), rx_rule, config)
-        idx_of_col.append(np.asarray(ap, int))
+        ap = np.asarray(rx_aperture(float(z), rx_rule, config), int)
+        xs = element_positions(ap, config)[None, :]
+        idx_of_col.append(ap)
         d_true.append(rx_delay_profile(float(z), ap, config).delays)
-        d_fix.append([rx_delay_profile(float(r), ap, config).delays for r in refs])
+        d_fix.append((refs - np.hypot(xs, refs)) / c)
     return idx_of_col, d_true, d_fix
 
 
@@ -206,10 +223,7 @@ def theta_matrix_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, r
         tb = targets[b0:b0 + _COL_BATCH]
         cols = _Columns(tb, config, tx_rule, tx_focus_depth, window_half_width, spreading)
         idx, d_true, d_fix = _profiles(tb, refs, config, rx_rule)
-        cell_col = np.repeat(np.arange(len(tb)), len(refs))
-        fix_cells = [d for t in range(len(tb)) for d in d_fix[t]]
-        th, _ = _theta_cells(cols, cell_col, idx, fix_cells, d_true, form)
-        values[:, b0:b0 + len(tb)] = th.reshape(len(tb), len(refs)).T
+        values[:, b0:b0 + len(tb)] = _theta_cells(cols, idx, d_fix, d_true, form).T
         del cols
     return ThetaMatrix(reference_depths=refs, target_depths=targets, values=values)
 
@@ -230,48 +244,51 @@ def error_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, rx_rule:
     R, T = len(refs), len(targets)
     th_m, loc_m, glo_m = (np.full((R, T), np.nan) for _ in range(3))
     fs = config.sampling_frequency
+    n_el, half = config.element_count, config.element_count // 2
     for b0 in range(0, T, _COL_BATCH):
         tb = targets[b0:b0 + _COL_BATCH]
         Tb = len(tb)
         cols = _Columns(tb, config, tx_rule, tx_focus_depth, window_half_width, spreading)
         idx, d_true, d_fix = _profiles(tb, refs, config, rx_rule)
         A = max(len(i) for i in idx)
-        half = config.element_count // 2
         # true-profile PSF per column (das_psf of the windowed frame), K3
         rows_t = np.full((Tb, A), cols.zero_row, np.int64)
         sh_t = np.zeros((Tb, A))
         for t in range(Tb):
             n = len(idx[t])
-            rows_t[t, :n] = t * config.element_count + idx[t] + half
+            rows_t[t, :n] = t * n_el + idx[t] + half
             sh_t[t, :n] = np.asarray(d_true[t]) * fs
         _das._count(int(sum(len(i) for i in idx)))
         refs_d = _das._delayed_sums_dev(cols.flat, rows_t, sh_t)
-        cell_col = np.repeat(np.arange(Tb), R)
-        fix_cells = [d for t in range(Tb) for d in d_fix[t]]
-        th, _ = _theta_cells(cols, cell_col, idx, fix_cells, d_true, form)
-        th_m[:, b0:b0 + Tb] = th.reshape(Tb, R).T
-        sel = np.flatnonzero(np.isfinite(th))
-        if sel.size == 0:
+        th = _theta_cells(cols, idx, d_fix, d_true, form)  # [t][r]
+        th_m[:, b0:b0 + Tb] = th.T
+        t_sel, r_sel = np.nonzero(np.isfinite(th))
+        C = t_sel.size
+        if C == 0:
             continue
         # fixed-profile sums on each cell's crop [lo - span, hi + 2) (tidas.py:336-349), K3
-        C = sel.size
         rows_c = np.full((C, A), cols.zero_row, np.int64)
         sh_c = np.zeros((C, A))
         clo = np.zeros(C, np.int32)
         chi = np.zeros(C, np.int32)
-        for j, c in enumerate(sel):
-            t = int(cell_col[c])
+        start = 0
+        for t in range(Tb):
+            m = r_sel[t_sel == t]
+            if m.size == 0:
+                continue
             n = len(idx[t])
-            d = np.asarray(fix_cells[c], float)
-            rows_c[j, :n] = t * config.element_count + idx[t] + half
-            sh_c[j, :n] = d * fs
-            span = int(np.ceil(-d.min() * fs)) + 2
-            clo[j] = max(int(cols.wlo[t]) - span, 0)
-            chi[j] = min(int(cols.whi[t]) + 2, int(cols.n_len[t]))
-        _das._count(int(sum(len(idx[int(cell_col[c])]) for c in sel)))
+            d = d_fix[t][m]  # (k, n)
+            sl = slice(start, start + m.size)
+            rows_c[sl, :n] = t * n_el + idx[t] + half
+            sh_c[sl, :n] = d * fs
+            span = np.ceil(-d.min(axis=1) * fs).astype(np.int64) + 2
+            clo[sl] = np.maximum(int(cols.wlo[t]) - span, 0)
+            chi[sl] = min(int(cols.whi[t]) + 2, int(cols.n_len[t]))
+            start += m.size
+        _das._count(int(sum(len(idx[t]) for t in t_sel)))
         sums = _das._delayed_sums_dev(cols.flat, rows_c, sh_c, lo=clo, hi=chi)
-        th_d = _f64(th[sel], dev)
-        cc_d = _i32(cell_col[sel], dev)
+        th_d = _f64(th[t_sel, r_sel], dev)
+        cc_d = _i32(t_sel, dev)
         clo_d, chi_d = _i32(clo, dev), _i32(chi, dev)
         n_d, wlo_d, whi_d = _i32(cols.n_len, dev), _i32(cols.wlo, dev), _i32(cols.whi, dev)
         out = torch.empty((C, 4), dtype=torch.float64, device=dev)
@@ -284,9 +301,8 @@ def error_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, rx_rule:
             glo = np.where(e[:, 3] > 0.0, e[:, 2] / np.where(e[:, 3] > 0.0, e[:, 3], 1.0), np.nan)
         # a failing local_error (experiments.py:327) leaves the global error unset
         glo = np.where(np.isfinite(loc), glo, np.nan)
-        r_idx, t_idx = sel % R, sel // R
-        loc_m[r_idx, b0 + t_idx] = loc
-        glo_m[r_idx, b0 + t_idx] = glo
+        loc_m[r_sel, b0 + t_sel] = loc
+        glo_m[r_sel, b0 + t_sel] = glo
         del cols, sums, refs_d
     return th_m, loc_m, glo_m
 
@@ -325,7 +341,8 @@ def estimate_theta(windowed_frame: RfFrame, fixed_delays: DelayProfile, true_del
     one.ok = np.array([True])
     one.has_support = np.array([True])
     idx = np.asarray(fixed_delays.element_indices, int)
-    th, _ = _theta_cells(one, np.array([0]), [idx], [fixed_delays.delays], [true_delays.delays], form)
-    if not np.isfinite(th[0]):
+    th = _theta_cells(one, [idx], [np.asarray(fixed_delays.delays, float)[None, :]],
+                      [np.asarray(true_delays.delays, float)], form)
+    if not np.isfinite(th[0, 0]):
         raise ZeroDivisionError("window missed the echo: fixed-profile sum has no energy")
-    return float(th[0])
+    return float(th[0, 0])
