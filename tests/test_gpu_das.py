@@ -128,6 +128,58 @@ def test_cfg5_int16_ingest_reduced():
     assert rel_l2(img, ref) <= FP32_TOL
 
 
+def _subgrid_parity(cfg, rf_host, rf_dev, angles, out, n_rows=24, n_cols=16, seed=0):
+    """Full-size GPU image vs the oracle on a seeded row x column sub-grid."""
+    x, z = grid(cfg)
+    plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                              n_samples=cfg["n_samples"], x=x, z=z, angles=angles,
+                              f_number=cfg["f_number"], out=out)
+    img = tb.das_image(rf_dev, plan).cpu().numpy()
+    assert img.shape == (rf_dev.shape[0], cfg["nz"], cfg["nx"])
+    rng = np.random.default_rng(seed)
+    ri = np.sort(rng.choice(cfg["nz"], n_rows, replace=False))
+    ci = np.sort(rng.choice(cfg["nx"], n_cols, replace=False))
+    ts = plane_t_star(cfg, x[ci], z[ri], angles)
+    for f in range(rf_dev.shape[0]):
+        A = od.analytic_signal(np.asarray(rf_host[f], float))
+        ref = od.das_image_vectorized(A, cfg["fs"], 0.0, x[ci], z[ri], cfg["pitch"], cfg["c"], ts,
+                                      cfg["f_number"], out=out)
+        assert rel_l2(img[f][np.ix_(ri, ci)], ref) <= FP32_TOL
+
+
+def test_cfg3_full_size_frames_sampled_pixels():
+    """cfg3 at its full size: 11 steered plane waves x 128 ch x 4096 f32, 1024 x 512
+    image, 2000 speckle scatterers + 5 bright targets, coherent compounding."""
+    cfg = CFG3
+    ang = list(cfg["angles"])
+    rng = np.random.default_rng(33)
+    F = 2
+    sx = rng.uniform(*cfg["region_x"], (F, cfg["n_scat"] + 5))
+    sz = rng.uniform(*cfg["region_z"], (F, cfg["n_scat"] + 5))
+    a = rng.standard_normal((F, cfg["n_scat"] + 5))
+    a[:, cfg["n_scat"]:] = 20.0
+    rf = tb.synthesize_batch(sx, sz, a, angles=ang, n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"],
+                             c=cfg["c"], f0=cfg["f0"], fbw=cfg["fbw"], n_samples=cfg["n_samples"])
+    _subgrid_parity(cfg, rf.cpu().numpy(), rf, ang, "coherent")
+
+
+def test_cfg5_full_size_int16_frames_sampled_pixels():
+    """cfg5 at its full size: 192 ch x 8192 int16 (std 1000, rounded, clipped),
+    1024 x 1024 image, 4000 speckle scatterers."""
+    cfg = CFG5
+    rng = np.random.default_rng(55)
+    F = 2
+    sx = rng.uniform(*cfg["x"], (F, cfg["n_scat"]))
+    sz = rng.uniform(8e-3, 58e-3, (F, cfg["n_scat"]))
+    a = rng.standard_normal((F, cfg["n_scat"]))
+    rf = tb.synthesize_batch(sx, sz, a, angles=[0.0], n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"],
+                             c=cfg["c"], f0=cfg["f0"], fbw=cfg["fbw"], n_samples=cfg["n_samples"],
+                             dtype=torch.float64).cpu().numpy()
+    q = np.stack([osim.quantize_int16(rf[f, 0], cfg["target_std"])[None] for f in range(F)])
+    assert q.dtype == np.int16 and q.shape == (F, 1, 192, 8192)
+    _subgrid_parity(cfg, q, torch.as_tensor(q).to(DEV), [0.0], "envelope")
+
+
 def test_iq_output_and_ragged_grid():
     cfg = CFG2
     rf, _ = speckle_rf(cfg, seed=7, n_scat=200)
