@@ -215,6 +215,32 @@ int tidas_psf_errors_f64(const double* sums, int32_t n_samples, const double* th
                          const int32_t* crop_hi, const int32_t* n_len, const int32_t* win_lo,
                          const int32_t* win_hi, double* out, void* stream);
 
+/* ------------------------------------------------------------------------
+ * On-device metrics over strided batches of lines.
+ * Line r = (o, i), o < n_outer, i < n_inner, starts at o*s_outer + i*s_inner
+ * (elements); its element k is at + k*s_elem. dtype F32 or F64; f64 results.
+ * ------------------------------------------------------------------------ */
+
+/* out[r] = {sum_{k in [lo,hi)} (cand - ref)^2, sum_{k in [lo,hi)} ref^2}.
+ * Replaces: global_error / local_error (metrics.py:92-112). */
+int tidas_line_sq_errors(const void* ref, const void* cand, int dtype, int64_t n_outer, int64_t n_inner,
+                         int64_t n, int64_t s_outer, int64_t s_inner, int64_t s_elem, int64_t lo,
+                         int64_t hi, double* out, void* stream);
+
+/* Width at half maximum (sub-sample crossings nearest the first maximum) / fs;
+ * status 1 = non-positive maximum, 2 = no crossing on one side (width NaN).
+ * Replaces: width_at_half_max (metrics.py:37-68). */
+int tidas_line_half_width(const void* x, int dtype, int64_t n_outer, int64_t n_inner, int64_t n,
+                          int64_t s_outer, int64_t s_inner, int64_t s_elem, double fs, double* width,
+                          int32_t* status, void* stream);
+
+/* out[r] = {max over main-lobe samples, sum of |x| over the other samples};
+ * main_mask[n] (1 = main lobe). Replaces: the reductions of sidelobe_stats
+ * (metrics.py:115-161). */
+int tidas_line_sidelobes(const void* x, int dtype, int64_t n_outer, int64_t n_inner, int64_t n,
+                         int64_t s_outer, int64_t s_inner, int64_t s_elem, const uint8_t* main_mask,
+                         double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

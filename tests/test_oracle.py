@@ -274,3 +274,21 @@ def test_oracle_theta_matrix_sweep_golden(ref_vectors, form, key):
     assert np.array_equal(np.isnan(ours), np.isnan(ref))
     ok = ~np.isnan(ref)
     np.testing.assert_allclose(ours[ok], ref[ok], rtol=1e-11, atol=1e-13)
+
+
+# ------------------------------------------------------ line metrics (§8(f)3)
+
+from oracle import metrics as om  # noqa: E402
+
+
+def test_oracle_line_metrics_golden(ref_vectors):
+    w = [om.width_at_half_max(r, 50e6) for r in ref_vectors["G_env_rows"]]
+    np.testing.assert_allclose(w, ref_vectors["G_half_widths"], rtol=1e-13)
+    d = np.linspace(5e-3, 40e-3, 64)
+    db, rel = om.sidelobe_stats(ref_vectors["A_tidas_line"], d, [12e-3, 25e-3, 31e-3], 3,
+                                reference=ref_vectors["A_das_line"])
+    np.testing.assert_allclose([db, rel], ref_vectors["G_sidelobe"], rtol=1e-12)
+    with pytest.raises(ValueError):
+        om.width_at_half_max(-np.ones(8), 1.0)
+    with pytest.raises(ValueError):
+        om.width_at_half_max(np.linspace(0, 1, 8), 1.0)  # maximum at the edge
