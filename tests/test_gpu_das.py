@@ -249,3 +249,27 @@ def test_plan_validation():
                               n_samples=cfg["n_samples"], x=x, z=z, f_number=cfg["f_number"])
     with pytest.raises(ValueError):
         tb.das_from_analytic(torch.zeros((1, 1, 4, 16), dtype=torch.complex64, device=DEV), plan)
+
+
+def test_file_ingest_to_images_through_host_pipeline(tmp_path):
+    """save_frame blobs -> read_frames_pinned -> HostPipeline == das_image."""
+    cfg = CFG2
+    bases = []
+    rfs = []
+    for f in range(3):
+        rf, _ = speckle_rf(cfg, seed=80 + f, n_scat=120)
+        fr = tb.RfFrame(rf[0], cfg["fs"], 0.0, 0.0, np.arange(-4, 4))
+        tb.save_frame(fr, tmp_path / f"frame{f}")
+        bases.append(tmp_path / f"frame{f}")
+        rfs.append(rf.astype(np.float32))
+    host, hdr = tb.read_frames_pinned(bases)
+    assert host.is_pinned() and hdr[0]["sampling_frequency"] == cfg["fs"]
+    x, z = grid(cfg, 48, 32)
+    plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                              n_samples=cfg["n_samples"], x=x, z=z, f_number=cfg["f_number"])
+    out = torch.empty((3, 48, 32), dtype=torch.float32).pin_memory()
+    pipe = tb.HostPipeline(plan, chunk=2)
+    pipe.run(host, out)
+    pipe.synchronize()
+    ref = tb.das_image(torch.as_tensor(np.stack(rfs)).to(DEV), plan).cpu()
+    assert torch.equal(out, ref)
