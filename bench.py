@@ -58,6 +58,16 @@ def committed_traffic():
     return None
 
 
+def k2_live_pairs(cfg, x, z) -> int:
+    """(pixel, channel) pairs inside the Hann F# aperture of pixels whose t*
+    lies on the trace — the gathers K2 must do per frame and transmit."""
+    xs = (np.arange(-cfg["n_el"] // 2, cfg["n_el"] // 2) + 0.5) * cfg["pitch"]
+    Z, X = np.meshgrid(np.asarray(z, float), np.asarray(x, float), indexing="ij")
+    live = (np.abs(xs[None, None, :] - X[..., None]) < (Z / (2.0 * cfg["f_number"]))[..., None]).sum(-1)
+    pos = 2.0 * Z / cfg["c"] * cfg["fs"]  # 0-degree plane wave: t* = 2 z / c
+    return int((live * ((pos >= 0) & (pos <= cfg["n_samples"] - 1))).sum())
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -289,6 +299,16 @@ def main():
                           "das_image_kernel (K2)",
                 "bytes_per_launch": BYTES_PER_FRAME_CFG2 * chunk, "peak_source": peak_kind,
                 "per_frame_us": {"K1_analytic": k1 * 1e3, "K2_das": k2 * 1e3}}
+    # K2's binding resource is shared memory: every live (pixel, channel) pair
+    # gathers 3 complex64 samples (24 B) per frame from the staged window
+    pairs = k2_live_pairs(cfg, x, z)
+    smem_peak = 148 * 128 * (clocks.get("sm_mhz") or 1965) * 1e6 / 1e9  # GB/s, 128 B/clk/SM
+    smem_ach = pairs * 24 / (k2 * 1e-3) / 1e9
+    k2_smem = {"bound": "smem", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
+               "frac": smem_ach / smem_peak, "live_pairs_per_frame": pairs,
+               "bytes_per_pair": 24, "kernel": "das_image_kernel (K2)",
+               "note": "shared-memory gather roofline of K2 (128 B/clk/SM at the measured SM clock); "
+                       "the HBM roofline above is the contract metric"}
 
     # ---- e2e through the public API with pinned host buffers: HostPipeline
     # (H2D of chunk i+1 || K1 + K2 of chunk i || D2H of chunk i-1, three streams)
@@ -411,7 +431,8 @@ def main():
                        "frames_per_step_per_gpu": F, "parallelism": f"frame-sharded dp{world}",
                        "l2": "inputs larger than L2 (128 MiB RF per GPU per step)",
                        "gather": "NCCL all_gather of images inside the step" if world > 1 else "none"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "k2_smem_roofline": k2_smem, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
             "gpu_launches_e2e": launches_e2e,
             "clocks": clocks, "tidas": tidas,
         }
