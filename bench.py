@@ -409,6 +409,29 @@ def main():
         }
         del maps4, y4, a4
 
+    # ---- the paper's "600 points in 600 configurations" error
+    # sweep (theta + local / global error matrices), default probe
+    sweep = None
+    if rank == 0 and not args.no_tidas:
+        eps = float(np.load(ROOT / "tests/golden/ref_vectors.npz")["eps"])
+        d600 = np.linspace(0.005, 0.042, 600)
+        run = lambda: tb.error_sweep(d600, tb.ProbeConfig(), tb.Kossoff(0.6), tb.FNumber(1.0),  # noqa: E731
+                                     tx_focus_depth=25e-3, window_half_width=eps)
+        run()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        th600, _, _ = run()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sec = s0.elapsed_time(s1) / 1e3
+        sweep = {"cells": 360000, "seconds": sec, "cells_per_s": 360000 / sec,
+                 "finite_cells": int(np.isfinite(th600).sum()),
+                 "paper_cpu_minutes": {"das": 28.35, "tidas": 21.11},
+                 "api": "error_sweep (theta, local and global error matrices of run_error_sweep), "
+                        "600 scatterer depths x 600 reference profiles, 5-42 mm, 7 MHz, Tx focus 25 mm",
+                 "timing": "CUDA events around the public call (host geometry + D2H of the matrices inside)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
@@ -434,7 +457,7 @@ def main():
             "roofline": roofline, "k2_smem_roofline": k2_smem, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "gpu_launches_e2e": launches_e2e,
-            "clocks": clocks, "tidas": tidas,
+            "clocks": clocks, "tidas": tidas, "theta_error_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
