@@ -58,6 +58,10 @@ def committed_traffic():
     return None
 
 
+WORKLOAD = ("cfg2 (BASELINE.json configs[1]): DAS, 128 ch x 4096 f32 RF -> 512x256 px, Hann F#1.5, "
+            "linear interp, envelope")
+
+
 def k2_live_pairs(cfg, x, z) -> int:
     """(pixel, channel) pairs inside the Hann F# aperture of pixels whose t*
     lies on the trace — the gathers K2 must do per frame and transmit."""
@@ -184,7 +188,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded speckle, 2000 scatterers, 0-degree plane wave (oracle simulator)",
-            "config": {"workload": "cfg2: DAS 128 ch x 4096 -> 512x256 px, Hann F#1.5", "device": "cpu"},
+            "config": {"workload": WORKLOAD, "device": "cpu (host cores, oracle port of the reference algorithm)"},
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": "port",
                              "sample": sample},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -449,8 +453,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: seeded speckle (2000 N(0,1) scatterers over 40x40 mm per frame), "
                     "0-degree plane-wave RF simulated on the device (float32)",
-            "config": {"workload": "cfg2 (BASELINE.json configs[1]): DAS, 128 ch x 4096 f32 RF -> "
-                                   "512x256 px, Hann F#1.5, linear interp, envelope",
+            "config": {"workload": WORKLOAD,
                        "frames_per_step_per_gpu": F, "parallelism": f"frame-sharded dp{world}",
                        "l2": "inputs larger than L2 (128 MiB RF per GPU per step)",
                        "gather": "NCCL all_gather of images inside the step" if world > 1 else "none"},
