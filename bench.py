@@ -241,9 +241,14 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        tb.das_image(rf, plan, out=img, workspace=ws)
-        if world > 1:
-            parallel.gather_images(img, total_frames, out=gathered)
+        if world == 1:
+            tb.das_image(rf, plan, out=img, workspace=ws)
+        else:
+            # 16-frame sub-chunks: the all-gather of chunk c (async NCCL over
+            # NVLink) overlaps the K1 + K2 of chunk c + 1
+            parallel.pipelined_gather(
+                lambda c0, c1: tb.das_image(rf[c0:c1], plan, out=img[c0:c1], workspace=ws),
+                len(frames), gathered, sub=16)
 
     def barrier():
         if world > 1:
@@ -272,7 +277,11 @@ def main():
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms_total / args.steps
     value = total_frames / (ms_step / 1e3)
-    launches = args.steps * imaging.launches_per_call(len(frames), plan, ws)
+    if world == 1:
+        launches = args.steps * imaging.launches_per_call(len(frames), plan, ws)
+    else:
+        launches = args.steps * sum(imaging.launches_per_call(min(16, len(frames) - c0), plan, ws)
+                                    for c0 in range(0, len(frames), 16))
 
     # ---- per-kernel timing of one step (roofline of the DAS pipeline K1 + K2)
     chunk = ws.chunk
@@ -456,7 +465,8 @@ def main():
             "config": {"workload": WORKLOAD,
                        "frames_per_step_per_gpu": F, "parallelism": f"frame-sharded dp{world}",
                        "l2": "inputs larger than L2 (128 MiB RF per GPU per step)",
-                       "gather": "NCCL all_gather of images inside the step" if world > 1 else "none"},
+                       "gather": "NCCL all_gather of images inside the step, pipelined per 16 frames with the "
+                                 "DAS of the next 16" if world > 1 else "none"},
             "roofline": roofline, "k2_smem_roofline": k2_smem, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "gpu_launches_e2e": launches_e2e,

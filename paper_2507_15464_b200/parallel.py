@@ -62,3 +62,31 @@ def gather_images(local: torch.Tensor, n_units: int, out: Optional[torch.Tensor]
         parts.append(buf[r * cap: r * cap + (b - a)])
     res = torch.cat(parts)
     return res if out is None else out.copy_(res)
+
+
+def pipelined_gather(compute, n_local: int, out: torch.Tensor, sub: int, group=None) -> torch.Tensor:
+    """Compute the local units in sub-chunks and all-gather each one as soon as
+    it exists, so NVLink moves chunk c while the kernels compute chunk c + 1.
+
+    ``compute(c0, c1)`` returns this rank's units [c0, c1) as a tensor
+    [c1 - c0][...] (enqueued on the current stream). Every rank holds the same
+    ``n_local`` units; ``out`` [world * n_local][...] receives them in global
+    (rank-major) order. Each gather is an async NCCL ``all_gather`` ordered
+    after the compute that produced its chunk; the call returns once the
+    current stream waits for all of them."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if out.shape[0] != world * n_local:
+        raise ValueError(f"out holds {out.shape[0]} units, expected world * n_local = {world * n_local}")
+    works = []
+    for c0 in range(0, n_local, sub):
+        c1 = min(n_local, c0 + sub)
+        part = compute(c0, c1)
+        if world == 1:
+            if part.data_ptr() != out[c0:c1].data_ptr():
+                out[c0:c1].copy_(part)
+            continue
+        views = [out[r * n_local + c0: r * n_local + c1] for r in range(world)]
+        works.append(dist.all_gather(views, part.contiguous(), group=group, async_op=True))
+    for w in works:
+        w.wait()
+    return out

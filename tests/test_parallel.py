@@ -56,3 +56,40 @@ def test_gather_two_ranks_matches_single_process(n_units):
     want = torch.stack([torch.full((3, 4), float(f)) + torch.arange(12.0).view(3, 4)
                         for f in range(n_units)]).numpy().tolist()
     assert res[0] == want and res[1] == want
+
+
+def _pipelined_worker(rank, world, port, n_local, sub, q):
+    from paper_2507_15464_b200.parallel import pipelined_gather
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = []
+
+    def compute(c0, c1):
+        calls.append((c0, c1))
+        f0 = rank * n_local
+        return torch.stack([torch.full((2, 3), float(f0 + f)) for f in range(c0, c1)])
+
+    out = torch.empty((world * n_local, 2, 3))
+    pipelined_gather(compute, n_local, out, sub)
+    q.put((rank, out.numpy().tolist(), calls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_local,sub", [(8, 3), (6, 6), (5, 1)])
+def test_pipelined_gather_two_ranks(n_local, sub):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipelined_worker, args=(r, 2, port, n_local, sub, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r: (o, c) for r, o, c in (q.get(timeout=120) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [[[float(f)] * 3] * 2 for f in range(2 * n_local)]
+    chunks = [(c0, min(n_local, c0 + sub)) for c0 in range(0, n_local, sub)]
+    for r in (0, 1):
+        assert res[r][0] == want
+        assert res[r][1] == chunks
