@@ -1,3 +1,4 @@
+#include <cstdlib>
 // K1 — RF ingest + periodic analytic signal, one CTA per channel row.
 //
 // Reference: the envelope of every DAS pixel is the periodic Hilbert transform
@@ -68,7 +69,7 @@ template <typename R> __device__ __forceinline__ cplx<R> spectral_op(cplx<R> v, 
 // bins), ifft(fft(x) h) = x + i IFFT(-i sgn(k) X)(k): the real part is the input
 // itself and the imaginary part uses the multiplier -i sgn(k) / N.
 // Delay mode (spectral fractional delay, one row per CTA): out = IFFT(X * ramp).
-template <typename R, typename In, bool DELAY, int EPT>
+template <typename R, typename In, bool DELAY, int EPT, int LOGN = 0>
 __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __restrict__ rf,
                                                             int64_t stride, R scale,
                                                             cplx<R>* __restrict__ out,
@@ -79,7 +80,9 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
   __shared__ int first_nz[2], last_nz[2];
-  const int N = 1 << logN;
+  // LOGN > 0: compile-time length (thread count N / EPT), constant strides
+  const int N = LOGN > 0 ? (1 << LOGN) : (1 << logN);
+  const int NT = LOGN > 0 ? (1 << LOGN) / EPT : (int)blockDim.x;
   const int64_t ra = DELAY ? (int64_t)blockIdx.x : 2 * (int64_t)blockIdx.x;
   const bool has_b = !DELAY && (ra + 1 < n_rows);
   const In* src_a = rf + ra * stride;
@@ -91,13 +94,13 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
   R xa[EPT], xb[EPT];
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
-    const int n = threadIdx.x + k * blockDim.x;
+    const int n = threadIdx.x + k * NT;
     xa[k] = R(load_as_double(src_a + n));
     xb[k] = has_b ? R(load_as_double(src_b + n)) : R(0);
   }
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
-    const int n = threadIdx.x + k * blockDim.x;
+    const int n = threadIdx.x + k * NT;
     xa[k] *= scale;
     xb[k] *= scale;
     if (xa[k] != R(0)) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
@@ -112,9 +115,10 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
     if (lo_b < N) atomicMin(&first_nz[1], lo_b);
     if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
   }
-  fft_inplace<R, false, EPT>(s, logN);
+  if constexpr (LOGN > 0) fft_ct<R, false, LOGN>(s);
+  else fft_inplace<R, false, EPT>(s, logN);
   const R invN = R(1) / R(N);
-  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+  for (int k = threadIdx.x; k < N; k += NT) {
     C v = s[fpad(k)];
     if (DELAY) {
       v = spectral_op<R>(v, k, N, shift);
@@ -128,13 +132,14 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
     s[fpad(k)] = v;
   }
   __syncthreads();
-  fft_inplace<R, true, EPT>(s, logN);
+  if constexpr (LOGN > 0) fft_ct<R, true, LOGN>(s);
+  else fft_inplace<R, true, EPT>(s, logN);
   C* dst_a = out + ra * (int64_t)N;
   C* dst_b = dst_a + N;
   // real parts = the inputs, re-read (L2) with all loads in flight first
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
-    const int n = threadIdx.x + k * blockDim.x;
+    const int n = threadIdx.x + k * NT;
     if (!DELAY) {
       xa[k] = R(load_as_double(src_a + n)) * scale;
       xb[k] = has_b ? R(load_as_double(src_b + n)) * scale : R(0);
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
   }
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
-    const int n = threadIdx.x + k * blockDim.x;
+    const int n = threadIdx.x + k * NT;
     const C y = s[fpad(n)];
     if (DELAY) {
       dst_a[n] = y;
@@ -160,6 +165,82 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
       const bool any = last_nz[c] >= 0;
       support[2 * (ra + c)] = any ? first_nz[c] : -1;
       support[2 * (ra + c) + 1] = any ? last_nz[c] : -1;
+    }
+  }
+}
+
+
+// Hilbert mode at N = 4096, FP32 (cfg2 / cfg3): four radix-8 passes per FFT,
+// 512 threads, 8 elements per thread. The first forward pass starts from the
+// registers the global loads filled, the Hilbert multiplier is applied as the
+// first inverse pass loads, and the last inverse pass writes global memory
+// straight from registers — three shared-memory round trips and three barriers
+// fewer than the generic schedule.
+template <typename In>
+__global__ void __launch_bounds__(512, 2) analytic_4096_kernel(const In* __restrict__ rf, int64_t stride,
+                                                               float scale, cplx<float>* __restrict__ out,
+                                                               int64_t n_rows, int32_t* __restrict__ support) {
+  using R = float;
+  using C = cplx<R>;
+  constexpr int N = 4096, NT = 512;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  __shared__ int first_nz[2], last_nz[2];
+  const int64_t ra = 2 * (int64_t)blockIdx.x;
+  const bool has_b = ra + 1 < n_rows;
+  const In* src_a = rf + ra * stride;
+  const In* src_b = rf + (ra + 1) * stride;
+  if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  R xa[8], xb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int n = threadIdx.x + k * NT;
+    xa[k] = R(load_as_double(src_a + n)) * scale;
+    xb[k] = has_b ? R(load_as_double(src_b + n)) * scale : R(0);
+  }
+  C v[8];
+  int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int n = threadIdx.x + k * NT;
+    if (xa[k] != R(0)) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+    if (xb[k] != R(0)) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    v[k].x = xa[k];
+    v[k].y = xb[k];
+  }
+  __syncthreads();  // first_nz / last_nz initialised
+  if (support) {
+    if (lo_a < N) atomicMin(&first_nz[0], lo_a);
+    if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
+    if (lo_b < N) atomicMin(&first_nz[1], lo_b);
+    if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
+  }
+  const R invN = R(1) / R(N);
+  pass8_fused<R, false, N, 1, false, true, false>(s, v, invN);
+  pass8_fused<R, false, N, 8, true, true, false>(s, v, invN);
+  pass8_fused<R, false, N, 64, true, true, false>(s, v, invN);
+  pass8_fused<R, false, N, 512, true, true, false>(s, v, invN);
+  pass8_fused<R, true, N, 1, true, true, true>(s, v, invN);
+  pass8_fused<R, true, N, 8, true, true, false>(s, v, invN);
+  pass8_fused<R, true, N, 64, true, true, false>(s, v, invN);
+  pass8_fused<R, true, N, 512, true, false, false>(s, v, invN);  // v[r] = element tid + r * 512
+  C* dst_a = out + ra * (int64_t)N;
+  C* dst_b = dst_a + N;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int n = threadIdx.x + k * NT;
+    C a; a.x = xa[k]; a.y = v[k].x;
+    dst_a[n] = a;
+    if (has_b) { C b; b.x = xb[k]; b.y = v[k].y; dst_b[n] = b; }
+  }
+  if (support) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < (has_b ? 2 : 1); ++c) {
+        const bool any = last_nz[c] >= 0;
+        support[2 * (ra + c)] = any ? first_nz[c] : -1;
+        support[2 * (ra + c) + 1] = any ? last_nz[c] : -1;
+      }
     }
   }
 }
@@ -334,6 +415,23 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
     // FP64: radix-16, 16 per thread (fewer passes; FP64 is the drop-in path)
     constexpr int EPT = sizeof(R) == 4 ? 8 : 16;
     auto kern = delay ? analytic_pow2_kernel<R, In, true, EPT> : analytic_pow2_kernel<R, In, false, EPT>;
+    if constexpr (sizeof(R) == 4) {
+      if (!delay && logN == 12 && !getenv("TIDAS_K1_GENERIC")) {
+        const int64_t ctas4 = (n_rows + 1) / 2;
+        auto k4 = analytic_4096_kernel<In>;
+        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(k4, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        k4<<<(unsigned)ctas4, 512, smem, st>>>(rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out),
+                                               n_rows, support);
+        TIDAS_LAUNCH_CHECK();
+        return TIDAS_OK;
+      }
+    }
+    if constexpr (sizeof(R) == 4) {  // compile-time FFT schedule for the common lengths
+      if (!delay && logN == 11) kern = analytic_pow2_kernel<R, In, false, EPT, 11>;
+      if (!delay && logN == 12) kern = analytic_pow2_kernel<R, In, false, EPT, 12>;
+      if (!delay && logN == 13) kern = analytic_pow2_kernel<R, In, false, EPT, 13>;
+    }
     TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     const int64_t ctas = delay ? n_rows : (n_rows + 1) / 2;

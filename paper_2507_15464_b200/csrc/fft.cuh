@@ -202,4 +202,116 @@ __device__ __forceinline__ void fft_inplace(cplx<R>* s, int logN) {
   }
 }
 
+
+// ---- compile-time schedule (N, the pass strides and the thread count known):
+// padded indices become one per-thread base plus immediates and the twiddle
+// masks constants. NT = N / EPT threads, radix-8 passes then one smaller pass.
+template <int X> struct Pad {  // fpad of a compile-time multiple of 16
+  static_assert(X % 16 == 0, "offset must be a multiple of 16");
+  static constexpr int v = X + X / 16;
+};
+
+template <typename R, int RADIX, bool INV, int N, int NS, int NT>
+__device__ __forceinline__ void stockham_pass_ct(cplx<R>* s) {
+  using C = cplx<R>;
+  constexpr int G = N / RADIX;      // butterflies per pass == NT (EPT == RADIX)
+  static_assert(G == NT, "one butterfly per thread");
+  constexpr int LOG_NR = __builtin_ctz(NS * RADIX);
+  constexpr int TW_SHIFT = TW_LOG - LOG_NR;
+  const int j = threadIdx.x;
+  const int jp = fpad(j);
+  C v[RADIX];
+  C w;
+  if (NS > 1) w = twiddle<R>((j & (NS - 1)) << TW_SHIFT);
+#pragma unroll
+  for (int r = 0; r < RADIX; ++r) v[r] = s[jp + r * Pad<G>::v];
+  __syncthreads();
+  if (NS > 1) {
+    if (INV) w.y = -w.y;
+    apply_twiddle_powers<RADIX>(w, v);
+  }
+  if (RADIX == 8) dft8<INV, R>(v);
+  if (RADIX == 4) dft4<INV>(v[0], v[1], v[2], v[3]);
+  if (RADIX == 2) dft2<INV>(v[0], v[1]);
+  const int jm = j & (NS - 1);
+  const int base = (j - jm) * RADIX + jm;
+  if constexpr (NS % 16 == 0) {
+    const int bp = fpad(base);
+#pragma unroll
+    for (int r = 0; r < RADIX; ++r) s[bp + r * Pad<NS>::v] = v[r];
+  } else {
+#pragma unroll
+    for (int r = 0; r < RADIX; ++r) s[fpad(base + r * NS)] = v[r];
+  }
+  __syncthreads();
+}
+
+template <typename R, bool INV, int LOGN, int DONE = 0>
+__device__ __forceinline__ void fft_ct(cplx<R>* s) {
+  if constexpr (DONE < LOGN) {
+    constexpr int LEFT = LOGN - DONE;
+    constexpr int RB = LEFT >= 3 ? 3 : LEFT;
+    constexpr int N = 1 << LOGN;
+    constexpr int NT = N / 8;  // EPT = 8 (FP32)
+    if constexpr (RB == 3) {
+      stockham_pass_ct<R, 8, INV, N, (1 << DONE), NT>(s);
+    } else {
+      // a final radix-4 / radix-2 pass with 8 elements per thread: runtime pass
+      stockham_pass<R, (1 << RB), INV, 8>(s, N, 1 << DONE, TW_LOG - LOGN);
+    }
+    fft_ct<R, INV, LOGN, DONE + RB>(s);
+  }
+}
+
+
+// Register-fused variant of one compile-time radix-8 pass (EPT == 8): with
+// LOAD = false the inputs are already in v (v[r] = element j + r * N / 8, as
+// the caller loaded them); with STORE = false the outputs stay in v (v[r] =
+// element base + r * NS; for the last pass base = j and NS = N / 8). HILB
+// applies the Hilbert multiplier -i sgn(k) / N to the loaded spectrum (first
+// inverse pass): sgn(k) is known per register, k = j + r N / 8.
+template <typename R, bool INV, int N, int NS, bool LOAD, bool STORE, bool HILB>
+__device__ __forceinline__ void pass8_fused(cplx<R>* s, cplx<R> (&v)[8], R invN) {
+  using C = cplx<R>;
+  constexpr int G = N / 8;
+  constexpr int TW_SHIFT = TW_LOG - __builtin_ctz(NS * 8);
+  const int j = threadIdx.x;
+  C w;
+  if (NS > 1) w = twiddle<R>((j & (NS - 1)) << TW_SHIFT);
+  if (LOAD) {
+    const int jp = fpad(j);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = s[jp + r * Pad<G>::v];
+    __syncthreads();
+  }
+  if (HILB) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {  // k = j + r G: r < 4 positive, r >= 4 negative frequencies
+      C t;
+      if (r < 4) { t.x = v[r].y * invN; t.y = -v[r].x * invN; }
+      else { t.x = -v[r].y * invN; t.y = v[r].x * invN; }
+      v[r] = t;
+    }
+    if (j == 0) { v[0].x = v[0].y = R(0); v[4].x = v[4].y = R(0); }  // DC and Nyquist
+  }
+  if (NS > 1) {
+    if (INV) w.y = -w.y;
+    apply_twiddle_powers<8>(w, v);
+  }
+  dft8<INV, R>(v);
+  if (STORE) {
+    const int jm = j & (NS - 1);
+    const int base = (j - jm) * 8 + jm;
+    if constexpr (NS % 16 == 0) {
+      const int bp = fpad(base);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) s[bp + r * Pad<NS>::v] = v[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) s[fpad(base + r * NS)] = v[r];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace tidas

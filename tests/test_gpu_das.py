@@ -57,6 +57,24 @@ def test_analytic_support_scan():
     assert sup.cpu().tolist() == [[10, 19], [63, 63], [-1, -1]]
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.int16, np.float64])
+def test_analytic_4096_fused_odd_rows_and_support(dtype, rng):
+    """FP32 N = 4096 runs the register-fused kernel: odd row count (last CTA has
+    one channel), zero rows and head/tail zeros for the support scan."""
+    x = (rng.standard_normal((7, 4096)) * (1000 if dtype == np.int16 else 1)).astype(dtype)
+    x[2] = 0
+    x[3, :700] = 0
+    x[3, 3001:] = 0
+    x[6, :4095] = 0
+    ref = od.analytic_signal(x.astype(np.float64))
+    sup = torch.empty((7, 2), dtype=torch.int32, device=DEV)
+    got = tb.rf_analytic(torch.as_tensor(x).to(DEV), "f32", support=sup).cpu().numpy()
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 2e-6
+    s = sup.cpu().numpy()
+    assert s[2].tolist() == [-1, -1] and s[3].tolist() == [700, 3000] and s[6].tolist() == [4095, 4095]
+    assert s[0].tolist() == [int(np.flatnonzero(x[0])[0]), int(np.flatnonzero(x[0])[-1])]
+
+
 def test_analytic_rejects_short_rows():
     with pytest.raises(ValueError):
         tb.rf_analytic(torch.zeros((2, 3), dtype=torch.float64, device=DEV))
