@@ -170,19 +170,38 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
 }
 
 
-// Hilbert mode at N = 4096, FP32 (cfg2 / cfg3): four radix-8 passes per FFT,
-// 512 threads, 8 elements per thread. The first forward pass starts from the
+// Hilbert mode, FP32, N = 2^LOGN in {2048, 4096, 8192} (cfg1 / cfg2-3 / cfg5):
+// radix-8 passes (plus one radix-4 / radix-2 pass when LOGN % 3 != 0), N / 8
+// threads, 8 elements per thread. The first forward pass starts from the
 // registers the global loads filled, the Hilbert multiplier is applied as the
-// first inverse pass loads, and the last inverse pass writes global memory
-// straight from registers — three shared-memory round trips and three barriers
-// fewer than the generic schedule.
-template <typename In>
-__global__ void __launch_bounds__(512, 2) analytic_4096_kernel(const In* __restrict__ rf, int64_t stride,
-                                                               float scale, cplx<float>* __restrict__ out,
-                                                               int64_t n_rows, int32_t* __restrict__ support) {
+// first inverse pass loads, and when the last inverse pass is radix-8 it writes
+// global memory straight from registers — up to three shared-memory round trips
+// and three barriers fewer than the generic schedule.
+template <int LOGN, int DONE, bool INV>
+__device__ __forceinline__ void fused_rest(cplx<float>* s, cplx<float> (&v)[8], float invN) {
+  constexpr int N = 1 << LOGN;
+  if constexpr (DONE < LOGN) {
+    constexpr int LEFT = LOGN - DONE;
+    if constexpr (LEFT > 3) {
+      pass8_fused<float, INV, N, (1 << DONE), true, true, false>(s, v, invN);
+      fused_rest<LOGN, DONE + 3, INV>(s, v, invN);
+    } else if constexpr (LEFT == 3) {
+      // last pass: the inverse keeps its outputs in registers (element tid + r N / 8)
+      pass8_fused<float, INV, N, (1 << DONE), true, !INV, false>(s, v, invN);
+    } else {
+      stockham_pass<float, (1 << LEFT), INV, 8>(s, N, 1 << DONE, TW_LOG - LOGN);
+    }
+  }
+}
+
+template <typename In, int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 8) analytic_fused_kernel(const In* __restrict__ rf, int64_t stride,
+                                                                       float scale, cplx<float>* __restrict__ out,
+                                                                       int64_t n_rows, int32_t* __restrict__ support) {
   using R = float;
   using C = cplx<R>;
-  constexpr int N = 4096, NT = 512;
+  constexpr int N = 1 << LOGN, NT = N / 8;
+  constexpr bool LAST_IN_REGS = (LOGN % 3) == 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
   __shared__ int first_nz[2], last_nz[2];
@@ -216,14 +235,14 @@ __global__ void __launch_bounds__(512, 2) analytic_4096_kernel(const In* __restr
     if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
   }
   const R invN = R(1) / R(N);
-  pass8_fused<R, false, N, 1, false, true, false>(s, v, invN);
-  pass8_fused<R, false, N, 8, true, true, false>(s, v, invN);
-  pass8_fused<R, false, N, 64, true, true, false>(s, v, invN);
-  pass8_fused<R, false, N, 512, true, true, false>(s, v, invN);
-  pass8_fused<R, true, N, 1, true, true, true>(s, v, invN);
-  pass8_fused<R, true, N, 8, true, true, false>(s, v, invN);
-  pass8_fused<R, true, N, 64, true, true, false>(s, v, invN);
-  pass8_fused<R, true, N, 512, true, false, false>(s, v, invN);  // v[r] = element tid + r * 512
+  pass8_fused<R, false, N, 1, false, true, false>(s, v, invN);  // inputs from registers
+  fused_rest<LOGN, 3, false>(s, v, invN);
+  pass8_fused<R, true, N, 1, true, true, true>(s, v, invN);     // Hilbert multiplier on load
+  fused_rest<LOGN, 3, true>(s, v, invN);
+  if constexpr (!LAST_IN_REGS) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = s[fpad(threadIdx.x + k * NT)];
+  }
   C* dst_a = out + ra * (int64_t)N;
   C* dst_b = dst_a + N;
 #pragma unroll
@@ -416,13 +435,14 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
     constexpr int EPT = sizeof(R) == 4 ? 8 : 16;
     auto kern = delay ? analytic_pow2_kernel<R, In, true, EPT> : analytic_pow2_kernel<R, In, false, EPT>;
     if constexpr (sizeof(R) == 4) {
-      if (!delay && logN == 12 && !getenv("TIDAS_K1_GENERIC")) {
-        const int64_t ctas4 = (n_rows + 1) / 2;
-        auto k4 = analytic_4096_kernel<In>;
-        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(k4, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        k4<<<(unsigned)ctas4, 512, smem, st>>>(rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out),
-                                               n_rows, support);
+      if (!delay && logN >= 11 && logN <= 13 && !getenv("TIDAS_K1_GENERIC")) {
+        const int64_t ctasf = (n_rows + 1) / 2;
+        auto kf = logN == 11 ? analytic_fused_kernel<In, 11>
+                             : (logN == 12 ? analytic_fused_kernel<In, 12> : analytic_fused_kernel<In, 13>);
+        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        kf<<<(unsigned)ctasf, N / 8, smem, st>>>(rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out),
+                                                 n_rows, support);
         TIDAS_LAUNCH_CHECK();
         return TIDAS_OK;
       }
