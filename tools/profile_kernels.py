@@ -1,7 +1,7 @@
 """Small driver for ncu: one cfg2 DAS chunk (K1 + K2) and one row-operator launch.
 
   python tools/profile_kernels.py [--iters 2]
-  ncu --set full -k regex:"das_image|analytic_pow2|rowconv" -c 3 python tools/profile_kernels.py --frames 64 --maps 256
+  ncu --set full -k regex:"das_image|analytic|rowconv" -c 3 python tools/profile_kernels.py --frames 64 --maps 256
 """
 import argparse
 import sys
