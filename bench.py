@@ -405,6 +405,20 @@ def main():
             ad.append(ev[1].elapsed_time(ev[2]))
         tf, ta = max_over_ranks(statistics.median(fw)), max_over_ranks(statistics.median(ad))
         g4 = (BYTES_PER_MAP_CFG4 * M + K4.numel() * 4) / (tf / 1e3) / 1e9
+        cpu_rowconv = None
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            # the row operator's float64 CPU restatement (no reference counterpart,
+            # SURVEY §8(d)), one process, on a bounded sample of one cfg4 map
+            sys.path.insert(0, str(ROOT))
+            from oracle import tidas as ot
+            rows = 128
+            g1 = maps4[0, :rows].double().cpu().numpy()[None]
+            K1h = K4[:rows].double().cpu().numpy()
+            t0 = time.perf_counter()
+            ot.rowconv_fwd(g1, K1h)
+            ct = time.perf_counter() - t0
+            cpu_rowconv = {"kind": "port (restatement)", "cores": 1, "unit": "maps/s (fwd)",
+                           "value": rows / c4["nz"] / ct, "sample": f"{rows} of {c4['nz']} rows of one cfg4 map"}
         tidas = {
             "cfg2_fwd": {"value": F * world / (t2 / 1e3), "unit": "maps/s", "maps_per_step_per_gpu": F,
                          "ms_per_step": t2,
@@ -417,6 +431,7 @@ def main():
                                           "frac": g4 / hbm,
                                           "traffic": (tr or {}).get("rowconv_cfg4_bytes_per_launch"),
                                           "kernel": "rowconv_tc_kernel<fwd> (tcgen05 3xTF32), 256 maps/launch"}},
+            "cpu_baseline": cpu_rowconv,
             "row_kernels": "K5 build_row_kernels, cfg2 geometry, 129 taps, neighbourhood 8 (cfg2); "
                            "seeded random K for cfg4 timing",
         }
@@ -444,6 +459,20 @@ def main():
                  "api": "error_sweep (theta, local and global error matrices of run_error_sweep), "
                         "600 scatterer depths x 600 reference profiles, 5-42 mm, 7 MHz, Tx focus 25 mm",
                  "timing": "CUDA events around the public call (host geometry + D2H of the matrices inside)"}
+        if not args.no_cpu_baseline:
+            # the same sweep's CPU algorithm (oracle port of tidas.py / experiments.py,
+            # pinned to the reference's CSV fixtures), one process, on a bounded
+            # 12 x 12 sample of the grid, extrapolated per cell
+            sys.path.insert(0, str(ROOT))
+            from oracle import theta as oth
+            probe = dict(n_el=192, pitch=0.2e-3, f0=7e6, fs=50e6, c=1540.0, fbw=0.75)
+            d12 = d600[::50]
+            t0 = time.perf_counter()
+            oth.error_sweep(d12, d12, probe, tx_focus=25e-3, half_width=eps)
+            ct = time.perf_counter() - t0
+            sweep["cpu_baseline"] = {"kind": "port", "cores": 1, "sample": f"{len(d12)} x {len(d12)} cells",
+                                     "seconds_per_cell": ct / len(d12) ** 2,
+                                     "extrapolated_600x600_minutes": ct / len(d12) ** 2 * 360000 / 60}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
