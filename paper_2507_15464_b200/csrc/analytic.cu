@@ -504,8 +504,9 @@ extern "C" int tidas_rf_analytic(const void* rf, int rf_dtype, int64_t rf_row_st
                                  void* out, int out_prec, int64_t n_rows, int32_t n_samples,
                                  int32_t* support, void* stream) {
   using namespace tidas;
-  TIDAS_REQUIRE(rf && out, "null pointer");
   TIDAS_REQUIRE(n_rows >= 0 && n_rows < (int64_t(1) << 31), "n_rows out of range");
+  if (n_rows == 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
+  TIDAS_REQUIRE(rf && out, "null pointer");
   TIDAS_REQUIRE(n_samples >= 4, "envelope needs at least 4 samples");
   TIDAS_REQUIRE(rf_row_stride >= n_samples, "row stride shorter than the row");
   if (n_rows == 0) return TIDAS_OK;
@@ -521,9 +522,9 @@ extern "C" int tidas_rf_analytic(const void* rf, int rf_dtype, int64_t rf_row_st
 extern "C" int tidas_spectral_shift_f64(const double* x, int64_t n_rows, int32_t n_samples,
                                         double shift, void* out, void* stream) {
   using namespace tidas;
-  TIDAS_REQUIRE(x && out, "null pointer");
   TIDAS_REQUIRE(n_samples >= 1 && !isnan(shift), "bad arguments");
-  if (n_rows == 0) return TIDAS_OK;
+  if (n_rows == 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
+  TIDAS_REQUIRE(x && out, "null pointer");
   if (n_samples < 16) {
     set_error("spectral delay needs at least 16 samples on the device path");
     return TIDAS_EUNSUPPORTED;

@@ -143,6 +143,8 @@ static Lines make_lines(int64_t n_outer, int64_t n_inner, int64_t n, int64_t s_o
 extern "C" int tidas_line_sq_errors(const void* ref, const void* cand, int dtype, TIDAS_LINES_ARGS, int64_t lo,
                                     int64_t hi, double* out, void* stream) {
   using namespace tidas;
+  TIDAS_REQUIRE(n_outer >= 0 && n_inner >= 0, "bad line batch shape");
+  if (n_outer * n_inner == 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
   TIDAS_REQUIRE(ref && cand && out, "null pointer");
   TIDAS_LINES_CHECK;
   TIDAS_REQUIRE(0 <= lo && lo <= hi && hi <= n, "window [lo, hi) outside the line");
@@ -160,6 +162,8 @@ extern "C" int tidas_line_sq_errors(const void* ref, const void* cand, int dtype
 extern "C" int tidas_line_half_width(const void* x, int dtype, TIDAS_LINES_ARGS, double fs, double* width,
                                      int32_t* status, void* stream) {
   using namespace tidas;
+  TIDAS_REQUIRE(n_outer >= 0 && n_inner >= 0, "bad line batch shape");
+  if (n_outer * n_inner == 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
   TIDAS_REQUIRE(x && width && status, "null pointer");
   TIDAS_LINES_CHECK;
   TIDAS_REQUIRE(fs > 0.0, "sampling frequency must be positive");
@@ -178,6 +182,8 @@ extern "C" int tidas_line_half_width(const void* x, int dtype, TIDAS_LINES_ARGS,
 extern "C" int tidas_line_sidelobes(const void* x, int dtype, TIDAS_LINES_ARGS, const uint8_t* main_mask,
                                     double* out, void* stream) {
   using namespace tidas;
+  TIDAS_REQUIRE(n_outer >= 0 && n_inner >= 0, "bad line batch shape");
+  if (n_outer * n_inner == 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
   TIDAS_REQUIRE(x && main_mask && out, "null pointer");
   TIDAS_LINES_CHECK;
   const int64_t rows = n_outer * n_inner;

@@ -150,10 +150,10 @@ static bool rowconv_tc_enabled() {
 template <bool ADJ>
 static int launch_rowconv(const float* in, const float* K, float* out, int64_t batch, int nz, int nx,
                           int T, cudaStream_t st) {
-  TIDAS_REQUIRE(in && K && out, "null pointer");
   TIDAS_REQUIRE(batch >= 0 && nz >= 0 && nx >= 0, "bad sizes");
   TIDAS_REQUIRE(T >= 1 && (T & 1) && T <= 255, "taps must be odd and in [1, 255]");
-  if (batch == 0 || nz == 0 || nx == 0) return TIDAS_OK;
+  if (batch == 0 || nz == 0 || nx == 0) return TIDAS_OK;  // empty (null data pointers allowed)
+  TIDAS_REQUIRE(in && K && out, "null pointer");
   // tensor cores (tcgen05, 3xTF32) for batches that fill the 128-map MMA tile
   if (rowconv_tc_enabled() && batch >= 32) {
     const int rc = launch_rowconv_tc<ADJ>(in, K, out, batch, nz, nx, T, st);

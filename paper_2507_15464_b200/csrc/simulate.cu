@@ -54,8 +54,9 @@ extern "C" int tidas_synthesize(const double* sx, const double* sz, const double
                                 double f0, double fbw, int32_t spreading, int32_t n_samples,
                                 void* out, int out_dtype, void* stream) {
   using namespace tidas;
-  TIDAS_REQUIRE(sx && sz && amp && t_tx && out, "null pointer");
   TIDAS_REQUIRE(n_scat >= 0 && n_frames >= 0 && n_angles >= 0 && n_el >= 2 && n_samples >= 1, "bad sizes");
+  if ((int64_t)n_frames * n_angles == 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
+  TIDAS_REQUIRE(sx && sz && amp && t_tx && out, "null pointer");
   const double sigma = sqrt(2.0 * log(2.0)) / (M_PI * fbw * f0);
   const int64_t total = (int64_t)n_frames * n_angles * n_scat * n_el;
   if (total == 0) return TIDAS_OK;

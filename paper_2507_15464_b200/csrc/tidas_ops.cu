@@ -160,8 +160,8 @@ extern "C" int tidas_window_envelope_f64(const double* traces, int32_t n_samples
                                          const int32_t* hi, const double* pos, const double* theta,
                                          int32_t n_pixels, double* out, void* stream) {
   using namespace tidas;
+  if (n_pixels <= 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
   TIDAS_REQUIRE(traces && trace_of && lo && hi && pos && out, "null pointer");
-  if (n_pixels <= 0) return TIDAS_OK;
   window_envelope_f64_kernel<<<(n_pixels + 127) / 128, 128, 0, as_stream(stream)>>>(
       traces, n_samples, trace_of, lo, hi, pos, theta, n_pixels, out);
   TIDAS_LAUNCH_CHECK();
@@ -172,8 +172,8 @@ extern "C" int tidas_window_dots_f64(const double* a, const double* b, int32_t n
                                      const int32_t* lo, const int32_t* hi, int32_t n_pairs,
                                      double* out, void* stream) {
   using namespace tidas;
+  if (n_pairs <= 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
   TIDAS_REQUIRE(a && b && lo && hi && out, "null pointer");
-  if (n_pairs <= 0) return TIDAS_OK;
   window_dots_f64_kernel<<<n_pairs, 256, 0, as_stream(stream)>>>(a, b, n_samples, lo, hi, out);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;

@@ -1,0 +1,64 @@
+"""Empty and minimal inputs through the public entry points (GPU)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2507_15464_b200 as tb
+from tests.setups import CFG2, grid
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _plan(nz=16, nx=8):
+    c = CFG2
+    x, z = grid(c, nz, nx)
+    return tb.plane_wave_plan(n_el=c["n_el"], pitch=c["pitch"], fs=c["fs"], c=c["c"], n_samples=c["n_samples"],
+                              x=x, z=z, f_number=c["f_number"])
+
+
+def test_das_image_zero_frames():
+    plan = _plan()
+    rf = torch.zeros((0, 1, CFG2["n_el"], CFG2["n_samples"]), device=DEV)
+    img = tb.das_image(rf, plan)
+    assert img.shape == (0, 16, 8)
+
+
+def test_rf_analytic_zero_rows():
+    out = tb.rf_analytic(torch.zeros((0, 4096), device=DEV), "f32")
+    assert out.shape == (0, 4096)
+
+
+def test_rowconv_zero_maps_and_single_row():
+    K = torch.randn((4, 9), device=DEV)
+    y = tb.tidas_rowconv(torch.zeros((0, 4, 32), device=DEV), K)
+    assert y.shape == (0, 4, 32)
+    g = torch.randn((1, 4, 1), device=DEV)  # one column: only the centre tap touches data
+    y = tb.tidas_rowconv(g, K)
+    assert torch.allclose(y[0, :, 0], g[0, :, 0] * K[:, 4])
+
+
+def test_host_pipeline_zero_frames():
+    plan = _plan()
+    pipe = tb.HostPipeline(plan, chunk=4)
+    host = torch.zeros((0, 1, CFG2["n_el"], CFG2["n_samples"]), pin_memory=True)
+    out = torch.empty((0, 16, 8), pin_memory=True)
+    pipe.run(host, out)
+    pipe.synchronize()
+
+
+def test_sweeps_single_depth(ref_vectors):
+    eps = float(ref_vectors["eps"])
+    m = tb.theta_matrix_sweep([20e-3], tb.ProbeConfig(), tb.Kossoff(0.6), tb.FNumber(1.0),
+                              tx_focus_depth=25e-3, window_half_width=eps)
+    assert m.values.shape == (1, 1) and m.values[0, 0] == pytest.approx(1.0, rel=1e-9)
+    th, loc, glo = tb.error_sweep([20e-3], tb.ProbeConfig(), tb.Kossoff(0.6), tb.FNumber(1.0),
+                                  tx_focus_depth=25e-3, window_half_width=eps)
+    assert th.shape == loc.shape == glo.shape == (1, 1)
+    assert loc[0, 0] == pytest.approx(0.0, abs=1e-20) and glo[0, 0] == pytest.approx(0.0, abs=1e-20)
+
+
+def test_batch_metrics_zero_batch():
+    z = torch.zeros((0, 8), dtype=torch.float64, device=DEV)
+    assert tb.batch_errors(z, z, axis=1).shape == (0,)
+    assert tb.batch_fwhm(z, 1.0).shape == (0,)
