@@ -139,6 +139,9 @@ __global__ void rowconv_generic_kernel(const float* __restrict__ in, const float
 template <bool ADJ>
 int launch_rowconv_tc(const float* in, const float* K, float* out, int64_t batch, int nz, int nx, int T,
                       cudaStream_t st);
+template <bool ADJ>
+int launch_rowconv_tc1(const float* in, const float* K, float* out, int64_t batch, int nz, int nx, int T,
+                      cudaStream_t st);
 
 // TIDAS_ROWCONV_PATH=simt forces the CUDA-core kernel (tests compare both paths)
 static bool rowconv_tc_enabled() {
@@ -156,7 +159,12 @@ static int launch_rowconv(const float* in, const float* K, float* out, int64_t b
   TIDAS_REQUIRE(in && K && out, "null pointer");
   // tensor cores (tcgen05, 3xTF32) for batches that fill the 128-map MMA tile
   if (rowconv_tc_enabled() && batch >= 32) {
-    const int rc = launch_rowconv_tc<ADJ>(in, K, out, batch, nz, nx, T, st);
+    // tcgen05 paths: 128 maps per block (rowconv_tc1.cu) unless
+    // TIDAS_ROWCONV_TC=2p selects the 64-map x 2-phase kernel (rowconv_tc.cu)
+    const char* e = getenv("TIDAS_ROWCONV_TC");
+    const bool two_phase = e && std::string(e) == "2p";
+    const int rc = two_phase ? launch_rowconv_tc<ADJ>(in, K, out, batch, nz, nx, T, st)
+                             : launch_rowconv_tc1<ADJ>(in, K, out, batch, nz, nx, T, st);
     if (rc != TIDAS_EUNSUPPORTED) return rc;
   }
   const bool aligned = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;

@@ -60,9 +60,12 @@ def test_rowconv_cfg4_map_size_and_adjoint_identity(rng):
 # the 64-output block), short and full-width kernels. Tolerance: 2e-6 relative
 # L2 vs the float64 oracle (the split drops the lo*lo term and truncates lo,
 # ~2^-21 relative per product).
+@pytest.mark.parametrize("kernel", ["tc1", "2p"])  # 128-map blocks (default) / 64 maps x 2 phases
 @pytest.mark.parametrize("shape", [(128, 3, 256), (40, 5, 96), (33, 2, 32), (200, 3, 1024), (257, 2, 64)])
 @pytest.mark.parametrize("taps", [129, 31, 1])
-def test_rowconv_tensor_core_path_vs_oracle(shape, taps, rng):
+def test_rowconv_tensor_core_path_vs_oracle(shape, taps, kernel, rng, monkeypatch):
+    if kernel == "2p":
+        monkeypatch.setenv("TIDAS_ROWCONV_TC", "2p")
     B, nz, nx = shape
     g = sparse_maps(rng, B, nz, nx, 0.2)
     K = rng.standard_normal((nz, taps)).astype(np.float32)

@@ -19,7 +19,7 @@ int main(int argc, char** argv) {
   cudaDeviceSynchronize();
   unsigned long long z[16][16];
   memset(z, 0, sizeof(z));
-  cudaMemcpyToSymbol(tidas::tc::g_rc_prof, z, sizeof(z));
+  cudaMemcpyToSymbol(tidas::tcx::g_rc_prof, z, sizeof(z));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -29,7 +29,7 @@ int main(int argc, char** argv) {
   cudaEventSynchronize(e1);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  cudaMemcpyFromSymbol(z, tidas::tc::g_rc_prof, sizeof(z));
+  cudaMemcpyFromSymbol(z, tidas::tcx::g_rc_prof, sizeof(z));
   printf("rc=%d  %.3f ms  (%s)\n", rc, ms, cudaGetErrorString(cudaGetLastError()));
   const char* site[10] = {"row_done", "c_free", "a_full", "mma_done", "a_empty", "c_full", "d_empty", "st_read", "-", "TOTAL"};
   const char* role[16] = {"conv0", "conv1", "conv2", "conv3", "epi0", "epi1", "epi2", "epi3", "mma", "tma",
