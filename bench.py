@@ -424,13 +424,13 @@ def main():
                          "ms_per_step": t2,
                          "roofline": {"bound": "hbm", "achieved": g2, "peak": hbm, "unit": "GB/s",
                                       "frac": g2 / hbm, "traffic": None,
-                                      "kernel": "rowconv_tc_kernel<fwd> (tcgen05 3xTF32)"}},
+                                      "kernel": "rowconv_tc1_kernel<fwd> (tcgen05 3xTF32)"}},
             "cfg4_fwd_adj": {"value": M * world / ((tf + ta) / 1e3), "unit": "maps/s (fwd+adj)",
                              "fwd_ms": tf, "adj_ms": ta, "maps_per_gpu": M,
                              "roofline": {"bound": "hbm", "achieved": g4, "peak": hbm, "unit": "GB/s",
                                           "frac": g4 / hbm,
                                           "traffic": (tr or {}).get("rowconv_cfg4_bytes_per_launch"),
-                                          "kernel": "rowconv_tc_kernel<fwd> (tcgen05 3xTF32), 256 maps/launch"}},
+                                          "kernel": "rowconv_tc1_kernel<fwd> (tcgen05 3xTF32), 256 maps/launch"}},
             "cpu_baseline": cpu_rowconv,
             "row_kernels": "K5 build_row_kernels, cfg2 geometry, 129 taps, neighbourhood 8 (cfg2); "
                            "seeded random K for cfg4 timing",
