@@ -459,7 +459,7 @@ def main():
                  "api": "error_sweep (theta, local and global error matrices of run_error_sweep), "
                         "600 scatterer depths x 600 reference profiles, 5-42 mm, 7 MHz, Tx focus 25 mm",
                  "timing": "CUDA events around the public call (host geometry + D2H of the matrices inside)"}
-        if not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline:
             # the same sweep's CPU algorithm (oracle port of tidas.py / experiments.py,
             # pinned to the reference's CSV fixtures), one process, on a bounded
             # 12 x 12 sample of the grid, extrapolated per cell
