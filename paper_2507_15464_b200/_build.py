@@ -37,18 +37,35 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every translation unit in parallel (one nvcc per .cu), then link."""
     if not force and not stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = PKG.parent / "build" / "obj"
+    objdir.mkdir(parents=True, exist_ok=True)
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+
+    def compile_one(src: str):
+        obj = objdir / (Path(src).stem + ".o")
+        cmd = [nvcc(), *ARCH, *compile_flags, "-c", str(CSRC / src), "-o", str(obj)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        return cmd, res, obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(tmp)]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    link = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *[str(r[2]) for r in results], "-o", str(tmp)]
+    lres = subprocess.run(link, capture_output=True, text=True) if all(r[1].returncode == 0 for r in results) else None
     log = PKG / "build.log"
-    log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stderr[-8000:])
+    log.write_text("".join(" ".join(c) + "\n" + r.stdout + r.stderr for c, r, _ in results)
+                   + (" ".join(link) + "\n" + lres.stdout + lres.stderr if lres else ""))
+    failed = [r for _, r, _ in results if r.returncode != 0] + ([lres] if lres and lres.returncode != 0 else [])
+    if failed:
+        sys.stderr.write(failed[0].stderr[-8000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(r.stderr for _, r, _ in results))
     os.replace(tmp, LIB)
     return LIB
 
