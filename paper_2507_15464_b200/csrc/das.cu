@@ -197,7 +197,7 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
 // empty[b] (all 8 consumer warps done); consumers never meet at a CTA barrier
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
-          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1>
+          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true>
 __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams p,
                                                                    const cplx<R>* __restrict__ A,
                                                                    void* __restrict__ out_,
@@ -361,10 +361,18 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
 #pragma unroll
       for (int b = 0; b < FB; ++b) { c0[b].x = c0[b].y = R(0); c1[b].x = c1[b].y = R(0); }
       auto accumulate = [&](const Tap<R>& t, int b, C am1, C a0, C ap1) {
-        c0[b].x = fma(t.w1, am1.x, fma(t.w0, a0.x, c0[b].x));
-        c0[b].y = fma(t.w1, am1.y, fma(t.w0, a0.y, c0[b].y));
-        c1[b].x = fma(t.w1, a0.x, fma(t.w0, ap1.x, c1[b].x));
-        c1[b].y = fma(t.w1, a0.y, fma(t.w0, ap1.y, c1[b].y));
+        if constexpr (sizeof(R) == 4 && F2) {
+          // packed FP32 (FFMA2, sm_100): one instruction per complex multiply-add,
+          // the same per-component roundings as the scalar form below
+          const float2 w0 = make_float2(t.w0, t.w0), w1 = make_float2(t.w1, t.w1);
+          c0[b] = __ffma2_rn(w1, am1, __ffma2_rn(w0, a0, c0[b]));
+          c1[b] = __ffma2_rn(w1, a0, __ffma2_rn(w0, ap1, c1[b]));
+        } else {
+          c0[b].x = fma(t.w1, am1.x, fma(t.w0, a0.x, c0[b].x));
+          c0[b].y = fma(t.w1, am1.y, fma(t.w0, a0.y, c0[b].y));
+          c1[b].x = fma(t.w1, a0.x, fma(t.w0, ap1.x, c1[b].x));
+          c1[b].y = fma(t.w1, a0.y, fma(t.w0, ap1.y, c1[b].y));
+        }
       };
       float dnf = 0.0f;
       if constexpr (sizeof(R) == 4) {
@@ -471,10 +479,10 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
 }
 
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
-          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1>
+          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB>;
+  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (TMAP) {
@@ -508,14 +516,14 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 
 // A fixed frame-batch width per precision (not chosen from F) keeps every
 // frame's arithmetic independent of how many frames share the launch, so
-// images are bit-identical under any batching or sharding.
+// images are bit-identical under any batching or sharding (all float variants
+// below use FB = 8 except 28/31, which exist for timing only).
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
-//   0: FB 8, 2-channel TMA tensor boxes, 3 buffers, 2 CTAs/SM (default; = 34)
-//   27: FB 4, bulk copies (earlier default)   1: FB 4, 6 buffers   2: FB 2, 8 buffers
-//   3: FB 8, 3 buffers   4: FB 4, no staging (L1 gathers)   5: FB 4, 4 buffers, 3 CTAs/SM
-//   6: FB 2, 4 buffers, 4 CTAs/SM   8: FB 8, 4 buffers, 2 CTAs/SM
-//   9/10/11: variant 0 with a 16x16 / 8x32 / 64x4 (depth x column) tile
-//   7: FB 4, no staging, 4 CTAs/SM
+//   0: FB 8, 2-channel TMA tensor boxes, 3 buffers, 2 CTAs/SM, FFMA2 accumulation
+//   34: variant 0 with scalar FFMA accumulation (round-1 default)
+//   28: FB 4, 3 buffers, 4 CTAs/SM   31: FB 4, 4 buffers, 3 CTAs/SM
+//   35: FB 4, 4 buffers, 16 consumer warps   41: FB 8, 3 buffers, 16 consumer warps, 1-channel boxes
+//   27: FB 4, per-frame bulk copies, 4 CTAs/SM (no tensor map)
 static int das_variant() {
   static int v = [] {
     const char* e = getenv("TIDAS_DAS_VARIANT");
@@ -526,53 +534,20 @@ static int das_variant() {
 
 template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
-  if (sizeof(R) == 8) return launch_das<R, AP, OUT, 1, 4>(p, A, out, st);
-  switch (das_variant()) {
-    case 0:  // measured best on B200 (cfg2): 8 frames per thread, TMA tensor boxes of
-             // [8 frames][2 channels][256 samples], 3 buffers, 2 CTAs/SM (6.3 us/frame)
-      return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
-    case 27: return launch_das<R, AP, OUT, 4, 4, 4>(p, A, out, st);  // previous default (bulk copies)
-    case 28: return launch_das<R, AP, OUT, 4, 3, 4, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
-    case 29: return launch_das<R, AP, OUT, 4, 2, 4, false, 4, 254, 0, 8, sizeof(R) == 4, 4>(p, A, out, st);
-    case 30: return launch_das<R, AP, OUT, 4, 3, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 4>(p, A, out, st);
-    case 31: return launch_das<R, AP, OUT, 4, 4, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
-    case 32: return launch_das<R, AP, OUT, 4, 6, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
-    case 33: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 4>(p, A, out, st);
-    case 34: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
-    case 35: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, sizeof(R) == 4, 2>(p, A, out, st);
-    case 36: return launch_das<R, AP, OUT, 4, 3, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 3>(p, A, out, st);
-    case 37: return launch_das<R, AP, OUT, 8, 4, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 1>(p, A, out, st);
-    case 38: return launch_das<R, AP, OUT, 8, 2, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 2>(p, A, out, st);
-    case 39: return launch_das<R, AP, OUT, 8, 2, 2, false, 4, 254, 0, 8, sizeof(R) == 4, 3>(p, A, out, st);
-    case 40: return launch_das<R, AP, OUT, 8, 3, 3, false, 4, 254, 0, 8, sizeof(R) == 4, 1>(p, A, out, st);
-    case 41: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 16, sizeof(R) == 4, 1>(p, A, out, st);
-    case 1: return launch_das<R, AP, OUT, 4, 6>(p, A, out, st);
-    case 2: return launch_das<R, AP, OUT, 2, 8>(p, A, out, st);
-    case 3: return launch_das<R, AP, OUT, 8, 3>(p, A, out, st);
-    case 4: return launch_das<R, AP, OUT, 4, 1, 3, true>(p, A, out, st);
-    case 5: return launch_das<R, AP, OUT, 4, 4, 3>(p, A, out, st);
-    case 6: return launch_das<R, AP, OUT, 2, 4, 4>(p, A, out, st);
-    case 7: return launch_das<R, AP, OUT, 4, 1, 4, true>(p, A, out, st);
-    case 8: return launch_das<R, AP, OUT, 8, 4, 2>(p, A, out, st);
-    case 9: return launch_das<R, AP, OUT, 4, 4, 4, false, 2>(p, A, out, st);
-    case 10: return launch_das<R, AP, OUT, 4, 4, 4, false, 1>(p, A, out, st);
-    case 11: return launch_das<R, AP, OUT, 4, 4, 4, false, 8>(p, A, out, st);
-    case 12: return launch_das<R, AP, OUT, 4, 8, 4, false, 4, 208>(p, A, out, st);
-    case 13: return launch_das<R, AP, OUT, 4, 6, 4, false, 4, 208>(p, A, out, st);
-    case 14: return launch_das<R, AP, OUT, 4, 8, 4, false, 2, 208>(p, A, out, st);
-    case 15: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, DAS_WMAX, 1>(p, A, out, st);  // diag: compute only
-    case 16: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, DAS_WMAX, 2>(p, A, out, st);  // diag: data only
-    case 17: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, DAS_WMAX, 0, 16>(p, A, out, st);  // 32 x 16 tile
-    case 18: return launch_das<R, AP, OUT, 4, 4, 2, false, 2, DAS_WMAX, 0, 16>(p, A, out, st);  // 16 x 32 tile
-    case 19: return launch_das<R, AP, OUT, 4, 4, 1, false, 4, DAS_WMAX, 0, 32>(p, A, out, st);  // 32 x 32 tile
-    case 20: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, DAS_WMAX, 2, 16>(p, A, out, st);  // diag data-only 32x16
-    case 21: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, DAS_WMAX, 3>(p, A, out, st);  // diag: data-only, 1 copy
-    case 22: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, DAS_WMAX, 4>(p, A, out, st);  // diag: barriers only
-    case 23: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, 254, 0, 8, sizeof(R) == 4>(p, A, out, st);  // TMA tensor
-    case 24: return launch_das<R, AP, OUT, 4, 4, 4, false, 4, 254, 2, 8, sizeof(R) == 4>(p, A, out, st);  // ... data only
-    case 25: return launch_das<R, AP, OUT, 4, 6, 4, false, 4, 254, 0, 8, sizeof(R) == 4>(p, A, out, st);
-    case 26: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, sizeof(R) == 4>(p, A, out, st);
-    default: return launch_das<R, AP, OUT, 4, 4>(p, A, out, st);
+  if constexpr (sizeof(R) == 8) {
+    return launch_das<R, AP, OUT, 1, 4>(p, A, out, st);
+  } else {
+    switch (das_variant()) {
+      case 34: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, false>(p, A, out, st);
+      case 27: return launch_das<R, AP, OUT, 4, 4, 4>(p, A, out, st);
+      case 28: return launch_das<R, AP, OUT, 4, 3, 4, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
+      case 31: return launch_das<R, AP, OUT, 4, 4, 3, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
+      case 35: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, true, 2>(p, A, out, st);
+      case 41: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 16, true, 1>(p, A, out, st);
+      default:  // measured best on B200 (cfg2): 8 frames per thread, TMA tensor boxes of
+                // [8 frames][2 channels][256 samples], 3 buffers, 2 CTAs/SM
+        return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
+    }
   }
 }
 
