@@ -12,6 +12,8 @@
 // (bluestein_* below), which keeps the exact length-N periodic semantics.
 #include <math.h>
 
+#include <algorithm>
+
 #include <mutex>
 #include <map>
 #include <tuple>
@@ -264,6 +266,310 @@ __global__ void __launch_bounds__((1 << LOGN) / 8) analytic_fused_kernel(const I
   }
 }
 
+// Persistent, TMA-staged form of analytic_fused_kernel (same arithmetic, so the
+// same bits): each CTA loops over channel pairs p = blockIdx.x + i gridDim.x.
+// Thread 0 streams pair i + 1's two input rows into the other half of a
+// double-buffered shared staging area with one cp.async.bulk per row
+// (mbarrier tx-count) while the CTA transforms pair i, so the HBM latency of
+// the input leaves the critical path; the real parts of the output are re-read
+// from the staging rows instead of being held in 16 registers across the FFT.
+// Needs 16-byte aligned rows (the launcher checks and otherwise uses
+// analytic_fused_kernel).
+__device__ __forceinline__ unsigned k1_su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void k1_bar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "K1W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1, %2;\n"
+      " @!p bra K1W_%=;\n}\n" ::"r"(k1_su32(b)), "r"(parity), "r"(1000000u) : "memory");
+}
+
+template <typename In, int LOGN>
+__device__ __forceinline__ void k1_issue_pair(const In* rf, int64_t stride, int64_t n_rows, int64_t pair, In* dst,
+                                              uint64_t* bar) {
+  constexpr int N = 1 << LOGN;
+  constexpr unsigned ROWB = N * sizeof(In);
+  const int64_t ra = 2 * pair;
+  const int nr = ra + 1 < n_rows ? 2 : 1;
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(k1_su32(bar)), "r"(nr * ROWB) : "memory");
+  for (int r = 0; r < nr; ++r)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(k1_su32(dst + r * N)), "l"(rf + (ra + r) * stride), "r"(ROWB), "r"(k1_su32(bar)) : "memory");
+}
+
+template <typename In, int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 8) analytic_stream_kernel(const In* __restrict__ rf, int64_t stride,
+                                                                        float scale, cplx<float>* __restrict__ out,
+                                                                        int64_t n_rows, int32_t* __restrict__ support) {
+  using R = float;
+  using C = cplx<R>;
+  constexpr int N = 1 << LOGN, NT = N / 8;
+  constexpr bool LAST_IN_REGS = (LOGN % 3) == 0;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  In* stage = reinterpret_cast<In*>(smem_raw);  // [2 buffers][2 rows][N]
+  C* s = reinterpret_cast<C*>(smem_raw + 4 * (size_t)N * sizeof(In));
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int first_nz[2][2], last_nz[2][2];
+  const int tid = threadIdx.x;
+  const int64_t n_pairs = (n_rows + 1) / 2;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(k1_su32(&bar[0])));
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(k1_su32(&bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (tid < 2) { first_nz[0][tid] = N; last_nz[0][tid] = -1; }
+  __syncthreads();
+  if (tid == 0 && (int64_t)blockIdx.x < n_pairs) k1_issue_pair<In, LOGN>(rf, stride, n_rows, blockIdx.x, stage, &bar[0]);
+  const R invN = R(1) / R(N);
+  int it = 0;
+  for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int64_t nxt = pair + gridDim.x;
+    if (tid == 0 && nxt < n_pairs) {
+      // the other buffer was last read in iteration it - 1, which ended at a barrier
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      k1_issue_pair<In, LOGN>(rf, stride, n_rows, nxt, stage + (size_t)(b ^ 1) * 2 * N, &bar[b ^ 1]);
+    }
+    const int64_t ra = 2 * pair;
+    const bool has_b = ra + 1 < n_rows;
+    const In* st_a = stage + (size_t)b * 2 * N;
+    const In* st_b = st_a + N;
+    k1_bar_wait(&bar[b], (unsigned)(it >> 1) & 1u);
+    C v[8];
+    int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int n = tid + k * NT;
+      const R xa = R(load_as_double(st_a + n)) * scale;
+      const R xb = has_b ? R(load_as_double(st_b + n)) * scale : R(0);
+      if (xa != R(0)) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+      if (xb != R(0)) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+      v[k].x = xa;
+      v[k].y = xb;
+    }
+    if (support) {  // slot b was reset in iteration it - 2 (or the prologue) before a barrier
+      if (lo_a < N) atomicMin(&first_nz[b][0], lo_a);
+      if (hi_a >= 0) atomicMax(&last_nz[b][0], hi_a);
+      if (lo_b < N) atomicMin(&first_nz[b][1], lo_b);
+      if (hi_b >= 0) atomicMax(&last_nz[b][1], hi_b);
+    }
+    pass8_fused<R, false, N, 1, false, true, false>(s, v, invN);  // inputs from registers
+    fused_rest<LOGN, 3, false>(s, v, invN);
+    pass8_fused<R, true, N, 1, true, true, true>(s, v, invN);     // Hilbert multiplier on load
+    fused_rest<LOGN, 3, true>(s, v, invN);
+    if constexpr (!LAST_IN_REGS) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = s[fpad(tid + k * NT)];
+    }
+    C* dst_a = out + ra * (int64_t)N;
+    C* dst_b = dst_a + N;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int n = tid + k * NT;
+      C a; a.x = R(load_as_double(st_a + n)) * scale; a.y = v[k].x;
+      dst_a[n] = a;
+      if (has_b) { C bb; bb.x = R(load_as_double(st_b + n)) * scale; bb.y = v[k].y; dst_b[n] = bb; }
+    }
+    if (support) {
+      __syncthreads();
+      if (tid == 0) {
+        for (int c = 0; c < (has_b ? 2 : 1); ++c) {
+          const bool any = last_nz[b][c] >= 0;
+          support[2 * (ra + c)] = any ? first_nz[b][c] : -1;
+          support[2 * (ra + c) + 1] = any ? last_nz[b][c] : -1;
+        }
+      }
+    }
+    if (tid < 2) { first_nz[b ^ 1][tid] = N; last_nz[b ^ 1][tid] = -1; }
+    __syncthreads();  // staging buffer b and s are free for the next pair
+  }
+}
+
+// ------------------------------------------- N = 4096: 64 x 64 in registers
+//
+// Four-step FFT with both 64-point stages in registers: thread t of a 64-thread
+// CTA owns 64 complex values, so a transform costs two 64-point register DFTs
+// (each 8 x 8: sixteen radix-8 butterflies and the W64 twiddles as constants),
+// one twiddle stage W4096^(t e) and ONE shared-memory transpose — against four
+// radix-8 passes with three shared-memory round trips and six CTA barriers in
+// the Stockham kernels above. Forward (thread t = n1 holds z[t + 64 m]):
+//   Y[n1, k2] = DFT64_m(z[n1 + 64 m]) W^(n1 k2);  X[k2 + 64 k1] = DFT64_n1(Y[n1, k2])
+// leaves thread t = k2 holding X[t + 64 k1]. The inverse consumes that layout
+// directly (the roles of the two indices swap, no reordering pass), so the
+// Hilbert transform of a channel pair is 4 register DFT64s, 2 transposes and 3
+// barriers, and thread t ends holding x[t + 64 n1] — coalesced stores.
+// Register slot order: dft64<INV, false> takes natural input and leaves
+// X[sig(j)] in slot j, sig(j) = (j >> 3) + 8 (j & 7); dft64<INV, true> takes
+// input permuted by sig and leaves natural output.
+__host__ __device__ constexpr int sig64(int j) { return (j >> 3) + 8 * (j & 7); }
+
+// cos / sin of 2 pi e / 64, e = 0..15 (the rest by symmetry)
+__device__ __forceinline__ float2 w64_first_octant(int e) {
+  constexpr float C[17] = {1.0f, 0.99518472667219688624f, 0.98078528040323044913f, 0.95694033573220886494f,
+                           0.92387953251128675613f, 0.88192126434835502971f, 0.83146961230254523708f,
+                           0.77301045336273696081f, 0.70710678118654752440f, 0.63439328416364549822f,
+                           0.55557023301960222474f, 0.47139673682599764856f, 0.38268343236508977173f,
+                           0.29028467725446236764f, 0.19509032201612826785f, 0.09801714032956060199f, 0.0f};
+  return make_float2(C[e], C[16 - e]);  // (cos, sin) of 2 pi e / 64 for e in [0, 16]
+}
+// v * W64^e, W64 = exp(-+ 2 pi i / 64), e compile-time after unrolling
+template <bool INV> __device__ __forceinline__ float2 tw64(float2 v, int e) {
+  e &= 63;
+  if (e == 0) return v;
+  if (e == 16) return mul_mi<INV>(v);
+  if (e == 32) return make_float2(-v.x, -v.y);
+  if (e == 48) return mul_mi<!INV>(v);
+  // exp(-i theta) for theta = 2 pi e / 64 in quadrant e / 16
+  const int q = e >> 4, r = e & 15;
+  const float2 cs = w64_first_octant(r);  // cos, sin of the in-quadrant angle
+  float c, s;  // exp(-i theta) = c + i s
+  if (q == 0) { c = cs.x; s = -cs.y; }
+  else if (q == 1) { c = -cs.y; s = -cs.x; }
+  else if (q == 2) { c = -cs.x; s = cs.y; }
+  else { c = cs.y; s = cs.x; }
+  if (INV) s = -s;
+  return make_float2(v.x * c - v.y * s, v.x * s + v.y * c);
+}
+
+template <bool INV, bool PERM_IN> __device__ __forceinline__ void dft64(float2 (&v)[64]) {
+  // logical input m = q + 8 p sits in slot m (natural) or sig(m) = p + 8 q (PERM_IN)
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float2 t[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) t[p] = v[PERM_IN ? p + 8 * q : q + 8 * p];
+    dft8<INV, float>(t);  // U[q][r] = sum_p x[q + 8 p] W8^(p r)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[PERM_IN ? r + 8 * q : q + 8 * r] = tw64<INV>(t[r], q * r);
+  }
+  // X[r + 8 s] = sum_q U[q][r] W8^(q s)
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    float2 t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = v[PERM_IN ? r + 8 * q : q + 8 * r];
+    dft8<INV, float>(t);
+    // natural output: X[r + 8 s] in slot r + 8 s; otherwise slot s + 8 r (= sig of r + 8 s)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[PERM_IN ? r + 8 * s : s + 8 * r] = t[s];
+  }
+}
+
+// v[j] *= W4096^(+-t e(j)), e(j) = sig(j) (PERM) or j; powers as W^(t a) W^(8 t b)
+// (e = a + 8 b) from 14 table reads, one rounding per product
+template <bool INV, bool PERM> __device__ __forceinline__ void twiddle4096(float2 (&v)[64], int t) {
+  constexpr int SH = TW_LOG - 12;
+  float2 wa[8], wb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    wa[k] = g_tw32[((t * k) & 4095) << SH];
+    wb[k] = g_tw32[((8 * t * k) & 4095) << SH];
+    if (INV) { wa[k].y = -wa[k].y; wb[k].y = -wb[k].y; }
+  }
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    const int e = PERM ? sig64(j) : j;
+    const int a = e & 7, b = e >> 3;
+    if (e == 0) continue;
+    const float2 w = a == 0 ? wb[b] : (b == 0 ? wa[a] : cmul(wa[a], wb[b]));
+    v[j] = cmul(v[j], w);
+  }
+}
+
+// Hilbert transform of one channel pair held as v[m] = (x_a, x_b)[t + 64 m];
+// on return slot j holds (H x_a, H x_b)[t + 64 sig(j)]. S: the 64 x 65 transpose
+// buffer; every thread must have finished with S before the call.
+__device__ __forceinline__ void hilbert4096_r64(float2 (&v)[64], float2* S, int t) {
+  constexpr int LP = 65;  // transpose rows padded to 65: conflict-free 8-byte columns
+  // forward: thread t = n1
+  dft64<false, false>(v);           // slot j: Y[t, sig(j)]
+  twiddle4096<false, true>(v, t);
+#pragma unroll
+  for (int j = 0; j < 64; ++j) S[sig64(j) * LP + t] = v[j];
+  __syncthreads();
+#pragma unroll
+  for (int n1 = 0; n1 < 64; ++n1) v[n1] = S[t * LP + n1];
+  dft64<false, false>(v);           // slot j: X[t + 64 sig(j)]
+  // Hilbert multiplier -i sgn(k) / N, k = t + 64 k1: k1 < 32 positive, >= 32 negative
+  const float invN = 1.0f / 4096.0f;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    const int k1 = sig64(j);
+    float2 r;
+    if (k1 < 32) { r.x = v[j].y * invN; r.y = -v[j].x * invN; }
+    else { r.x = -v[j].y * invN; r.y = v[j].x * invN; }
+    if (t == 0 && (k1 == 0 || k1 == 32)) r.x = r.y = 0.0f;  // DC and Nyquist
+    v[j] = r;
+  }
+  // inverse: thread t = k2 holds X[t + 64 k1] with k1 = sig(slot)
+  dft64<true, true>(v);             // slot n2 (natural): Z[t, n2]
+  twiddle4096<true, false>(v, t);
+  __syncthreads();                  // every thread has read its transpose column
+#pragma unroll
+  for (int n2 = 0; n2 < 64; ++n2) S[n2 * LP + t] = v[n2];
+  __syncthreads();
+#pragma unroll
+  for (int k2 = 0; k2 < 64; ++k2) v[k2] = S[t * LP + k2];
+  dft64<true, false>(v);            // slot j: x[t + 64 sig(j)]
+}
+
+template <typename In>
+__global__ void __launch_bounds__(64) analytic_r64_kernel(const In* __restrict__ rf, int64_t stride, float scale,
+                                                          cplx<float>* __restrict__ out, int64_t n_rows,
+                                                          int32_t* __restrict__ support) {
+  constexpr int N = 4096;
+  __shared__ float2 S[64 * 65];
+  __shared__ int first_nz[2], last_nz[2];
+  const int t = threadIdx.x;
+  const int64_t ra = 2 * (int64_t)blockIdx.x;
+  const bool has_b = ra + 1 < n_rows;
+  const In* src_a = rf + ra * stride;
+  const In* src_b = rf + (ra + 1) * stride;
+  if (t < 2) { first_nz[t] = N; last_nz[t] = -1; }
+  float2 v[64];
+#pragma unroll
+  for (int m = 0; m < 64; ++m) {
+    v[m].x = (float)load_as_double(src_a + t + 64 * m);
+    v[m].y = has_b ? (float)load_as_double(src_b + t + 64 * m) : 0.0f;
+  }
+  int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
+#pragma unroll
+  for (int m = 0; m < 64; ++m) {
+    v[m].x *= scale;
+    v[m].y *= scale;
+    const int n = t + 64 * m;
+    if (v[m].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+    if (v[m].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+  }
+  __syncthreads();  // first_nz / last_nz initialised
+  if (support) {
+    if (lo_a < N) atomicMin(&first_nz[0], lo_a);
+    if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
+    if (lo_b < N) atomicMin(&first_nz[1], lo_b);
+    if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
+  }
+  hilbert4096_r64(v, S, t);
+  // real parts = the inputs, re-read (L2)
+  cplx<float>* dst_a = out + ra * (int64_t)N;
+  cplx<float>* dst_b = dst_a + N;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    const int n = t + 64 * sig64(j);
+    float2 a; a.x = (float)load_as_double(src_a + n) * scale; a.y = v[j].x;
+    dst_a[n] = a;
+    if (has_b) { float2 b; b.x = (float)load_as_double(src_b + n) * scale; b.y = v[j].y; dst_b[n] = b; }
+  }
+  if (support) {
+    __syncthreads();
+    if (t == 0) {
+      for (int c = 0; c < (has_b ? 2 : 1); ++c) {
+        const bool any = last_nz[c] >= 0;
+        support[2 * (ra + c)] = any ? first_nz[c] : -1;
+        support[2 * (ra + c) + 1] = any ? last_nz[c] : -1;
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------------- Bluestein path
 //
 // DFT_N(x)_k = conj(b_k) * sum_n (x_n conj(b_n)) b_{k-n},  b_j = exp(i pi j^2 / N)
@@ -435,6 +741,37 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
     constexpr int EPT = sizeof(R) == 4 ? 8 : 16;
     auto kern = delay ? analytic_pow2_kernel<R, In, true, EPT> : analytic_pow2_kernel<R, In, false, EPT>;
     if constexpr (sizeof(R) == 4) {
+      const bool aligned = (reinterpret_cast<uintptr_t>(rf) % 16 == 0) && ((stride * sizeof(In)) % 16 == 0) &&
+                           ((N * sizeof(In)) % 16 == 0);
+      static const int k1_mode = [] {
+        // 0 = fused (one CTA per pair), 1 = persistent TMA-staged, 2 (default) = 1 except
+        // N = 4096, which runs in registers (64 x 64)
+        const char* e = getenv("TIDAS_K1_MODE");
+        return e ? atoi(e) : 2;
+      }();
+      if (!delay && logN == 12 && k1_mode == 2) {
+        analytic_r64_kernel<In><<<(unsigned)((n_rows + 1) / 2), 64, 0, st>>>(
+            rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support);
+        TIDAS_LAUNCH_CHECK();
+        return TIDAS_OK;
+      }
+      if (!delay && logN >= 11 && logN <= 13 && aligned && sizeof(In) <= 4 && k1_mode >= 1 &&
+          !getenv("TIDAS_K1_GENERIC")) {
+        auto ks = logN == 11 ? analytic_stream_kernel<In, 11>
+                             : (logN == 12 ? analytic_stream_kernel<In, 12> : analytic_stream_kernel<In, 13>);
+        const size_t smem_s = smem + 4 * (size_t)N * sizeof(In);
+        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(ks, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        int per_sm = 0, sms = 0;
+        TIDAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, N / 8, smem_s));
+        TIDAS_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int64_t pairs = (n_rows + 1) / 2;
+        const int64_t grid = std::min<int64_t>(pairs, (int64_t)std::max(per_sm, 1) * sms);
+        ks<<<(unsigned)grid, N / 8, smem_s, st>>>(rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out),
+                                                  n_rows, support);
+        TIDAS_LAUNCH_CHECK();
+        return TIDAS_OK;
+      }
       if (!delay && logN >= 11 && logN <= 13 && !getenv("TIDAS_K1_GENERIC")) {
         const int64_t ctasf = (n_rows + 1) / 2;
         auto kf = logN == 11 ? analytic_fused_kernel<In, 11>
