@@ -386,22 +386,14 @@ __global__ void __launch_bounds__((1 << LOGN) / 8) analytic_stream_kernel(const 
 
 // ------------------------------------------- N = 4096: 64 x 64 in registers
 //
-// Four-step FFT with both 64-point stages in registers: thread t of a 64-thread
-// CTA owns 64 complex values, so a transform costs two 64-point register DFTs
-// (each 8 x 8: sixteen radix-8 butterflies and the W64 twiddles as constants),
-// one twiddle stage W4096^(t e) and ONE shared-memory transpose — against four
-// radix-8 passes with three shared-memory round trips and six CTA barriers in
-// the Stockham kernels above. Forward (thread t = n1 holds z[t + 64 m]):
-//   Y[n1, k2] = DFT64_m(z[n1 + 64 m]) W^(n1 k2);  X[k2 + 64 k1] = DFT64_n1(Y[n1, k2])
-// leaves thread t = k2 holding X[t + 64 k1]. The inverse consumes that layout
-// directly (the roles of the two indices swap, no reordering pass), so the
-// Hilbert transform of a channel pair is 4 register DFT64s, 2 transposes and 3
-// barriers, and thread t ends holding x[t + 64 n1] — coalesced stores.
-// Register slot order: dft64<INV, false> takes natural input and leaves
-// X[sig(j)] in slot j, sig(j) = (j >> 3) + 8 (j & 7); dft64<INV, true> takes
-// input permuted by sig and leaves natural output.
-__host__ __device__ constexpr int sig64(int j) { return (j >> 3) + 8 * (j & 7); }
-
+// Four-step FFT with the 64-point stages in registers: N = 64 x 64,
+//   Y[n1, k2] = DFT64_m(z[n1 + 64 m]) W4096^(n1 k2);  X[k2 + 64 k1] = DFT64_n1(Y[n1, k2]),
+// so a transform is two register DFT64s (radix-8 / radix-4 butterflies with the
+// W64 twiddles as constants), one twiddle stage and ONE shared-memory transpose —
+// against four radix-8 passes with three shared-memory round trips and six CTA
+// barriers in the Stockham kernels above. The inverse consumes the forward's
+// output layout directly (the roles of the two indices swap, no reordering
+// pass): the Hilbert transform of a channel pair is 2 transposes and 3 barriers.
 // cos / sin of 2 pi e / 64, e = 0..15 (the rest by symmetry)
 __device__ __forceinline__ float2 w64_first_octant(int e) {
   constexpr float C[17] = {1.0f, 0.99518472667219688624f, 0.98078528040323044913f, 0.95694033573220886494f,
@@ -430,115 +422,118 @@ template <bool INV> __device__ __forceinline__ float2 tw64(float2 v, int e) {
   return make_float2(v.x * c - v.y * s, v.x * s + v.y * c);
 }
 
-template <bool INV, bool PERM_IN> __device__ __forceinline__ void dft64(float2 (&v)[64]) {
-  // logical input m = q + 8 p sits in slot m (natural) or sig(m) = p + 8 q (PERM_IN)
+// ------------------------- N = 4096, 128 threads: 32 values per thread
+//
+// Each 64-point column DFT is split over a lane pair (h = 0 / 1, lanes l and
+// l ^ 16): 32 values per thread (<= 128 registers, 4 CTAs / 16 warps per SM;
+// one thread per column with 64 values needs 255 registers and ran at 8 warps
+// per SM, 2.13 against 1.93 us per cfg2 frame) for one 16-value shuffle
+// exchange per 64-point DFT. Thread (t, h), t = 16 warp + (lane & 15).
+//   forward 64-point DFT, decimation in time: thread h holds the inputs
+//   m = h + 2 p (p = 0..31, natural slots), takes a 32-point DFT (E for h = 0,
+//   O for h = 1), h = 1 applies W64^k, the pair swaps half of its values and
+//   ends with the outputs X[16 h + i] (slot 2 i) and X[16 h + i + 32] (slot 2 i + 1);
+//   inverse 64-point DFT, decimation in frequency: consumes exactly that pair
+//   layout (a = X[k] + X[k + 32], b = (X[k] - X[k + 32]) W64^-k locally), swaps,
+//   and h = 0 / 1 takes the 32-point inverse DFT of a / b: slot j ends holding
+//   x[2 sig32(j) + h] — the forward input layout up to the sig32 slot order.
+// dft32: natural input, slot j <- X[sig32(j)], sig32(j) = (j >> 2) + 8 (j & 3).
+__host__ __device__ constexpr int sig32(int j) { return (j >> 2) + 8 * (j & 3); }
+__host__ __device__ constexpr int sig32_inv(int k) { return 4 * (k & 7) + (k >> 3); }
+
+template <bool INV> __device__ __forceinline__ void dft32(float2 (&v)[32]) {
+  // m = q + 4 p (q < 4, p < 8), k = r + 8 s (r < 8, s < 4)
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < 4; ++q) {
     float2 t[8];
 #pragma unroll
-    for (int p = 0; p < 8; ++p) t[p] = v[PERM_IN ? p + 8 * q : q + 8 * p];
-    dft8<INV, float>(t);  // U[q][r] = sum_p x[q + 8 p] W8^(p r)
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[PERM_IN ? r + 8 * q : q + 8 * r] = tw64<INV>(t[r], q * r);
-  }
-  // X[r + 8 s] = sum_q U[q][r] W8^(q s)
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    float2 t[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) t[q] = v[PERM_IN ? r + 8 * q : q + 8 * r];
+    for (int p = 0; p < 8; ++p) t[p] = v[q + 4 * p];
     dft8<INV, float>(t);
-    // natural output: X[r + 8 s] in slot r + 8 s; otherwise slot s + 8 r (= sig of r + 8 s)
 #pragma unroll
-    for (int s = 0; s < 8; ++s) v[PERM_IN ? r + 8 * s : s + 8 * r] = t[s];
+    for (int r = 0; r < 8; ++r) v[q + 4 * r] = tw64<INV>(t[r], 2 * q * r);  // W32^(q r)
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // slots 4 r .. 4 r + 3 hold U[q][r], q = 0..3
+    dft4<INV>(v[4 * r], v[4 * r + 1], v[4 * r + 2], v[4 * r + 3]);  // slot s + 4 r <- X[r + 8 s]
   }
 }
 
-// v[j] *= W4096^(+-t e(j)), e(j) = sig(j) (PERM) or j; powers as W^(t a) W^(8 t b)
-// (e = a + 8 b) from 14 table reads, one rounding per product
-template <bool INV, bool PERM> __device__ __forceinline__ void twiddle4096(float2 (&v)[64], int t) {
-  constexpr int SH = TW_LOG - 12;
-  float2 wa[8], wb[8];
+__device__ __forceinline__ float2 shfl16(float2 a) {
+  return make_float2(__shfl_xor_sync(0xffffffffu, a.x, 16), __shfl_xor_sync(0xffffffffu, a.y, 16));
+}
+__device__ __forceinline__ float2 csel(bool c, float2 a, float2 b) { return c ? a : b; }
+
+// forward (DIT) 64-point DFT over a lane pair; v: natural p (input m = h + 2 p);
+// w[2 i] = X[16 h + i], w[2 i + 1] = X[16 h + i + 32]
+template <bool INV> __device__ __forceinline__ void dft64_pair_dit(float2 (&v)[32], float2 (&w)[32], bool h) {
+  dft32<INV>(v);  // slot j: D[sig32(j)] (E on h = 0, O on h = 1)
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    wa[k] = g_tw32[((t * k) & 4095) << SH];
-    wb[k] = g_tw32[((8 * t * k) & 4095) << SH];
-    if (INV) { wa[k].y = -wa[k].y; wb[k].y = -wb[k].y; }
-  }
+  for (int j = 0; j < 32; ++j) v[j] = csel(h, tw64<INV>(v[j], sig32(j)), v[j]);  // O'[k] = W64^k O[k]
 #pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    const int e = PERM ? sig64(j) : j;
-    const int a = e & 7, b = e >> 3;
-    if (e == 0) continue;
-    const float2 w = a == 0 ? wb[b] : (b == 0 ? wa[a] : cmul(wa[a], wb[b]));
-    v[j] = cmul(v[j], w);
+  for (int i = 0; i < 16; ++i) {
+    // h = 0 sends E[16 + i], receives O'[i]; h = 1 sends O'[i], receives E[16 + i]
+    const float2 send = csel(h, v[sig32_inv(i)], v[sig32_inv(16 + i)]);
+    const float2 recv = shfl16(send);
+    const float2 e = csel(h, recv, v[sig32_inv(i)]);
+    const float2 o = csel(h, v[sig32_inv(16 + i)], recv);
+    w[2 * i] = cadd(e, o);
+    w[2 * i + 1] = csub(e, o);
   }
 }
 
-// Hilbert transform of one channel pair held as v[m] = (x_a, x_b)[t + 64 m];
-// on return slot j holds (H x_a, H x_b)[t + 64 sig(j)]. S: the 64 x 65 transpose
-// buffer; every thread must have finished with S before the call.
-__device__ __forceinline__ void hilbert4096_r64(float2 (&v)[64], float2* S, int t) {
-  constexpr int LP = 65;  // transpose rows padded to 65: conflict-free 8-byte columns
-  // forward: thread t = n1
-  dft64<false, false>(v);           // slot j: Y[t, sig(j)]
-  twiddle4096<false, true>(v, t);
+// inverse-direction (DIF) 64-point DFT over a lane pair; w: pair layout as above
+// (input index k = 16 h + i and k + 32); on return slot j of v holds output
+// n = 2 sig32(j) + h
+template <bool INV> __device__ __forceinline__ void dft64_pair_dif(float2 (&w)[32], float2 (&v)[32], bool h) {
+  float2 a[16], b[16];
 #pragma unroll
-  for (int j = 0; j < 64; ++j) S[sig64(j) * LP + t] = v[j];
-  __syncthreads();
-#pragma unroll
-  for (int n1 = 0; n1 < 64; ++n1) v[n1] = S[t * LP + n1];
-  dft64<false, false>(v);           // slot j: X[t + 64 sig(j)]
-  // Hilbert multiplier -i sgn(k) / N, k = t + 64 k1: k1 < 32 positive, >= 32 negative
-  const float invN = 1.0f / 4096.0f;
-#pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    const int k1 = sig64(j);
-    float2 r;
-    if (k1 < 32) { r.x = v[j].y * invN; r.y = -v[j].x * invN; }
-    else { r.x = -v[j].y * invN; r.y = v[j].x * invN; }
-    if (t == 0 && (k1 == 0 || k1 == 32)) r.x = r.y = 0.0f;  // DC and Nyquist
-    v[j] = r;
+  for (int i = 0; i < 16; ++i) {
+    a[i] = cadd(w[2 * i], w[2 * i + 1]);
+    const float2 d = csub(w[2 * i], w[2 * i + 1]);
+    b[i] = csel(h, tw64<INV>(d, 16 + i), tw64<INV>(d, i));  // W64^(-+ k), k = 16 h + i
   }
-  // inverse: thread t = k2 holds X[t + 64 k1] with k1 = sig(slot)
-  dft64<true, true>(v);             // slot n2 (natural): Z[t, n2]
-  twiddle4096<true, false>(v, t);
-  __syncthreads();                  // every thread has read its transpose column
 #pragma unroll
-  for (int n2 = 0; n2 < 64; ++n2) S[n2 * LP + t] = v[n2];
-  __syncthreads();
-#pragma unroll
-  for (int k2 = 0; k2 < 64; ++k2) v[k2] = S[t * LP + k2];
-  dft64<true, false>(v);            // slot j: x[t + 64 sig(j)]
+  for (int i = 0; i < 16; ++i) {
+    // h = 0 keeps a, needs a[16 + i] (from h = 1); h = 1 keeps b, needs b[i] (from h = 0)
+    const float2 recv = shfl16(csel(h, a[i], b[i]));
+    v[i] = csel(h, recv, a[i]);
+    v[16 + i] = csel(h, b[i], recv);
+  }
+  dft32<INV>(v);  // slot j: output 2 sig32(j) + h
 }
 
 template <typename In>
-__global__ void __launch_bounds__(64) analytic_r64_kernel(const In* __restrict__ rf, int64_t stride, float scale,
-                                                          cplx<float>* __restrict__ out, int64_t n_rows,
-                                                          int32_t* __restrict__ support) {
-  constexpr int N = 4096;
-  __shared__ float2 S[64 * 65];
+__global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restrict__ rf, int64_t stride, float scale,
+                                                           cplx<float>* __restrict__ out, int64_t n_rows,
+                                                           int32_t* __restrict__ support) {
+  constexpr int N = 4096, LP = 65;
+  constexpr int SH = TW_LOG - 12;
+  __shared__ float2 S[64 * LP];
   __shared__ int first_nz[2], last_nz[2];
-  const int t = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int t = (threadIdx.x >> 5) * 16 + (lane & 15);
+  const int hi = lane >> 4;
+  const bool h = hi != 0;
   const int64_t ra = 2 * (int64_t)blockIdx.x;
   const bool has_b = ra + 1 < n_rows;
   const In* src_a = rf + ra * stride;
   const In* src_b = rf + (ra + 1) * stride;
-  if (t < 2) { first_nz[t] = N; last_nz[t] = -1; }
-  float2 v[64];
+  if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  float2 v[32], w[32];
 #pragma unroll
-  for (int m = 0; m < 64; ++m) {
-    v[m].x = (float)load_as_double(src_a + t + 64 * m);
-    v[m].y = has_b ? (float)load_as_double(src_b + t + 64 * m) : 0.0f;
+  for (int p = 0; p < 32; ++p) {
+    const int n = t + 64 * (hi + 2 * p);
+    v[p].x = (float)load_as_double(src_a + n);
+    v[p].y = has_b ? (float)load_as_double(src_b + n) : 0.0f;
   }
   int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
 #pragma unroll
-  for (int m = 0; m < 64; ++m) {
-    v[m].x *= scale;
-    v[m].y *= scale;
-    const int n = t + 64 * m;
-    if (v[m].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
-    if (v[m].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+  for (int p = 0; p < 32; ++p) {
+    v[p].x *= scale;
+    v[p].y *= scale;
+    const int n = t + 64 * (hi + 2 * p);
+    if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+    if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
   }
   __syncthreads();  // first_nz / last_nz initialised
   if (support) {
@@ -547,20 +542,80 @@ __global__ void __launch_bounds__(64) analytic_r64_kernel(const In* __restrict__
     if (lo_b < N) atomicMin(&first_nz[1], lo_b);
     if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
   }
-  hilbert4096_r64(v, S, t);
+  // ---- forward, stage 1: thread (t = n1, h); w[2 i (+1)] = Y[n1, k2], k2 = 16 h + i (+ 32)
+  dft64_pair_dit<false>(v, w, h);
+  {  // W4096^(n1 k2), k2 = 16 h + i + 32 u = a + 8 b: a = i & 7, b = 2 h + (i >> 3) + 4 u
+    float2 wa[8], wb[4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) wa[a] = g_tw32[((t * a) & 4095) << SH];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) wb[c] = g_tw32[((8 * t * (2 * hi + (c & 1) + 4 * (c >> 1))) & 4095) << SH];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int a = i & 7, c = (i >> 3) + 2 * u;
+        w[2 * i + u] = cmul(w[2 * i + u], a == 0 ? wb[c] : cmul(wa[a], wb[c]));
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    S[(16 * hi + i) * LP + t] = w[2 * i];
+    S[(16 * hi + i + 32) * LP + t] = w[2 * i + 1];
+  }
+  __syncthreads();
+  // ---- forward, stage 2: thread (t = k2, h) takes n1 = h + 2 p
+#pragma unroll
+  for (int p = 0; p < 32; ++p) v[p] = S[t * LP + hi + 2 * p];
+  dft64_pair_dit<false>(v, w, h);  // w[2 i (+1)] = X[t + 64 k1], k1 = 16 h + i (+ 32)
+  // ---- Hilbert multiplier -i sgn(k) / N: slot 2 i positive, 2 i + 1 negative frequencies
+  const float invN = 1.0f / (float)N;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 p0 = w[2 * i], p1 = w[2 * i + 1];
+    w[2 * i] = make_float2(p0.y * invN, -p0.x * invN);
+    w[2 * i + 1] = make_float2(-p1.y * invN, p1.x * invN);
+  }
+  if (t == 0 && !h) { w[0] = make_float2(0.0f, 0.0f); w[1] = make_float2(0.0f, 0.0f); }  // DC, Nyquist
+  // ---- inverse, stage 1: over k1 for fixed k2 = t; slot j: Z[t, n2], n2 = 2 sig32(j) + h
+  dft64_pair_dif<true>(w, v, h);
+  {  // W4096^-(k2 n2), n2 = 2 sig32(j) + h = a + 8 b
+    float2 wa[4], wb[8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { wa[c] = g_tw32[((t * (2 * c + hi)) & 4095) << SH]; wa[c].y = -wa[c].y; }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) { wb[b] = g_tw32[((8 * t * b) & 4095) << SH]; wb[b].y = -wb[b].y; }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int e2 = 2 * sig32(j);  // n2 = e2 + h: a = (e2 & 7) + h, b = e2 >> 3
+      const int c = (e2 & 7) >> 1, b = e2 >> 3;
+      v[j] = cmul(v[j], cmul(wa[c], wb[b]));
+    }
+  }
+  __syncthreads();  // every thread has read its stage-2 column
+#pragma unroll
+  for (int j = 0; j < 32; ++j) S[(2 * sig32(j) + hi) * LP + t] = v[j];
+  __syncthreads();
+  // ---- inverse, stage 2: thread (t = n2, h) takes k2 = 16 h + i (+ 32) in the pair layout
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    w[2 * i] = S[t * LP + 16 * hi + i];
+    w[2 * i + 1] = S[t * LP + 16 * hi + i + 32];
+  }
+  dft64_pair_dif<true>(w, v, h);  // slot j: x[t + 64 (2 sig32(j) + h)]
   // real parts = the inputs, re-read (L2)
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
 #pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    const int n = t + 64 * sig64(j);
+  for (int j = 0; j < 32; ++j) {
+    const int n = t + 64 * (2 * sig32(j) + hi);
     float2 a; a.x = (float)load_as_double(src_a + n) * scale; a.y = v[j].x;
     dst_a[n] = a;
     if (has_b) { float2 b; b.x = (float)load_as_double(src_b + n) * scale; b.y = v[j].y; dst_b[n] = b; }
   }
   if (support) {
     __syncthreads();
-    if (t == 0) {
+    if (threadIdx.x == 0) {
       for (int c = 0; c < (has_b ? 2 : 1); ++c) {
         const bool any = last_nz[c] >= 0;
         support[2 * (ra + c)] = any ? first_nz[c] : -1;
@@ -745,12 +800,12 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
                            ((N * sizeof(In)) % 16 == 0);
       static const int k1_mode = [] {
         // 0 = fused (one CTA per pair), 1 = persistent TMA-staged, 2 (default) = 1 except
-        // N = 4096, which runs in registers (64 x 64)
+        // N = 4096, which runs as a 64 x 64 four-step in registers (analytic_r32_kernel)
         const char* e = getenv("TIDAS_K1_MODE");
         return e ? atoi(e) : 2;
       }();
       if (!delay && logN == 12 && k1_mode == 2) {
-        analytic_r64_kernel<In><<<(unsigned)((n_rows + 1) / 2), 64, 0, st>>>(
+        analytic_r32_kernel<In><<<(unsigned)((n_rows + 1) / 2), 128, 0, st>>>(
             rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support);
         TIDAS_LAUNCH_CHECK();
         return TIDAS_OK;

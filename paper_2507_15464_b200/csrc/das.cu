@@ -197,7 +197,8 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
 // empty[b] (all 8 consumer warps done); consumers never meet at a CTA barrier
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
-          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true>
+          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
+          bool U32 = false>
 __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams p,
                                                                    const cplx<R>* __restrict__ A,
                                                                    void* __restrict__ out_,
@@ -384,6 +385,9 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
       const int wn_hi = __reduce_max_sync(0xffffffffu, active_px ? n_hi : INT_MIN);
       const unsigned full_u = smem_u32(&full[0]), empty_u = smem_u32(&empty[0]);
       const C* win_lane = win - s0;  // + buf * SLOT + (b * CPB + c) * WSTRIDE + j
+      // U32: the same window addressed as a 32-bit shared-window offset (no generic-to-shared
+      // conversion per channel); element e of buffer b at win_u32 + 8 (b * SLOT + e)
+      const unsigned win_u32 = smem_u32(win) - 8u * (unsigned)s0;
       for (int kb = 0; kb < n_blk; ++kb) {
         const unsigned g = g0 + kb;
         const int buf = (int)(g % DAS_NBUF);
@@ -403,6 +407,21 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
             live = (t.w0 != R(0) || t.w1 != R(0));
           }
           if (!live) continue;
+          if constexpr (U32 && sizeof(R) == 4) {
+            if (staged && nfb == FB) {
+              const unsigned q0 = win_u32 + 8u * (unsigned)(buf * SLOT + c * DAS_WSTRIDE + t.j);
+#pragma unroll
+              for (int b = 0; b < FB; ++b) {
+                const unsigned q = q0 + 8u * (unsigned)(b * CPB * DAS_WSTRIDE);
+                float2 am1, a0v, ap1;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(am1.x), "=f"(am1.y) : "r"(q - 8u));
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a0v.x), "=f"(a0v.y) : "r"(q));
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(ap1.x), "=f"(ap1.y) : "r"(q + 8u));
+                accumulate(t, b, am1, a0v, ap1);
+              }
+              continue;
+            }
+          }
           if (staged) {
             const C* wb = win_lane + (size_t)buf * SLOT + c * DAS_WSTRIDE + t.j;
             if (nfb == FB) {  // CTA-uniform: no per-frame bounds in the common case
@@ -479,10 +498,11 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
 }
 
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
-          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true>
+          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
+          bool U32 = false>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2>;
+  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2, U32>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (TMAP) {
@@ -519,8 +539,9 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // images are bit-identical under any batching or sharding (all float variants
 // below use FB = 8 except 28/31, which exist for timing only).
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
-//   0: FB 8, 2-channel TMA tensor boxes, 3 buffers, 2 CTAs/SM, FFMA2 accumulation
-//   34: variant 0 with scalar FFMA accumulation (round-1 default)
+//   0: FB 8, 2-channel TMA tensor boxes, 3 buffers, 2 CTAs/SM, FFMA2 accumulation,
+//      gathers as ld.shared on 32-bit window offsets
+//   59: variant 0 with generic-pointer gathers   34: 59 with scalar FFMA (round-1 default)
 //   28: FB 4, 3 buffers, 4 CTAs/SM   31: FB 4, 4 buffers, 3 CTAs/SM
 //   35: FB 4, 4 buffers, 16 consumer warps   41: FB 8, 3 buffers, 16 consumer warps, 1-channel boxes
 //   27: FB 4, per-frame bulk copies, 4 CTAs/SM (no tensor map)
@@ -544,9 +565,10 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
       case 31: return launch_das<R, AP, OUT, 4, 4, 3, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
       case 35: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, true, 2>(p, A, out, st);
       case 41: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 16, true, 1>(p, A, out, st);
+      case 59: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, false>(p, A, out, st);
       default:  // measured best on B200 (cfg2): 8 frames per thread, TMA tensor boxes of
                 // [8 frames][2 channels][256 samples], 3 buffers, 2 CTAs/SM
-        return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
+        return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, true>(p, A, out, st);
     }
   }
 }
