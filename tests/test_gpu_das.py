@@ -59,7 +59,7 @@ def test_analytic_support_scan():
 
 @pytest.mark.parametrize("dtype", [np.float32, np.int16, np.float64])
 def test_analytic_4096_fused_odd_rows_and_support(dtype, rng):
-    """FP32 N = 4096 runs the register-fused kernel: odd row count (last CTA has
+    """FP32 N = 4096 runs the four-step register kernel: odd row count (last CTA has
     one channel), zero rows and head/tail zeros for the support scan."""
     x = (rng.standard_normal((7, 4096)) * (1000 if dtype == np.int16 else 1)).astype(dtype)
     x[2] = 0
@@ -73,6 +73,25 @@ def test_analytic_4096_fused_odd_rows_and_support(dtype, rng):
     s = sup.cpu().numpy()
     assert s[2].tolist() == [-1, -1] and s[3].tolist() == [700, 3000] and s[6].tolist() == [4095, 4095]
     assert s[0].tolist() == [int(np.flatnonzero(x[0])[0]), int(np.flatnonzero(x[0])[-1])]
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 8192])
+@pytest.mark.parametrize("pad, offset", [(0, 0), (1, 0), (0, 1), (4, 4)])
+def test_analytic_strided_rows_through_the_abi(n, pad, offset, rng):
+    """Row strides / base pointers that are not 16-byte aligned take the
+    non-TMA kernels; aligned ones the TMA-staged / register kernels — every
+    combination must give the same analytic rows (C ABI, row stride n + pad)."""
+    from paper_2507_15464_b200 import _lib
+    rows = 5
+    buf = torch.as_tensor(rng.standard_normal(rows * (n + pad) + offset).astype(np.float32)).to(DEV)
+    x = buf[offset:offset + rows * (n + pad)].view(rows, n + pad)[:, :n]
+    ref = od.analytic_signal(x.cpu().numpy().astype(np.float64))
+    out = torch.empty((rows, n), dtype=torch.complex64, device=DEV)
+    _lib.check(_lib.lib().tidas_rf_analytic(_lib.ptr(x), _lib.DTYPE_CODE[torch.float32], n + pad, 1.0,
+                                           _lib.ptr(out), _lib.PREC_F32, rows, n, None,
+                                           _lib.stream_handle(None)))
+    got = out.cpu().numpy()
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 2e-6
 
 
 def test_analytic_rejects_short_rows():
