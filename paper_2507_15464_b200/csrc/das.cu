@@ -14,9 +14,10 @@
 //
 // Layout / schedule (B200, default variant — case 0 of the variant table):
 //   * CTA = 8 consumer warps + 1 producer warp, 2 CTAs per SM. The consumers
-//     cover 32 depths x 8 columns; a warp covers 8 depths x 4 columns so the
-//     16 lanes of a half-warp read nearly coincident taps (shared-memory
-//     wavefronts ~1.5x the minimum). Each thread owns one pixel for FB = 8
+//     cover 32 depths x 8 columns; a warp covers 4 depths x 8 columns, so the
+//     16 lanes of a half-warp (2 depths x 8 columns) read taps within ~16
+//     samples of each other: nearby columns share taps (broadcast) and few
+//     lanes sit 16 samples (one bank period of complex64) apart. Each thread owns one pixel for FB = 8
 //     frames, so the time-of-flight math (FP32, cancellation-free
 //     s = -dx^2 / (sqrt(dx^2 + z^2) + z) in sample units) is paid once per
 //     (pixel, channel) and reused for 8 frames.
@@ -198,7 +199,7 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
           int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
-          bool U32 = false>
+          bool U32 = false, int WZ = 8>
 __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams p,
                                                                    const cplx<R>* __restrict__ A,
                                                                    void* __restrict__ out_,
@@ -213,12 +214,12 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
   const int lane = threadIdx.x, wid = threadIdx.y;
   const int tid = wid * 32 + lane;
   const bool producer = wid == NW;  // NW consumer warps, then the producer warp
-  // each consumer warp covers 8 depths x 4 adjacent columns: the 16 lanes of a
-  // half-warp read nearly coincident taps (shared-memory wavefronts ~1.5x min);
-  // the CTA is DG depth groups x (8 / DG) column groups of warps
+  // each consumer warp covers WZ depths x WX = 32 / WZ adjacent columns (default
+  // 4 x 8); the CTA is DG depth groups x (NW / DG) column groups of warps
   constexpr int CG = NW / DG;
-  const int iz = blockIdx.x * (8 * DG) + (wid / CG) * 8 + (lane >> 2);
-  const int ix = blockIdx.y * (4 * CG) + (wid % CG) * 4 + (lane & 3);
+  constexpr int WX = 32 / WZ;
+  const int iz = blockIdx.x * (WZ * DG) + (wid / CG) * WZ + lane / WX;
+  const int ix = blockIdx.y * (WX * CG) + (wid % CG) * WX + lane % WX;
   const int f0 = blockIdx.z * FB;
   const bool pix = !producer && (iz < p.nz) && (ix < p.nx);
   const int half = p.E / 2;
@@ -499,10 +500,10 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
 
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
           int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
-          bool U32 = false>
+          bool U32 = false, int WZ = 8>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2, U32>;
+  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2, U32, WZ>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (TMAP) {
@@ -526,7 +527,7 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
   const size_t smem = sizeof(C) * DAS_NBUF * FB * CPB * (WCAP + 2);
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 block(32, NW + 1);  // NW consumer warps + 1 producer warp
-  constexpr int TZ = 8 * DG, TXC = 4 * (NW / DG);
+  constexpr int TZ = WZ * DG, TXC = (32 / WZ) * (NW / DG);
   dim3 grid((p.nz + TZ - 1) / TZ, (p.nx + TXC - 1) / TXC, (p.F + FB - 1) / FB);
   TIDAS_REQUIRE(grid.y <= 65535 && grid.z <= 65535, "pixel grid / frame batch too large");
   kern<<<grid, block, smem, st>>>(p, reinterpret_cast<const C*>(A), out, tmap);
@@ -540,8 +541,11 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // below use FB = 8 except 28/31, which exist for timing only).
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
 //   0: FB 8, 2-channel TMA tensor boxes, 3 buffers, 2 CTAs/SM, FFMA2 accumulation,
-//      gathers as ld.shared on 32-bit window offsets
-//   59: variant 0 with generic-pointer gathers   34: 59 with scalar FFMA (round-1 default)
+//      gathers as ld.shared on 32-bit window offsets, warps of 4 depths x 8 columns
+//      (a half-warp spans ~2 depths = ~8 + lateral samples: fewer distance-16 bank
+//      conflicts than 8 x 4 warps, 5.99 against 6.12 us/frame)
+//   58: variant 0 with 8 x 4 warps   62: 2 x 16 warps (CTA 16 x 16)
+//   59: 58 with generic-pointer gathers   34: 59 with scalar FFMA (round-1 default)
 //   28: FB 4, 3 buffers, 4 CTAs/SM   31: FB 4, 4 buffers, 3 CTAs/SM
 //   35: FB 4, 4 buffers, 16 consumer warps   41: FB 8, 3 buffers, 16 consumer warps, 1-channel boxes
 //   27: FB 4, per-frame bulk copies, 4 CTAs/SM (no tensor map)
@@ -565,10 +569,12 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
       case 31: return launch_das<R, AP, OUT, 4, 4, 3, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
       case 35: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, true, 2>(p, A, out, st);
       case 41: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 16, true, 1>(p, A, out, st);
+      case 58: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, true, 8>(p, A, out, st);
+      case 62: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 2>(p, A, out, st);
       case 59: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, false>(p, A, out, st);
       default:  // measured best on B200 (cfg2): 8 frames per thread, TMA tensor boxes of
                 // [8 frames][2 channels][256 samples], 3 buffers, 2 CTAs/SM
-        return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, true>(p, A, out, st);
+        return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
     }
   }
 }
