@@ -13,7 +13,7 @@
 // so each (pixel, channel) reads three consecutive complex samples.
 //
 // Layout / schedule (B200, default variant — case 0 of the variant table):
-//   * CTA = 8 consumer warps + 1 producer warp, 2 CTAs per SM. The consumers
+//   * CTA = 8 consumer warps + 1 producer warp, 3 CTAs per SM. The consumers
 //     cover 32 depths x 8 columns; a warp covers 4 depths x 8 columns, so the
 //     16 lanes of a half-warp (2 depths x 8 columns) read taps within ~16
 //     samples of each other: nearby columns share taps (broadcast) and few
@@ -26,10 +26,10 @@
 //     every channel) is fetched by the producer warp as ONE TMA tensor copy
 //     per 2 channels: a box [8 frames][2 channels][256 samples] of the 4-D
 //     tensor map over the analytic RF [F][A][E][N] (complex64 as 8-byte
-//     elements). Three such buffers rotate under full / empty mbarriers (the
+//     elements). Two such buffers rotate under full / empty mbarriers (the
 //     consumers arrive per warp on "empty"), so no CTA-wide barrier sits in
 //     the channel loop and the copy of channels c+2, c+3 overlaps the gather
-//     of channels c, c+1.
+//     of channels c, c+1 (64 KB per CTA, so three CTAs fit an SM).
 //   * t* (one per pixel and transmit) is precomputed in float64 (plane-wave
 //     table kernel or the host's focused-transmit table) and split into an
 //     integer sample index plus an FP32 fraction — the FP32 ulp at index 8192
@@ -540,11 +540,13 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // images are bit-identical under any batching or sharding (all float variants
 // below use FB = 8 except 28/31, which exist for timing only).
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
-//   0: FB 8, 2-channel TMA tensor boxes, 3 buffers, 2 CTAs/SM, FFMA2 accumulation,
-//      gathers as ld.shared on 32-bit window offsets, warps of 4 depths x 8 columns
-//      (a half-warp spans ~2 depths = ~8 + lateral samples: fewer distance-16 bank
-//      conflicts than 8 x 4 warps, 5.99 against 6.12 us/frame)
-//   58: variant 0 with 8 x 4 warps   62: 2 x 16 warps (CTA 16 x 16)
+//   0: FB 8, 2-channel TMA tensor boxes, 2 buffers, 3 CTAs/SM (27 warps: the
+//      kernel is latency-bound once the bank conflicts are gone; 5.70 us/frame),
+//      FFMA2 accumulation, gathers as ld.shared on 32-bit window offsets, warps
+//      of 4 depths x 8 columns (a half-warp spans ~2 depths = ~8 + lateral
+//      samples: 1.0M instead of 16.1M bank conflicts per 64 frames with 8 x 4)
+//   73: FB 6, 3 buffers, 3 CTAs/SM   57: FB 8, 3 buffers, 2 CTAs/SM (5.99 us)
+//   58: 57 with 8 x 4 warps (6.12 us)   62: 2 x 16 warps (CTA 16 x 16)
 //   59: 58 with generic-pointer gathers   34: 59 with scalar FFMA (round-1 default)
 //   28: FB 4, 3 buffers, 4 CTAs/SM   31: FB 4, 4 buffers, 3 CTAs/SM
 //   35: FB 4, 4 buffers, 16 consumer warps   41: FB 8, 3 buffers, 16 consumer warps, 1-channel boxes
@@ -569,12 +571,14 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
       case 31: return launch_das<R, AP, OUT, 4, 4, 3, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
       case 35: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, true, 2>(p, A, out, st);
       case 41: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 16, true, 1>(p, A, out, st);
+      case 57: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 58: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, true, 8>(p, A, out, st);
+      case 73: return launch_das<R, AP, OUT, 6, 3, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 62: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 2>(p, A, out, st);
       case 59: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, false>(p, A, out, st);
       default:  // measured best on B200 (cfg2): 8 frames per thread, TMA tensor boxes of
-                // [8 frames][2 channels][256 samples], 3 buffers, 2 CTAs/SM
-        return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
+                // [8 frames][2 channels][256 samples], 2 buffers, 3 CTAs/SM
+        return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
     }
   }
 }
