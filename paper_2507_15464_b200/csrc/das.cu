@@ -541,7 +541,8 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // below use FB = 8 except 28/31, which exist for timing only).
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
 //   0: FB 8, 2-channel TMA tensor boxes, 2 buffers, 3 CTAs/SM (27 warps: the
-//      kernel is latency-bound once the bank conflicts are gone; 5.70 us/frame),
+//      kernel is latency-bound once the bank conflicts are gone; 5.70 us/frame;
+//      multi-transmit / complex-output plans use 57 instead, see dispatch_fb),
 //      FFMA2 accumulation, gathers as ld.shared on 32-bit window offsets, warps
 //      of 4 depths x 8 columns (a half-warp spans ~2 depths = ~8 + lateral
 //      samples: 1.0M instead of 16.1M bank conflicts per 64 frames with 8 x 4)
@@ -576,9 +577,16 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
       case 73: return launch_das<R, AP, OUT, 6, 3, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 62: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 2>(p, A, out, st);
       case 59: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, false>(p, A, out, st);
-      default:  // measured best on B200 (cfg2): 8 frames per thread, TMA tensor boxes of
-                // [8 frames][2 channels][256 samples], 2 buffers, 3 CTAs/SM
-        return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
+      default:
+        // measured best on B200: 8 frames per thread, TMA tensor boxes of [8 frames][2
+        // channels][256 samples]; single-transmit envelope images (cfg1 / 2 / 5) with 2
+        // buffers and 3 CTAs/SM, multi-transmit or complex accumulation (cfg3: 11 angles,
+        // coherent — more registers, and a pipeline refill per transmit) with 3 buffers
+        // and 2 CTAs/SM (3663 against 3367 frames/s). The choice depends on the plan only,
+        // never on the frame count, so images stay bitwise batching-invariant.
+        if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1)
+          return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
+        return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
     }
   }
 }
