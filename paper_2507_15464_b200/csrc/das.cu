@@ -199,7 +199,7 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
           int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
-          bool U32 = false, int WZ = 8>
+          bool U32 = false, int WZ = 8, bool ONE_TX = false>
 __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams p,
                                                                    const cplx<R>* __restrict__ A,
                                                                    void* __restrict__ out_,
@@ -281,7 +281,10 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
 
   const int64_t rowN = p.N;
   unsigned g0 = 0;  // windows streamed before this transmit (buffer g % NBUF, use g / NBUF)
-  for (int a = 0; a < p.A; ++a) {
+  // ONE_TX: a single transmit known at compile time, so the frame accumulators
+  // are not live across the channel loop (fewer registers at 3 CTAs/SM)
+  const int n_tx = ONE_TX ? 1 : p.A;
+  for (int a = 0; a < n_tx; ++a) {
     // arrival split into integer index + fraction in float64
     int k0 = 0;
     R fr = R(0);
@@ -500,10 +503,10 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
 
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
           int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
-          bool U32 = false, int WZ = 8>
+          bool U32 = false, int WZ = 8, bool ONE_TX = false>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2, U32, WZ>;
+  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2, U32, WZ, ONE_TX>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (TMAP) {
@@ -572,6 +575,7 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
       case 31: return launch_das<R, AP, OUT, 4, 4, 3, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
       case 35: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, true, 2>(p, A, out, st);
       case 41: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 16, true, 1>(p, A, out, st);
+      case 56: return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 57: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 58: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, true, 8>(p, A, out, st);
       case 73: return launch_das<R, AP, OUT, 6, 3, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
@@ -585,7 +589,7 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
         // and 2 CTAs/SM (3663 against 3367 frames/s). The choice depends on the plan only,
         // never on the frame count, so images stay bitwise batching-invariant.
         if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1)
-          return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
+          return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true>(p, A, out, st);
         return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
     }
   }
