@@ -365,8 +365,19 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
       C c0[FB], c1[FB];
 #pragma unroll
       for (int b = 0; b < FB; ++b) { c0[b].x = c0[b].y = R(0); c1[b].x = c1[b].y = R(0); }
+      // complex outputs (coherent / IQ) are linear in the samples, so the
+      // interpolation between C(k0) and C(k0 + 1) folds into per-pair weights
+      // and one accumulator per frame carries the whole sum over transmits:
+      //   (1 - f) C(k0) + f C(k0 + 1) = sum_n u_-1 A[j - 1] + u_0 A[j] + u_+1 A[j + 1]
+      //   u_-1 = w1 (1 - f), u_0 = w0 (1 - f) + w1 f, u_+1 = w0 f
+      constexpr bool FOLD_IQ = sizeof(R) == 4 && F2 && OUT != TIDAS_OUT_ENVELOPE;
       auto accumulate = [&](const Tap<R>& t, int b, C am1, C a0, C ap1) {
-        if constexpr (sizeof(R) == 4 && F2) {
+        if constexpr (FOLD_IQ) {
+          const float g = 1.0f - fr;
+          const float um = t.w1 * g, up = t.w0 * fr, u0 = fmaf(t.w0, g, t.w1 * fr);
+          acc_iq[b] = __ffma2_rn(make_float2(um, um), am1,
+                                 __ffma2_rn(make_float2(u0, u0), a0, __ffma2_rn(make_float2(up, up), ap1, acc_iq[b])));
+        } else if constexpr (sizeof(R) == 4 && F2) {
           // packed FP32 (FFMA2, sm_100): one instruction per complex multiply-add,
           // the same per-component roundings as the scalar form below
           const float2 w0 = make_float2(t.w0, t.w0), w1 = make_float2(t.w1, t.w1);
@@ -456,7 +467,7 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
           if (DIAG != 1 && lane == 0) mbar_arrive_u32(empty_u + 8u * buf);
         }
       }
-      if (active_px) {
+      if (active_px && !FOLD_IQ) {
 #pragma unroll
         for (int b = 0; b < FB; ++b) {
           if (OUT == TIDAS_OUT_ENVELOPE) {
@@ -585,8 +596,8 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
         // measured best on B200: 8 frames per thread, TMA tensor boxes of [8 frames][2
         // channels][256 samples]; single-transmit envelope images (cfg1 / 2 / 5) with 2
         // buffers and 3 CTAs/SM, multi-transmit or complex accumulation (cfg3: 11 angles,
-        // coherent — more registers, and a pipeline refill per transmit) with 3 buffers
-        // and 2 CTAs/SM (3663 against 3367 frames/s). The choice depends on the plan only,
+        // coherent — a pipeline refill per transmit) with 3 buffers and 2 CTAs/SM
+        // (3663 against 3367 frames/s before the folded complex accumulation; equal after). The choice depends on the plan only,
         // never on the frame count, so images stay bitwise batching-invariant.
         if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1)
           return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true>(p, A, out, st);
