@@ -625,6 +625,238 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   }
 }
 
+// ------------------------ N = 8192, 256 threads: 32 values per thread
+//
+// Four-step 8192 = 64 x 128: n = n1 + 64 m, k = k2 + 128 k1,
+//   Y[n1, k2] = DFT128_m(x[n1 + 64 m]) W8192^(n1 k2);  X[k2 + 128 k1] = DFT64_n1(Y[n1, k2]).
+// The 64-point DFTs run over lane pairs exactly as in analytic_r32_kernel; each
+// 128-point DFT runs over a lane quad (q0, q1) as one more radix-2 level on top
+// of the pair DFT: the quad's q0 = 0 / 1 halves take the pair DFT-64 of the even
+// / odd samples, q0 = 1 applies W128^k, and one 16-value xor-8 exchange forms
+// X[k] = E[k] + W128^k O[k] and X[k + 64] = E[k] - W128^k O[k]. The inverse
+// mirrors it (decimation in frequency). Quad roles: column n1 = 8 warp + (lane & 7),
+// q0 = (lane >> 3) & 1, q1 = lane >> 4; pair roles: row k2 = 16 warp + (lane & 15),
+// h = lane >> 4.
+// cos / sin of 2 pi e / 128 for e in [0, 32]
+__device__ __forceinline__ float2 w128_first_octant(int e) {
+  constexpr float C[33] = {
+      1.0f, 0.99879545620517239271f, 0.99518472667219688624f, 0.98917650996478097345f,
+      0.98078528040323044913f, 0.97003125319454399260f, 0.95694033573220886494f, 0.94154406518302077841f,
+      0.92387953251128675613f, 0.90398929312344333159f, 0.88192126434835502971f, 0.85772861000027206990f,
+      0.83146961230254523708f, 0.80320753148064490981f, 0.77301045336273696081f, 0.74095112535495909118f,
+      0.70710678118654752440f, 0.67155895484701840063f, 0.63439328416364549822f, 0.59569930449243334347f,
+      0.55557023301960222474f, 0.51410274419322172659f, 0.47139673682599764856f, 0.42755509343028209432f,
+      0.38268343236508977173f, 0.33688985339222005069f, 0.29028467725446236764f, 0.24298017990326388995f,
+      0.19509032201612826785f, 0.14673047445536175166f, 0.09801714032956060199f, 0.04906767432741801426f, 0.0f};
+  return make_float2(C[e], C[32 - e]);
+}
+// v * W128^e (W128 = exp(-+ 2 pi i / 128)), e compile-time after unrolling
+template <bool INV> __device__ __forceinline__ float2 tw128(float2 v, int e) {
+  e &= 127;
+  if ((e & 1) == 0) return tw64<INV>(v, e >> 1);
+  const int q = e >> 5, r = e & 31;
+  const float2 cs = w128_first_octant(r);
+  float c, s;  // exp(-i theta) = c + i s
+  if (q == 0) { c = cs.x; s = -cs.y; }
+  else if (q == 1) { c = -cs.y; s = -cs.x; }
+  else if (q == 2) { c = -cs.x; s = cs.y; }
+  else { c = cs.y; s = cs.x; }
+  if (INV) s = -s;
+  return make_float2(v.x * c - v.y * s, v.x * s + v.y * c);
+}
+
+__device__ __forceinline__ float2 shfl8(float2 a) {
+  return make_float2(__shfl_xor_sync(0xffffffffu, a.x, 8), __shfl_xor_sync(0xffffffffu, a.y, 8));
+}
+
+// forward 128-point DFT over a lane quad; v: natural p, input m = q0 + 2 q1 + 4 p;
+// y[4 i + 2 u + t] = X[16 q1 + 8 q0 + i + 32 u + 64 t] (i < 8, u, t in {0, 1})
+__device__ __forceinline__ void dft128_quad_dit(float2 (&v)[32], float2 (&y)[32], bool q0, bool q1) {
+  float2 w[32];
+  dft64_pair_dit<false>(v, w, q1);  // w[2 i + u] = D[16 q1 + i + 32 u], D = E (q0 = 0) / O (q0 = 1)
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)  // O'[k] = W128^k O[k], k = 16 q1 + i + 32 u
+      w[2 * i + u] = csel(q0, csel(q1, tw128<false>(w[2 * i + u], 16 + i + 32 * u), tw128<false>(w[2 * i + u], i + 32 * u)),
+                          w[2 * i + u]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      // q0 = 0 keeps k = ... + i (E), needs O'[... + i]; q0 = 1 keeps k = ... + 8 + i (O'), needs E[... + 8 + i]
+      const float2 send = csel(q0, w[2 * i + u], w[2 * (i + 8) + u]);
+      const float2 recv = shfl8(send);
+      const float2 e = csel(q0, recv, w[2 * i + u]);
+      const float2 o = csel(q0, w[2 * (i + 8) + u], recv);
+      y[4 * i + 2 * u] = cadd(e, o);
+      y[4 * i + 2 * u + 1] = csub(e, o);
+    }
+}
+
+// inverse-direction 128-point DFT over a lane quad; y: the layout above;
+// on return slot j of v holds output m = q0 + 2 q1 + 4 sig32(j)
+template <bool INV> __device__ __forceinline__ void dft128_quad_dif(float2 (&y)[32], float2 (&v)[32], bool q0, bool q1) {
+  float2 ab[32];  // ab[2 i + u]: a (q0 = 0 keeps) or b (q0 = 1 keeps) for k = 16 q1 + 8 q0 + i + 32 u
+  float2 other[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float2 x0 = y[4 * i + 2 * u], x1 = y[4 * i + 2 * u + 1];  // Z[k], Z[k + 64]
+      const float2 a = cadd(x0, x1);
+      const float2 d = csub(x0, x1);
+      // b = d W128^-k, k = 16 q1 + 8 q0 + i + 32 u
+      const float2 b = csel(q1, csel(q0, tw128<INV>(d, 24 + i + 32 * u), tw128<INV>(d, 16 + i + 32 * u)),
+                            csel(q0, tw128<INV>(d, 8 + i + 32 * u), tw128<INV>(d, i + 32 * u)));
+      // q0 = 0 computes IDFT64(a) and sends b; q0 = 1 computes IDFT64(b) and sends a
+      const float2 recv = shfl8(csel(q0, a, b));
+      ab[2 * i + u] = csel(q0, b, a);
+      other[2 * i + u] = recv;
+    }
+  // pair layout for dft64_pair_dif: w[2 i + u] = c[16 q1 + i + 32 u], i < 16
+  float2 w[32];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      w[2 * i + u] = csel(q0, other[2 * i + u], ab[2 * i + u]);            // k-offset i: owned by q0 = 0
+      w[2 * (i + 8) + u] = csel(q0, ab[2 * i + u], other[2 * i + u]);      // k-offset 8 + i: owned by q0 = 1
+    }
+  dft64_pair_dif<INV>(w, v, q1);  // slot j: output m'' = 2 sig32(j) + q1 of the half-length inverse
+}
+
+template <typename In>
+__global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __restrict__ rf, int64_t stride, float scale,
+                                                                cplx<float>* __restrict__ out, int64_t n_rows,
+                                                                int32_t* __restrict__ support) {
+  constexpr int N = 8192;
+  constexpr int LP1 = 65, LP2 = 129;  // [128][65] and [64][129] transposes: conflict-free columns
+  constexpr int SH = TW_LOG - 13;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* S = reinterpret_cast<float2*>(smem_raw);
+  __shared__ int first_nz[2], last_nz[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n1 = warp * 8 + (lane & 7);            // quad roles
+  const int q0i = (lane >> 3) & 1, q1i = lane >> 4;
+  const bool q0 = q0i != 0, q1 = q1i != 0;
+  const int k2r = warp * 16 + (lane & 15);         // pair roles
+  const int hi = lane >> 4;
+  const bool h = hi != 0;
+  const int64_t ra = 2 * (int64_t)blockIdx.x;
+  const bool has_b = ra + 1 < n_rows;
+  const In* src_a = rf + ra * stride;
+  const In* src_b = rf + (ra + 1) * stride;
+  if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  float2 v[32], y[32];
+  const int mq = q0i + 2 * q1i;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    const int n = n1 + 64 * (mq + 4 * p);
+    v[p].x = (float)load_as_double(src_a + n);
+    v[p].y = has_b ? (float)load_as_double(src_b + n) : 0.0f;
+  }
+  int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    v[p].x *= scale;
+    v[p].y *= scale;
+    const int n = n1 + 64 * (mq + 4 * p);
+    if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+    if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+  }
+  __syncthreads();  // first_nz / last_nz initialised
+  if (support) {
+    if (lo_a < N) atomicMin(&first_nz[0], lo_a);
+    if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
+    if (lo_b < N) atomicMin(&first_nz[1], lo_b);
+    if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
+  }
+  // ---- forward stage 1 (quads): y[4 i + 2 u + t] = Y[n1, k2], k2 = 16 q1 + 8 q0 + i + 32 u + 64 t
+  dft128_quad_dit(v, y, q0, q1);
+  {  // W8192^(n1 k2), k2 = a + 8 b: a = i, b = q0 + 2 q1 + 4 u + 8 t
+    float2 wa[8], wb[4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) wa[a] = g_tw32[((n1 * a) & 8191) << SH];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) wb[c] = g_tw32[((8 * n1 * (mq + 4 * c)) & 8191) << SH];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // c = u + 2 t
+        const int slot = 4 * i + 2 * (c & 1) + (c >> 1);
+        y[slot] = cmul(y[slot], i == 0 ? wb[c] : cmul(wa[i], wb[c]));
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k2 = 16 * q1i + 8 * q0i + i + 32 * (c & 1) + 64 * (c >> 1);
+      S[k2 * LP1 + n1] = y[4 * i + 2 * (c & 1) + (c >> 1)];
+    }
+  __syncthreads();
+  // ---- forward stage 2 (pairs): thread (k2, h) takes n1 = h + 2 p
+#pragma unroll
+  for (int p = 0; p < 32; ++p) v[p] = S[k2r * LP1 + hi + 2 * p];
+  dft64_pair_dit<false>(v, y, h);  // y[2 i (+1)] = X[k2 + 128 k1], k1 = 16 h + i (+ 32)
+  // ---- Hilbert multiplier -i sgn(k) / N: slot 2 i positive, 2 i + 1 negative frequencies
+  const float invN = 1.0f / (float)N;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 p0 = y[2 * i], p1 = y[2 * i + 1];
+    y[2 * i] = make_float2(p0.y * invN, -p0.x * invN);
+    y[2 * i + 1] = make_float2(-p1.y * invN, p1.x * invN);
+  }
+  if (k2r == 0 && !h) { y[0] = make_float2(0.0f, 0.0f); y[1] = make_float2(0.0f, 0.0f); }  // DC, Nyquist
+  // ---- inverse stage 1 (pairs): over k1 for fixed k2; slot j: Z[k2, n1], n1 = 2 sig32(j) + h
+  dft64_pair_dif<true>(y, v, h);
+  {  // W8192^-(k2 n1), n1 = 2 sig32(j) + h = a + 8 b
+    float2 wa[4], wb[8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { wa[c] = g_tw32[((k2r * (2 * c + hi)) & 8191) << SH]; wa[c].y = -wa[c].y; }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) { wb[b] = g_tw32[((8 * k2r * b) & 8191) << SH]; wb[b].y = -wb[b].y; }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int e2 = 2 * sig32(j);
+      v[j] = cmul(v[j], cmul(wa[(e2 & 7) >> 1], wb[e2 >> 3]));
+    }
+  }
+  __syncthreads();  // every thread has read its stage-2 column
+#pragma unroll
+  for (int j = 0; j < 32; ++j) S[(2 * sig32(j) + hi) * LP2 + k2r] = v[j];
+  __syncthreads();
+  // ---- inverse stage 2 (quads): thread (n1, q0, q1) takes k2 in the quad layout
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k2 = 16 * q1i + 8 * q0i + i + 32 * (c & 1) + 64 * (c >> 1);
+      y[4 * i + 2 * (c & 1) + (c >> 1)] = S[n1 * LP2 + k2];
+    }
+  dft128_quad_dif<true>(y, v, q0, q1);  // slot j: x[n1 + 64 (q0 + 2 q1 + 4 sig32(j))]
+  cplx<float>* dst_a = out + ra * (int64_t)N;
+  cplx<float>* dst_b = dst_a + N;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int n = n1 + 64 * (mq + 4 * sig32(j));
+    float2 a; a.x = (float)load_as_double(src_a + n) * scale; a.y = v[j].x;
+    dst_a[n] = a;
+    if (has_b) { float2 b; b.x = (float)load_as_double(src_b + n) * scale; b.y = v[j].y; dst_b[n] = b; }
+  }
+  if (support) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < (has_b ? 2 : 1); ++c) {
+        const bool any = last_nz[c] >= 0;
+        support[2 * (ra + c)] = any ? first_nz[c] : -1;
+        support[2 * (ra + c) + 1] = any ? last_nz[c] : -1;
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------------- Bluestein path
 //
 // DFT_N(x)_k = conj(b_k) * sum_n (x_n conj(b_n)) b_{k-n},  b_j = exp(i pi j^2 / N)
@@ -800,10 +1032,20 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
                            ((N * sizeof(In)) % 16 == 0);
       static const int k1_mode = [] {
         // 0 = fused (one CTA per pair), 1 = persistent TMA-staged, 2 (default) = 1 except
-        // N = 4096, which runs as a 64 x 64 four-step in registers (analytic_r32_kernel)
+        // N = 4096 / 8192, which run as 64 x 64 / 64 x 128 four-steps in registers
+        // (analytic_r32_kernel / analytic_r8192_kernel)
         const char* e = getenv("TIDAS_K1_MODE");
         return e ? atoi(e) : 2;
       }();
+      if (!delay && logN == 13 && k1_mode == 2) {
+        auto kr = analytic_r8192_kernel<In>;
+        const size_t smem8 = sizeof(float2) * 128 * 65;
+        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8));
+        kr<<<(unsigned)((n_rows + 1) / 2), 256, smem8, st>>>(rf, stride, (float)scale,
+                                                            reinterpret_cast<cplx<float>*>(out), n_rows, support);
+        TIDAS_LAUNCH_CHECK();
+        return TIDAS_OK;
+      }
       if (!delay && logN == 12 && k1_mode == 2) {
         analytic_r32_kernel<In><<<(unsigned)((n_rows + 1) / 2), 128, 0, st>>>(
             rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support);
