@@ -552,20 +552,20 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // A fixed frame-batch width per precision (not chosen from F) keeps every
 // frame's arithmetic independent of how many frames share the launch, so
 // images are bit-identical under any batching or sharding (all float variants
-// below use FB = 8 except 28/31, which exist for timing only).
+// below use FB = 8 except 73, which exists for timing only).
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
 //   0: FB 8, 2-channel TMA tensor boxes, 2 buffers, 3 CTAs/SM (27 warps: the
-//      kernel is latency-bound once the bank conflicts are gone; 5.70 us/frame;
-//      multi-transmit / complex-output plans use 57 instead, see dispatch_fb),
+//      kernel is latency-bound once the bank conflicts are gone), single-transmit
+//      loop compiled without live frame accumulators (5.32 us/frame; 56 = the same
+//      without that specialisation, 5.70 us); multi-transmit / complex-output
+//      plans use 57 instead, see the default branch below,
 //      FFMA2 accumulation, gathers as ld.shared on 32-bit window offsets, warps
 //      of 4 depths x 8 columns (a half-warp spans ~2 depths = ~8 + lateral
 //      samples: 1.0M instead of 16.1M bank conflicts per 64 frames with 8 x 4)
 //   73: FB 6, 3 buffers, 3 CTAs/SM   57: FB 8, 3 buffers, 2 CTAs/SM (5.99 us)
+//   (round-1 FB 4 / 16-warp / 1-channel-box variants were slower and are removed)
 //   58: 57 with 8 x 4 warps (6.12 us)   62: 2 x 16 warps (CTA 16 x 16)
 //   59: 58 with generic-pointer gathers   34: 59 with scalar FFMA (round-1 default)
-//   28: FB 4, 3 buffers, 4 CTAs/SM   31: FB 4, 4 buffers, 3 CTAs/SM
-//   35: FB 4, 4 buffers, 16 consumer warps   41: FB 8, 3 buffers, 16 consumer warps, 1-channel boxes
-//   27: FB 4, per-frame bulk copies, 4 CTAs/SM (no tensor map)
 static int das_variant() {
   static int v = [] {
     const char* e = getenv("TIDAS_DAS_VARIANT");
@@ -581,11 +581,6 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
   } else {
     switch (das_variant()) {
       case 34: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, false>(p, A, out, st);
-      case 27: return launch_das<R, AP, OUT, 4, 4, 4>(p, A, out, st);
-      case 28: return launch_das<R, AP, OUT, 4, 3, 4, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
-      case 31: return launch_das<R, AP, OUT, 4, 4, 3, false, 4, 254, 0, 8, true, 2>(p, A, out, st);
-      case 35: return launch_das<R, AP, OUT, 4, 4, 2, false, 4, 254, 0, 16, true, 2>(p, A, out, st);
-      case 41: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 16, true, 1>(p, A, out, st);
       case 56: return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 57: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 58: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, true, 8>(p, A, out, st);
@@ -597,8 +592,9 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
         // channels][256 samples]; single-transmit envelope images (cfg1 / 2 / 5) with 2
         // buffers and 3 CTAs/SM, multi-transmit or complex accumulation (cfg3: 11 angles,
         // coherent — a pipeline refill per transmit) with 3 buffers and 2 CTAs/SM
-        // (3663 against 3367 frames/s before the folded complex accumulation; equal after). The choice depends on the plan only,
-        // never on the frame count, so images stay bitwise batching-invariant.
+        // (3663 against 3367 frames/s before the folded complex accumulation; equal
+        // after). The choice depends on the plan only, never on the frame count, so
+        // images stay bitwise batching-invariant.
         if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1)
           return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true>(p, A, out, st);
         return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
