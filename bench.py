@@ -205,6 +205,7 @@ def main():
     ap.add_argument("--frames", type=int, default=64, help="cfg2 frames per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tidas", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg1 / cfg3 / cfg5 DAS lines")
     ap.add_argument("--cpu-pixels", type=int, default=0, help="cpu_baseline pixel sample (0 = auto)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -474,6 +475,20 @@ def main():
                                      "seconds_per_cell": ct / len(d12) ** 2,
                                      "extrapolated_600x600_minutes": ct / len(d12) ** 2 * 360000 / 60}
 
+    # ---- the other BASELINE.json DAS configs (1 GPU, RF resident; parity-tested
+    # in tests/test_gpu_das.py): cfg1 f64 PSF, cfg3 11-angle coherent, cfg5 int16
+    others = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        sys.path.insert(0, str(ROOT / "tools"))
+        import bench_configs
+        others = {k: {"frames_per_s": v["frames_per_s"], "ms_per_step": v["ms_per_step"],
+                      "frames_per_step": v["frames_per_step"], "hbm_frac": v["hbm_frac"],
+                      "bytes_per_frame": v["bytes_per_frame"], "rf_dtype": v["rf_dtype"],
+                      "transmits": v["transmits"], "grid": v["grid"], "out": v["out"]}
+                  for k, v in bench_configs.run_configs(["cfg1", "cfg3", "cfg5"]).items()}
+        others["note"] = ("das_image (K1 + K2) with the RF resident in HBM, CUDA events over 10 steps; "
+                          "cfg5 timed on 64 of its 1024 frames per step")
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
@@ -499,7 +514,7 @@ def main():
             "roofline": roofline, "k2_smem_roofline": k2_smem, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "gpu_launches_e2e": launches_e2e,
-            "clocks": clocks, "tidas": tidas, "theta_error_sweep": sweep,
+            "clocks": clocks, "tidas": tidas, "theta_error_sweep": sweep, "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -57,14 +57,10 @@ def make_rf(name, c):
     return rf
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--configs", default="cfg1,cfg3,cfg5")
-    args = ap.parse_args()
+def run_configs(names, steps=10, warmup=3, echo=False):
+    """Frames/s of das_image (K1 + K2, RF resident) per config; returns {name: record}."""
     res = {}
-    for name in args.configs.split(","):
+    for name in names:
         c = CFGS[name]
         rf = make_rf(name, c)
         x, z = np.linspace(*c["x"], c["nx"]), np.linspace(*c["z"], c["nz"])
@@ -72,16 +68,16 @@ def main():
                                   x=x, z=z, angles=c["angles"], f_number=1.5, out=c["out"])
         ws = imaging.DasWorkspace(plan)
         img = torch.empty((rf.shape[0], c["nz"], c["nx"]), device="cuda")
-        for _ in range(args.warmup):
+        for _ in range(warmup):
             tb.das_image(rf, plan, out=img, workspace=ws)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             tb.das_image(rf, plan, out=img, workspace=ws)
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.steps
+        ms = e0.elapsed_time(e1) / steps
         fps = rf.shape[0] / (ms / 1e3)
         gbs = c["bytes"] * fps / 1e9
         res[name] = {"frames_per_step": int(rf.shape[0]), "ms_per_step": ms, "frames_per_s": fps,
@@ -89,10 +85,20 @@ def main():
                      "rf_dtype": str(c["dtype"]).replace("torch.", ""), "transmits": len(c["angles"]),
                      "grid": [c["nz"], c["nx"]], "out": c["out"], "chunk_frames": ws.chunk,
                      "checksum": float(img.double().sum())}
-        print(json.dumps({name: res[name]}), flush=True)
+        if echo:
+            print(json.dumps({name: res[name]}), flush=True)
         del rf, img, ws
         torch.cuda.empty_cache()
-    print(json.dumps(res))
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--configs", default="cfg1,cfg3,cfg5")
+    args = ap.parse_args()
+    print(json.dumps(run_configs(args.configs.split(","), args.steps, args.warmup, echo=True)))
 
 
 if __name__ == "__main__":
