@@ -199,7 +199,7 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
           int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
-          bool U32 = false, int WZ = 8, bool ONE_TX = false>
+          bool U32 = false, int WZ = 8, bool ONE_TX = false, bool LPT = false>
 __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams p,
                                                                    const cplx<R>* __restrict__ A,
                                                                    void* __restrict__ out_,
@@ -218,9 +218,21 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
   // 4 x 8); the CTA is DG depth groups x (NW / DG) column groups of warps
   constexpr int CG = NW / DG;
   constexpr int WX = 32 / WZ;
-  const int iz = blockIdx.x * (WZ * DG) + (wid / CG) * WZ + lane / WX;
-  const int ix = blockIdx.y * (WX * CG) + (wid % CG) * WX + lane % WX;
-  const int f0 = blockIdx.z * FB;
+  // LPT: a 1-D grid ordered deepest depth tile first — deep tiles have the widest
+  // apertures (most channels), so the longest CTAs are dispatched first and the
+  // last wave holds the shortest ones (less tail idle)
+  int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  if constexpr (LPT) {
+    const int nzt = (p.nz + WZ * DG - 1) / (WZ * DG), nct = (p.nx + WX * CG - 1) / (WX * CG);
+    const int nfb = (p.F + FB - 1) / FB;
+    const int t = (int)blockIdx.x, per_dt = nct * nfb;
+    bx = (nzt - 1) - t / per_dt;
+    by = (t % per_dt) % nct;
+    bz = (t % per_dt) / nct;
+  }
+  const int iz = bx * (WZ * DG) + (wid / CG) * WZ + lane / WX;
+  const int ix = by * (WX * CG) + (wid % CG) * WX + lane % WX;
+  const int f0 = bz * FB;
   const bool pix = !producer && (iz < p.nz) && (ix < p.nx);
   const int half = p.E / 2;
 
@@ -514,10 +526,10 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
 
 template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
           int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
-          bool U32 = false, int WZ = 8, bool ONE_TX = false>
+          bool U32 = false, int WZ = 8, bool ONE_TX = false, bool LPT = false>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2, U32, WZ, ONE_TX>;
+  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2, U32, WZ, ONE_TX, LPT>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (TMAP) {
@@ -544,6 +556,11 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
   constexpr int TZ = WZ * DG, TXC = (32 / WZ) * (NW / DG);
   dim3 grid((p.nz + TZ - 1) / TZ, (p.nx + TXC - 1) / TXC, (p.F + FB - 1) / FB);
   TIDAS_REQUIRE(grid.y <= 65535 && grid.z <= 65535, "pixel grid / frame batch too large");
+  if (LPT) {
+    const long long total = (long long)grid.x * grid.y * grid.z;
+    TIDAS_REQUIRE(total < (1LL << 31), "pixel grid / frame batch too large");
+    grid = dim3((unsigned)total, 1, 1);
+  }
   kern<<<grid, block, smem, st>>>(p, reinterpret_cast<const C*>(A), out, tmap);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
@@ -556,9 +573,11 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
 //   0: FB 8, 2-channel TMA tensor boxes, 2 buffers, 3 CTAs/SM (27 warps: the
 //      kernel is latency-bound once the bank conflicts are gone), single-transmit
-//      loop compiled without live frame accumulators (5.32 us/frame; 56 = the same
-//      without that specialisation, 5.70 us); multi-transmit / complex-output
-//      plans use 57 instead, see the default branch below,
+//      loop compiled without live frame accumulators, CTAs dispatched deepest
+//      depth tile first (longest first: a short last wave; 5.13 us/frame; 55 = the
+//      same in the natural grid order, 5.31 us; 56 = 55 without the single-transmit
+//      specialisation, 5.70 us); multi-transmit / complex-output plans use 57 in
+//      the deepest-first order instead (cfg3 4338 against 3975 frames/s),
 //      FFMA2 accumulation, gathers as ld.shared on 32-bit window offsets, warps
 //      of 4 depths x 8 columns (a half-warp spans ~2 depths = ~8 + lateral
 //      samples: 1.0M instead of 16.1M bank conflicts per 64 frames with 8 x 4)
@@ -581,6 +600,7 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
   } else {
     switch (das_variant()) {
       case 34: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, false>(p, A, out, st);
+      case 55: return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true>(p, A, out, st);
       case 56: return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 57: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
       case 58: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, true, 8>(p, A, out, st);
@@ -596,8 +616,8 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
         // after). The choice depends on the plan only, never on the frame count, so
         // images stay bitwise batching-invariant.
         if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1)
-          return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true>(p, A, out, st);
-        return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
+          return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true, true>(p, A, out, st);
+        return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4, false, true>(p, A, out, st);
     }
   }
 }
