@@ -21,7 +21,7 @@ for _ in range(10): tb.das_from_analytic(an, plan, out=img)
 e1.record(); torch.cuda.synchronize()
 print("us/frame", e0.elapsed_time(e1) * 1e3 / 10 / F, "checksum", float(img.double().sum()))
 '''
-for v in sys.argv[1:] or ["0", "1", "2", "3"]:
+for v in sys.argv[1:] or ["0", "55", "57", "58", "34"]:
     env = dict(os.environ, TIDAS_DAS_VARIANT=v)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print("variant", v, (out.stdout.strip() or out.stderr.strip()[-400:]))
