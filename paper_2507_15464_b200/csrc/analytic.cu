@@ -857,6 +857,137 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   }
 }
 
+// ------------------------ N = 2048, 64 threads: 32 values per thread
+//
+// Four-step 2048 = 32 x 64: n = n1 + 32 m, k = k2 + 64 k1,
+//   Y[n1, k2] = DFT64_m(x[n1 + 32 m]) W2048^(n1 k2);  X[k2 + 64 k1] = DFT32_n1(Y[n1, k2]).
+// The 64-point DFTs run over lane pairs (as in analytic_r32_kernel), the
+// 32-point DFTs in one thread's registers (the forward's output slots feed the
+// inverse DFT-32 by register renaming, no data movement). Pair roles: column
+// n1 = 16 warp + (lane & 15), h = lane >> 4; row roles: k2 = threadIdx.x.
+template <typename In>
+__global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict__ rf, int64_t stride, float scale,
+                                                            cplx<float>* __restrict__ out, int64_t n_rows,
+                                                            int32_t* __restrict__ support) {
+  constexpr int N = 2048, LP1 = 33, LP2 = 65;  // [64][33] and [32][65] transposes
+  constexpr int SH = TW_LOG - 11;
+  __shared__ float2 S[64 * LP1 > 32 * LP2 ? 64 * LP1 : 32 * LP2];
+  __shared__ int first_nz[2], last_nz[2];
+  const int lane = threadIdx.x & 31;
+  const int n1 = (threadIdx.x >> 5) * 16 + (lane & 15);  // pair roles
+  const int hi = lane >> 4;
+  const bool h = hi != 0;
+  const int k2r = threadIdx.x;                           // row roles
+  const int64_t ra = 2 * (int64_t)blockIdx.x;
+  const bool has_b = ra + 1 < n_rows;
+  const In* src_a = rf + ra * stride;
+  const In* src_b = rf + (ra + 1) * stride;
+  if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  float2 v[32], w[32];
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    const int n = n1 + 32 * (hi + 2 * p);
+    v[p].x = (float)load_as_double(src_a + n);
+    v[p].y = has_b ? (float)load_as_double(src_b + n) : 0.0f;
+  }
+  int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    v[p].x *= scale;
+    v[p].y *= scale;
+    const int n = n1 + 32 * (hi + 2 * p);
+    if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+    if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+  }
+  __syncthreads();
+  if (support) {
+    if (lo_a < N) atomicMin(&first_nz[0], lo_a);
+    if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
+    if (lo_b < N) atomicMin(&first_nz[1], lo_b);
+    if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
+  }
+  // forward stage 1 (pairs): w[2 i + u] = Y[n1, k2], k2 = 16 h + i + 32 u
+  dft64_pair_dit<false>(v, w, h);
+  {  // W2048^(n1 k2), k2 = a + 8 b: a = i & 7, b = 2 h + (i >> 3) + 4 u
+    float2 wa[8], wb[4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) wa[a] = g_tw32[((n1 * a) & 2047) << SH];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) wb[c] = g_tw32[((8 * n1 * (2 * hi + (c & 1) + 4 * (c >> 1))) & 2047) << SH];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int a = i & 7, c = (i >> 3) + 2 * u;
+        w[2 * i + u] = cmul(w[2 * i + u], a == 0 ? wb[c] : cmul(wa[a], wb[c]));
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    S[(16 * hi + i) * LP1 + n1] = w[2 * i];
+    S[(16 * hi + i + 32) * LP1 + n1] = w[2 * i + 1];
+  }
+  __syncthreads();
+  // forward stage 2 (rows): DFT-32 over n1 in registers; slot j: X[k2 + 64 sig32(j)]
+#pragma unroll
+  for (int q = 0; q < 32; ++q) v[q] = S[k2r * LP1 + q];
+  dft32<false>(v);
+  // Hilbert multiplier -i sgn(k) / N, k = k2 + 64 k1: k1 < 16 positive, >= 16 negative;
+  // the inverse DFT-32 takes natural k1 order: slot k1 of u = slot sig32_inv(k1) of v
+  const float invN = 1.0f / (float)N;
+#pragma unroll
+  for (int k1 = 0; k1 < 32; ++k1) {
+    const float2 p0 = v[sig32_inv(k1)];
+    float2 r = (k1 < 16) ? make_float2(p0.y * invN, -p0.x * invN) : make_float2(-p0.y * invN, p0.x * invN);
+    if (k2r == 0 && (k1 == 0 || k1 == 16)) r = make_float2(0.0f, 0.0f);  // DC, Nyquist
+    w[k1] = r;
+  }
+  // inverse stage 1 (rows): slot j: Z[k2, n1 = sig32(j)]
+  dft32<true>(w);
+  {  // W2048^-(k2 n1), n1 = a + 8 b
+    float2 wa[8], wb[4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) { wa[a] = g_tw32[((k2r * a) & 2047) << SH]; wa[a].y = -wa[a].y; }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) { wb[b] = g_tw32[((8 * k2r * b) & 2047) << SH]; wb[b].y = -wb[b].y; }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int e = sig32(j), a = e & 7, b = e >> 3;
+      w[j] = cmul(w[j], a == 0 ? wb[b] : cmul(wa[a], wb[b]));
+    }
+  }
+  __syncthreads();  // every thread has read its stage-2 row
+#pragma unroll
+  for (int j = 0; j < 32; ++j) S[sig32(j) * LP2 + k2r] = w[j];
+  __syncthreads();
+  // inverse stage 2 (pairs): w[2 i + u] = Z[k2 = 16 h + i + 32 u, n1]
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    w[2 * i] = S[n1 * LP2 + 16 * hi + i];
+    w[2 * i + 1] = S[n1 * LP2 + 16 * hi + i + 32];
+  }
+  dft64_pair_dif<true>(w, v, h);  // slot j: x[n1 + 32 (2 sig32(j) + h)]
+  cplx<float>* dst_a = out + ra * (int64_t)N;
+  cplx<float>* dst_b = dst_a + N;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int n = n1 + 32 * (2 * sig32(j) + hi);
+    float2 a; a.x = (float)load_as_double(src_a + n) * scale; a.y = v[j].x;
+    dst_a[n] = a;
+    if (has_b) { float2 b; b.x = (float)load_as_double(src_b + n) * scale; b.y = v[j].y; dst_b[n] = b; }
+  }
+  if (support) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < (has_b ? 2 : 1); ++c) {
+        const bool any = last_nz[c] >= 0;
+        support[2 * (ra + c)] = any ? first_nz[c] : -1;
+        support[2 * (ra + c) + 1] = any ? last_nz[c] : -1;
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------------- Bluestein path
 //
 // DFT_N(x)_k = conj(b_k) * sum_n (x_n conj(b_n)) b_{k-n},  b_j = exp(i pi j^2 / N)
@@ -1031,12 +1162,18 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
       const bool aligned = (reinterpret_cast<uintptr_t>(rf) % 16 == 0) && ((stride * sizeof(In)) % 16 == 0) &&
                            ((N * sizeof(In)) % 16 == 0);
       static const int k1_mode = [] {
-        // 0 = fused (one CTA per pair), 1 = persistent TMA-staged, 2 (default) = 1 except
-        // N = 4096 / 8192, which run as 64 x 64 / 64 x 128 four-steps in registers
-        // (analytic_r32_kernel / analytic_r8192_kernel)
+        // 0 = fused (one CTA per pair), 1 = persistent TMA-staged, 2 (default): N = 2048 /
+        // 4096 / 8192 run as 32 x 64 / 64 x 64 / 64 x 128 four-steps in registers
+        // (analytic_r2048_kernel / analytic_r32_kernel / analytic_r8192_kernel)
         const char* e = getenv("TIDAS_K1_MODE");
         return e ? atoi(e) : 2;
       }();
+      if (!delay && logN == 11 && k1_mode == 2) {
+        analytic_r2048_kernel<In><<<(unsigned)((n_rows + 1) / 2), 64, 0, st>>>(
+            rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support);
+        TIDAS_LAUNCH_CHECK();
+        return TIDAS_OK;
+      }
       if (!delay && logN == 13 && k1_mode == 2) {
         auto kr = analytic_r8192_kernel<In>;
         const size_t smem8 = sizeof(float2) * 128 * 65;

@@ -12,8 +12,9 @@ sx, sz, a = frame_scatterers(cfg, range(F))
 rf = tb.synthesize_batch(sx, sz, a, angles=[0.0], n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"], f0=cfg["f0"], fbw=cfg["fbw"], n_samples=cfg["n_samples"])
 g = torch.Generator(device="cuda"); g.manual_seed(5)
 rf5 = (torch.randn((16, 1, 192, 8192), device="cuda", generator=g) * 1000).round().clamp(-32768, 32767).to(torch.int16)
+rf1 = torch.randn((256, 1, 64, 2048), device="cuda", generator=g, dtype=torch.float64)
 res = {}
-for name, x in (("cfg2_f32", rf), ("cfg5_i16", rf5)):
+for name, x in (("cfg2_f32", rf), ("cfg5_i16", rf5), ("cfg1_f64", rf1)):
     an = torch.empty(x.shape, dtype=torch.complex64, device="cuda")
     for _ in range(3): tb.rf_analytic(x, "f32", out=an)
     torch.cuda.synchronize()
