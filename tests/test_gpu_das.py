@@ -94,6 +94,21 @@ def test_analytic_strided_rows_through_the_abi(n, pad, offset, rng):
     assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 2e-6
 
 
+@pytest.mark.parametrize("n", [2048, 4096, 8192])
+@pytest.mark.parametrize("rows", [1, 2, 3])
+def test_analytic_register_fft_scale_and_row_counts(n, rows, rng):
+    """The register four-step kernels (N = 2048 / 4096 / 8192) with one, two and
+    three rows (a lone last channel) and a non-unit ingest scale on int16."""
+    x = (rng.standard_normal((rows, n)) * 1000).astype(np.int16)
+    scale = 1e-3
+    ref = od.analytic_signal(x.astype(np.float64) * scale)
+    sup = torch.empty((rows, 2), dtype=torch.int32, device=DEV)
+    got = tb.rf_analytic(torch.as_tensor(x).to(DEV), "f32", scale=scale, support=sup).cpu().numpy()
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 2e-6
+    nz = [np.flatnonzero(x[r]) for r in range(rows)]
+    assert sup.cpu().tolist() == [[int(z[0]), int(z[-1])] for z in nz]
+
+
 def test_analytic_rejects_short_rows():
     with pytest.raises(ValueError):
         tb.rf_analytic(torch.zeros((2, 3), dtype=torch.float64, device=DEV))
