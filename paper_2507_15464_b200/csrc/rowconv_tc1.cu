@@ -58,7 +58,7 @@ template <bool ADJ>
 __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                   const __grid_constant__ CUtensorMap omap,
                                                                   const float* __restrict__ K, int batch, int nz,
-                                                                  int nx, int T, int rows_per, int diag) {
+                                                                  int nx, int T, int units_per, int diag) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sbase = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   unsigned char* B_st = sbase;                        // [2 rows][40 KB]
@@ -104,8 +104,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
   const unsigned tmem = tmem_base_s;
   if (tmem != 0) __trap();  // a full 512-column allocation always starts at column 0
 
-  const int row0 = (int)blockIdx.x * rows_per;
-  const int rows_mine = max(0, min(rows_per, nz - row0));
+  // work units are (row, 128-map block) pairs in row-major order; a CTA owns a
+  // contiguous range of them, so a row's map blocks may be split between two
+  // CTAs (both build that row's Toeplitz block) and every SM gets work even
+  // when nz is not a multiple of the SM count
+  const long long u0 = (long long)blockIdx.x * units_per;
+  const long long u1 = min((long long)nz * n_mb, u0 + units_per);
+  const int row0 = (int)(u0 / n_mb);
+  const int rows_mine = u1 > u0 ? (int)((u1 - 1) / n_mb) - row0 + 1 : 0;
+  const int mb_first = (int)(u0 % n_mb);
+  const int mb_end_last = u1 > u0 ? (int)((u1 - 1) % n_mb) + 1 : 0;
+  auto mb_lo = [&](int r) { return r == 0 ? mb_first : 0; };
+  auto mb_hi = [&](int r) { return r == rows_mine - 1 ? mb_end_last : n_mb; };
 
   if (warp < 4 || warp >= CONV_SET1) {
     // ===== converters: two sets of 4 warps take even / odd chunks
@@ -136,7 +146,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
       }
-      for (int mb = 0; mb < n_mb; ++mb, gs0 += NSG) {
+      for (int mb = mb_lo(r); mb < mb_hi(r); ++mb, gs0 += NSG) {
         for (int q = 0; q < NQ; ++q, ++gc) {
           if ((int)(gc & 1) != set) continue;
           const int slot = (int)(gc % RING);
@@ -184,7 +194,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
     long long b = 0;
     for (int r = 0; r < rows_mine; ++r) {
       const int row = row0 + r;
-      for (int mb = 0; mb < n_mb; ++mb) {
+      for (int mb = mb_lo(r); mb < mb_hi(r); ++mb) {
         for (int j = 0; j < n_xb; ++j, ++b) {
           const int dbuf = (int)(b & 1);
           bar_wait(&mma_done[dbuf], (unsigned)((b >> 1) & 1));
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
       long long gp = 0;
       for (int r = 0; r < rows_mine; ++r) {
         const int row = row0 + r;
-        for (int mb = 0; mb < n_mb; ++mb) {
+        for (int mb = mb_lo(r); mb < mb_hi(r); ++mb) {
           for (int u = 0; u < NSG; ++u, ++gp) {
             const int st = (int)(gp % NSTAGE);
             if (gp >= NSTAGE) bar_wait(&a_empty[st], (unsigned)(((gp / NSTAGE) - 1) & 1));
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
     for (int r = 0; r < rows_mine; ++r) {
       const uint64_t db = smem_desc_sw128(su32(B_st + (r & 1) * B_BYTES));
       const unsigned b_lo32 = (unsigned)db, b_hi32 = (unsigned)(db >> 32);
-      for (int mb = 0; mb < n_mb; ++mb, g0 += NQ) {
+      for (int mb = mb_lo(r); mb < mb_hi(r); ++mb, g0 += NQ) {
         for (int j = 0; j < n_xb; ++j, ++b) {
           for (int c = (j == 0 ? 0 : CHB - 1); c < CHB; ++c) {
             const long long g = g0 + j + c;
@@ -321,10 +331,11 @@ int launch_rowconv_tc1(const float* in, const float* K, float* out, int64_t batc
   const size_t smem = 2 * B_BYTES + NSTAGE * A_STAGE + 4 * O_SLAB + 1024;
   auto kern = rowconv_tc1_kernel<ADJ>;
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int rows_per = (nz + sms - 1) / sms;
-  const int grid = (nz + rows_per - 1) / rows_per;
+  const long long units = (long long)nz * ((batch + MAPS - 1) / MAPS);
+  const int units_per = (int)((units + sms - 1) / sms);
+  const int grid = (int)((units + units_per - 1) / units_per);
   static const int diag = getenv("TIDAS_ROWCONV_DIAG") ? atoi(getenv("TIDAS_ROWCONV_DIAG")) : 0;
-  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, (int)batch, nz, nx, T, rows_per, diag);
+  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, (int)batch, nz, nx, T, units_per, diag);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
 }
