@@ -3,8 +3,8 @@
 ``DasPlan`` holds the frame-invariant geometry on the device (pixel grid,
 per-transmit arrival table t*, aperture), ``das_image`` runs K1 (RF ingest +
 analytic signal) and K2 (fused DAS) over a batch of frames, in chunks of up to
-256 MB of complex analytic RF (64 cfg2 frames) so each K2 launch spans many
-waves of CTAs.
+1 GB of complex analytic RF (256 cfg2 frames) so each launch spans many waves
+of CTAs and the last-wave tails stay short.
 
 Semantics: the pixel value is the reference's das_value
 (das.py:181-193) — envelope of the dynamic-focus delayed sum at t*, two-tap
@@ -50,7 +50,7 @@ class DasPlan:
     prec: str = "f32"
     t0: float = 0.0
     ap_half: Optional[torch.Tensor] = None
-    chunk_bytes: int = 256 << 20
+    chunk_bytes: int = 1 << 30
     _desc: Optional[_lib.DasDesc] = field(default=None, repr=False)
 
     @property
