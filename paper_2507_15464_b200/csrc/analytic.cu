@@ -519,6 +519,7 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   const In* src_a = rf + ra * stride;
   const In* src_b = rf + (ra + 1) * stride;
   if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   float2 v[32], w[32];
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
@@ -603,6 +604,9 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
     w[2 * i + 1] = S[t * LP + 16 * hi + i + 32];
   }
   dft64_pair_dif<true>(w, v, h);  // slot j: x[t + 64 (2 sig32(j) + h)]
+  // programmatic dependent launch: the output rows may still be read by the
+  // previous kernel in the stream (the last chunk's DAS) — wait before storing
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   // real parts = the inputs, re-read (L2)
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
@@ -1184,8 +1188,17 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         return TIDAS_OK;
       }
       if (!delay && logN == 12 && k1_mode == 2) {
-        analytic_r32_kernel<In><<<(unsigned)((n_rows + 1) / 2), 128, 0, st>>>(
-            rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)((n_rows + 1) / 2));
+        cfg.blockDim = dim3(128);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        TIDAS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, analytic_r32_kernel<In>, rf, stride, (float)scale,
+                                            reinterpret_cast<cplx<float>*>(out), n_rows, support));
         TIDAS_LAUNCH_CHECK();
         return TIDAS_OK;
       }

@@ -296,6 +296,12 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
   // ONE_TX: a single transmit known at compile time, so the frame accumulators
   // are not live across the channel loop (fewer registers at 3 CTAs/SM)
   const int n_tx = ONE_TX ? 1 : p.A;
+  // programmatic dependent launch: everything above (geometry, channel ranges,
+  // barrier setup) overlaps the tail of the kernel that wrote the analytic RF;
+  // its reads start only after that kernel has completed. Let the next kernel
+  // in the stream start its own prologue during this kernel's last wave.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   for (int a = 0; a < n_tx; ++a) {
     // arrival split into integer index + fraction in float64
     int k0 = 0;
@@ -561,7 +567,17 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
     TIDAS_REQUIRE(total < (1LL << 31), "pixel grid / frame batch too large");
     grid = dim3((unsigned)total, 1, 1);
   }
-  kern<<<grid, block, smem, st>>>(p, reinterpret_cast<const C*>(A), out, tmap);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TIDAS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, p, reinterpret_cast<const C*>(A), out, tmap));
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
 }
