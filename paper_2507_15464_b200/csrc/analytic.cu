@@ -752,6 +752,7 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   const In* src_a = rf + ra * stride;
   const In* src_b = rf + (ra + 1) * stride;
   if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   float2 v[32], y[32];
   const int mq = q0i + 2 * q1i;
 #pragma unroll
@@ -840,6 +841,7 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
       y[4 * i + 2 * (c & 1) + (c >> 1)] = S[n1 * LP2 + k2];
     }
   dft128_quad_dif<true>(y, v, q0, q1);  // slot j: x[n1 + 64 (q0 + 2 q1 + 4 sig32(j))]
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the previous kernel may still read the output
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
 #pragma unroll
@@ -887,6 +889,7 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   const In* src_a = rf + ra * stride;
   const In* src_b = rf + (ra + 1) * stride;
   if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   float2 v[32], w[32];
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
@@ -971,6 +974,7 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
     w[2 * i + 1] = S[n1 * LP2 + 16 * hi + i + 32];
   }
   dft64_pair_dif<true>(w, v, h);  // slot j: x[n1 + 32 (2 sig32(j) + h)]
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the previous kernel may still read the output
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
 #pragma unroll
@@ -1143,6 +1147,24 @@ static int get_chirp_spectra(int device, int N, int logM, const cplx<R>** out) {
   return TIDAS_OK;
 }
 
+// launch with programmatic dependent launch enabled (the kernel calls
+// griddepcontrol.wait before its first global store)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <typename R, typename In>
 static int launch_analytic(const In* rf, int64_t stride, double scale, void* out, int64_t n_rows,
                            int32_t N, int32_t* support, double shift, cudaStream_t st) {
@@ -1173,18 +1195,16 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         return e ? atoi(e) : 2;
       }();
       if (!delay && logN == 11 && k1_mode == 2) {
-        analytic_r2048_kernel<In><<<(unsigned)((n_rows + 1) / 2), 64, 0, st>>>(
-            rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support);
-        TIDAS_LAUNCH_CHECK();
+        TIDAS_CUDA_CHECK(launch_pdl(analytic_r2048_kernel<In>, dim3((unsigned)((n_rows + 1) / 2)), dim3(64), 0, st,
+                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
         return TIDAS_OK;
       }
       if (!delay && logN == 13 && k1_mode == 2) {
         auto kr = analytic_r8192_kernel<In>;
         const size_t smem8 = sizeof(float2) * 128 * 65;
         TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8));
-        kr<<<(unsigned)((n_rows + 1) / 2), 256, smem8, st>>>(rf, stride, (float)scale,
-                                                            reinterpret_cast<cplx<float>*>(out), n_rows, support);
-        TIDAS_LAUNCH_CHECK();
+        TIDAS_CUDA_CHECK(launch_pdl(kr, dim3((unsigned)((n_rows + 1) / 2)), dim3(256), smem8, st, rf, stride,
+                                    (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
         return TIDAS_OK;
       }
       if (!delay && logN == 12 && k1_mode == 2) {
