@@ -519,7 +519,12 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   const In* src_a = rf + ra * stride;
   const In* src_b = rf + (ra + 1) * stride;
   if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  // programmatic dependent launch: let the next kernel (the DAS of this chunk)
+  // start its prologue during this kernel's last wave; wait for the previous
+  // kernel (which may have written the input or still read the output rows)
+  // before touching global data
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   float2 v[32], w[32];
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
@@ -604,9 +609,6 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
     w[2 * i + 1] = S[t * LP + 16 * hi + i + 32];
   }
   dft64_pair_dif<true>(w, v, h);  // slot j: x[t + 64 (2 sig32(j) + h)]
-  // programmatic dependent launch: the output rows may still be read by the
-  // previous kernel in the stream (the last chunk's DAS) — wait before storing
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   // real parts = the inputs, re-read (L2)
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
@@ -752,7 +754,12 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   const In* src_a = rf + ra * stride;
   const In* src_b = rf + (ra + 1) * stride;
   if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  // programmatic dependent launch: let the next kernel (the DAS of this chunk)
+  // start its prologue during this kernel's last wave; wait for the previous
+  // kernel (which may have written the input or still read the output rows)
+  // before touching global data
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   float2 v[32], y[32];
   const int mq = q0i + 2 * q1i;
 #pragma unroll
@@ -841,7 +848,6 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
       y[4 * i + 2 * (c & 1) + (c >> 1)] = S[n1 * LP2 + k2];
     }
   dft128_quad_dif<true>(y, v, q0, q1);  // slot j: x[n1 + 64 (q0 + 2 q1 + 4 sig32(j))]
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the previous kernel may still read the output
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
 #pragma unroll
@@ -889,7 +895,12 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   const In* src_a = rf + ra * stride;
   const In* src_b = rf + (ra + 1) * stride;
   if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  // programmatic dependent launch: let the next kernel (the DAS of this chunk)
+  // start its prologue during this kernel's last wave; wait for the previous
+  // kernel (which may have written the input or still read the output rows)
+  // before touching global data
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   float2 v[32], w[32];
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
@@ -974,7 +985,6 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
     w[2 * i + 1] = S[n1 * LP2 + 16 * hi + i + 32];
   }
   dft64_pair_dif<true>(w, v, h);  // slot j: x[n1 + 32 (2 sig32(j) + h)]
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the previous kernel may still read the output
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
 #pragma unroll
@@ -1148,7 +1158,7 @@ static int get_chirp_spectra(int device, int N, int logM, const cplx<R>** out) {
 }
 
 // launch with programmatic dependent launch enabled (the kernel calls
-// griddepcontrol.wait before its first global store)
+// griddepcontrol.wait before its first global access)
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args... args) {
