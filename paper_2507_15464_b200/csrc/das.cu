@@ -298,8 +298,11 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
   const int n_tx = ONE_TX ? 1 : p.A;
   // programmatic dependent launch: everything above (geometry, channel ranges,
   // barrier setup) overlaps the tail of the kernel that wrote the analytic RF;
-  // its reads start only after that kernel has completed. Let the next kernel
-  // in the stream start its own prologue during this kernel's last wave.
+  // it reads only the plan's pixel coordinates / aperture table, which the plan
+  // constructors copy to the device once (never the output of the kernel just
+  // ahead in the stream). The analytic RF and t* are read only after the wait.
+  // Let the next kernel in the stream start its own prologue during this
+  // kernel's last wave.
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   for (int a = 0; a < n_tx; ++a) {
