@@ -108,6 +108,10 @@ typedef struct {
  *   ap_half  : int32[nz] aperture half count for TIDAS_AP_REF_BOXCAR (else NULL)
  *   out      : [F][nz][nx] real (complex for TIDAS_OUT_IQ) of `prec`
  * Replaces: das_value / das_line (das.py:181-221) — O(channels) per pixel.
+ * Launched with programmatic dependent launch: `analytic` and `t_star` are read
+ * only after the preceding kernel on `stream` completed; `x`, `z` and `ap_half`
+ * (plan constants) may be read during its last wave, so they must not be the
+ * output of the kernel immediately ahead on the same stream.
  */
 int tidas_das_image(const tidas_das_desc_t* desc, const void* analytic,
                     const double* t_star, const double* x, const double* z,
