@@ -628,14 +628,17 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
       case 59: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, false>(p, A, out, st);
       default:
         // measured best on B200: 8 frames per thread, TMA tensor boxes of [8 frames][2
-        // channels][256 samples]; single-transmit envelope images (cfg1 / 2 / 5) with 2
-        // buffers and 3 CTAs/SM, multi-transmit or complex accumulation (cfg3: 11 angles,
-        // coherent — a pipeline refill per transmit) with 3 buffers and 2 CTAs/SM
-        // (3663 against 3367 frames/s before the folded complex accumulation; equal
-        // after). The choice depends on the plan only, never on the frame count, so
-        // images stay bitwise batching-invariant.
+        // channels][256 samples], 2 buffers and 3 CTAs/SM for single-transmit envelope
+        // images (cfg1 / 2 / 5, single-transmit specialisation) and for complex outputs
+        // (cfg3 coherent: folded accumulation, 4512 against 4393 frames/s with 2 CTAs/SM);
+        // multi-transmit envelope compounding keeps c0 / c1 and the frame accumulators
+        // live across transmits and runs with 3 buffers at 2 CTAs/SM. The choice depends
+        // on the plan only, never on the frame count, so images stay bitwise
+        // batching-invariant.
         if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1)
           return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true, true>(p, A, out, st);
+        if (OUT != TIDAS_OUT_ENVELOPE)  // folded complex accumulation: few registers, 3 CTAs/SM
+          return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, false, true>(p, A, out, st);
         return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4, false, true>(p, A, out, st);
     }
   }
