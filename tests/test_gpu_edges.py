@@ -62,3 +62,30 @@ def test_batch_metrics_zero_batch():
     z = torch.zeros((0, 8), dtype=torch.float64, device=DEV)
     assert tb.batch_errors(z, z, axis=1).shape == (0,)
     assert tb.batch_fwhm(z, 1.0).shape == (0,)
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 8192])
+def test_rf_analytic_writes_stay_inside_the_output(n):
+    """Guard bands around the output rows stay untouched (no out-of-bounds stores
+    from the register four-step kernels, odd row count)."""
+    rows, guard = 3, 4096
+    x = torch.randn((rows, n), device=DEV)
+    buf = torch.full((rows * n + 2 * guard,), complex(7.0, -7.0), dtype=torch.complex64, device=DEV)
+    out = buf[guard: guard + rows * n].view(rows, n)
+    tb.rf_analytic(x, "f32", out=out)
+    assert bool((buf[:guard] == complex(7.0, -7.0)).all()) and bool((buf[-guard:] == complex(7.0, -7.0)).all())
+    assert bool(torch.isfinite(out.real).all()) and bool(torch.isfinite(out.imag).all())
+
+
+@pytest.mark.parametrize("frames", [1, 9])
+def test_das_image_writes_stay_inside_the_output(frames):
+    """Guard bands around the image batch stay untouched (ragged grid, partial
+    frame batch, deepest-first 1-D grid)."""
+    nz, nx, guard = 45, 21, 1024
+    plan = _plan(nz, nx)
+    rf = torch.randn((frames, 1, CFG2["n_el"], CFG2["n_samples"]), device=DEV)
+    buf = torch.full((frames * nz * nx + 2 * guard,), -3.0, device=DEV)
+    out = buf[guard: guard + frames * nz * nx].view(frames, nz, nx)
+    tb.das_image(rf, plan, out=out)
+    assert bool((buf[:guard] == -3.0).all()) and bool((buf[-guard:] == -3.0).all())
+    assert bool((out >= 0).all())  # envelopes
