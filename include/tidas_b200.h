@@ -161,6 +161,13 @@ int tidas_rowconv_fwd_f32(const float* g, const float* K, float* y, int64_t batc
                           int32_t nz, int32_t nx, int32_t taps, void* stream);
 int tidas_rowconv_adj_f32(const float* y, const float* K, float* g, int64_t batch,
                           int32_t nz, int32_t nx, int32_t taps, void* stream);
+/* Both directions with an explicit kernel choice (the two entry points above
+ * are TIDAS_ROWCONV_AUTO): tensor cores (tcgen05 3xTF32 Toeplitz GEMM; needs
+ * batch >= 32, nx % 32 == 0, taps <= 129, else TIDAS_EUNSUPPORTED) or CUDA
+ * cores (any shape). `in` and `out` must not overlap. */
+enum tidas_rowconv_path { TIDAS_ROWCONV_AUTO = 0, TIDAS_ROWCONV_TENSOR = 1, TIDAS_ROWCONV_SIMT = 2 };
+int tidas_rowconv_f32(const float* in, const float* K, float* out, int64_t batch, int32_t nz,
+                      int32_t nx, int32_t taps, int32_t adjoint, int32_t path, void* stream);
 
 /*
  * RF synthesis (simulate.py:193-259 model), for seeded inputs:
@@ -177,6 +184,22 @@ int tidas_synthesize(const double* sx, const double* sz, const double* amp, cons
                      double pitch, double c, double fs, double f0, double fbw,
                      int32_t spreading, int32_t n_samples, void* out, int out_dtype,
                      void* stream);
+
+/*
+ * Per-frame standard deviation (numpy np.std semantics: about the frame mean,
+ * two passes in float64) of x [n_frames][frame_len], dtype F32 or F64.
+ * std_out: double[n_frames] (device). Enqueues a stream-ordered scratch alloc.
+ */
+int tidas_frame_std(const void* x, int dtype, int64_t n_frames, int64_t frame_len, double* std_out,
+                    void* stream);
+/*
+ * int16 quantisation (cfg5 ingest format): out = clip(rint(x * target_std / std_f),
+ * -32768, 32767), round-half-even like np.rint; scale 1 for a zero std.
+ * frame_std: double[n_frames] on the device (e.g. from tidas_frame_std).
+ * Extends: synthesize_frame (simulate.py:193-259), which has no integer output.
+ */
+int tidas_quantize_i16(const void* x, int dtype, int64_t n_frames, int64_t frame_len,
+                       const double* frame_std, double target_std, int16_t* out, void* stream);
 
 /* ------------------------------------------------------------------------
  * FFT theta estimator and theta / error sweeps, float64.

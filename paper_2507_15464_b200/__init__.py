@@ -21,7 +21,7 @@ from .tidas import (ThetaMatrix, TimeWindow, build_row_kernels, estimate_theta_a
                     tidas_psf, tidas_rowconv, tidas_rowconv_adjoint, window_signals)
 from .sweep import error_sweep, estimate_theta, theta_matrix_sweep
 from .metrics import batch_errors, batch_fwhm, batch_sidelobe_stats
-from .simulate import read_frames_pinned
+from .simulate import frame_std, quantize_int16, read_frames_pinned
 from .imaging import (DasPlan, DasWorkspace, HostPipeline, das_from_analytic, das_image, plane_wave_plan,
                       rf_analytic, table_plan)
 

@@ -19,6 +19,7 @@ F64, F32, I16 = 0, 1, 2
 PREC_F32, PREC_F64 = 0, 1
 AP_REF_BOXCAR, AP_HANN = 0, 1
 OUT_ENVELOPE, OUT_COHERENT, OUT_IQ = 0, 1, 2
+ROWCONV_PATHS = {"auto": 0, "tensor": 1, "simt": 2}
 
 DTYPE_CODE = {torch.float64: F64, torch.float32: F32, torch.int16: I16}
 
@@ -47,6 +48,7 @@ SIGNATURES = {
     "tidas_window_dots_f64": ([_P, _P, _I32, _P, _P, _I32, _P, _P], C.c_int),
     "tidas_rowconv_fwd_f32": ([_P, _P, _P, _I64, _I32, _I32, _I32, _P], C.c_int),
     "tidas_rowconv_adj_f32": ([_P, _P, _P, _I64, _I32, _I32, _I32, _P], C.c_int),
+    "tidas_rowconv_f32": ([_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P], C.c_int),
     "tidas_window_frames_f64": ([_P, _I32, _I32, _I32, _P, _P, _P, _P, _P], C.c_int),
     "tidas_window_spectra_f64": ([_P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _I32, _P, _P],
                                  C.c_int),
@@ -57,6 +59,8 @@ SIGNATURES = {
     "tidas_line_sidelobes": ([_P, C.c_int, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P], C.c_int),
     "tidas_synthesize": ([_P, _P, _P, _P, _I32, _I32, _I32, _I32, _D, _D, _D, _D, _D, _I32,
                           _I32, _P, C.c_int, _P], C.c_int),
+    "tidas_frame_std": ([_P, C.c_int, _I64, _I64, _P, _P], C.c_int),
+    "tidas_quantize_i16": ([_P, C.c_int, _I64, _I64, _P, _D, _P, _P], C.c_int),
 }
 
 _lock = threading.Lock()

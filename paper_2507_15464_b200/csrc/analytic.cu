@@ -172,217 +172,6 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
 }
 
 
-// Hilbert mode, FP32, N = 2^LOGN in {2048, 4096, 8192} (cfg1 / cfg2-3 / cfg5):
-// radix-8 passes (plus one radix-4 / radix-2 pass when LOGN % 3 != 0), N / 8
-// threads, 8 elements per thread. The first forward pass starts from the
-// registers the global loads filled, the Hilbert multiplier is applied as the
-// first inverse pass loads, and when the last inverse pass is radix-8 it writes
-// global memory straight from registers — up to three shared-memory round trips
-// and three barriers fewer than the generic schedule.
-template <int LOGN, int DONE, bool INV>
-__device__ __forceinline__ void fused_rest(cplx<float>* s, cplx<float> (&v)[8], float invN) {
-  constexpr int N = 1 << LOGN;
-  if constexpr (DONE < LOGN) {
-    constexpr int LEFT = LOGN - DONE;
-    if constexpr (LEFT > 3) {
-      pass8_fused<float, INV, N, (1 << DONE), true, true, false>(s, v, invN);
-      fused_rest<LOGN, DONE + 3, INV>(s, v, invN);
-    } else if constexpr (LEFT == 3) {
-      // last pass: the inverse keeps its outputs in registers (element tid + r N / 8)
-      pass8_fused<float, INV, N, (1 << DONE), true, !INV, false>(s, v, invN);
-    } else {
-      stockham_pass<float, (1 << LEFT), INV, 8>(s, N, 1 << DONE, TW_LOG - LOGN);
-    }
-  }
-}
-
-template <typename In, int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 8) analytic_fused_kernel(const In* __restrict__ rf, int64_t stride,
-                                                                       float scale, cplx<float>* __restrict__ out,
-                                                                       int64_t n_rows, int32_t* __restrict__ support) {
-  using R = float;
-  using C = cplx<R>;
-  constexpr int N = 1 << LOGN, NT = N / 8;
-  constexpr bool LAST_IN_REGS = (LOGN % 3) == 0;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* s = reinterpret_cast<C*>(smem_raw);
-  __shared__ int first_nz[2], last_nz[2];
-  const int64_t ra = 2 * (int64_t)blockIdx.x;
-  const bool has_b = ra + 1 < n_rows;
-  const In* src_a = rf + ra * stride;
-  const In* src_b = rf + (ra + 1) * stride;
-  if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
-  R xa[8], xb[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int n = threadIdx.x + k * NT;
-    xa[k] = R(load_as_double(src_a + n)) * scale;
-    xb[k] = has_b ? R(load_as_double(src_b + n)) * scale : R(0);
-  }
-  C v[8];
-  int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int n = threadIdx.x + k * NT;
-    if (xa[k] != R(0)) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
-    if (xb[k] != R(0)) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
-    v[k].x = xa[k];
-    v[k].y = xb[k];
-  }
-  __syncthreads();  // first_nz / last_nz initialised
-  if (support) {
-    if (lo_a < N) atomicMin(&first_nz[0], lo_a);
-    if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
-    if (lo_b < N) atomicMin(&first_nz[1], lo_b);
-    if (hi_b >= 0) atomicMax(&last_nz[1], hi_b);
-  }
-  const R invN = R(1) / R(N);
-  pass8_fused<R, false, N, 1, false, true, false>(s, v, invN);  // inputs from registers
-  fused_rest<LOGN, 3, false>(s, v, invN);
-  pass8_fused<R, true, N, 1, true, true, true>(s, v, invN);     // Hilbert multiplier on load
-  fused_rest<LOGN, 3, true>(s, v, invN);
-  if constexpr (!LAST_IN_REGS) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = s[fpad(threadIdx.x + k * NT)];
-  }
-  C* dst_a = out + ra * (int64_t)N;
-  C* dst_b = dst_a + N;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int n = threadIdx.x + k * NT;
-    C a; a.x = xa[k]; a.y = v[k].x;
-    dst_a[n] = a;
-    if (has_b) { C b; b.x = xb[k]; b.y = v[k].y; dst_b[n] = b; }
-  }
-  if (support) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int c = 0; c < (has_b ? 2 : 1); ++c) {
-        const bool any = last_nz[c] >= 0;
-        support[2 * (ra + c)] = any ? first_nz[c] : -1;
-        support[2 * (ra + c) + 1] = any ? last_nz[c] : -1;
-      }
-    }
-  }
-}
-
-// Persistent, TMA-staged form of analytic_fused_kernel (same arithmetic, so the
-// same bits): each CTA loops over channel pairs p = blockIdx.x + i gridDim.x.
-// Thread 0 streams pair i + 1's two input rows into the other half of a
-// double-buffered shared staging area with one cp.async.bulk per row
-// (mbarrier tx-count) while the CTA transforms pair i, so the HBM latency of
-// the input leaves the critical path; the real parts of the output are re-read
-// from the staging rows instead of being held in 16 registers across the FFT.
-// Needs 16-byte aligned rows (the launcher checks and otherwise uses
-// analytic_fused_kernel).
-__device__ __forceinline__ unsigned k1_su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void k1_bar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "K1W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1, %2;\n"
-      " @!p bra K1W_%=;\n}\n" ::"r"(k1_su32(b)), "r"(parity), "r"(1000000u) : "memory");
-}
-
-template <typename In, int LOGN>
-__device__ __forceinline__ void k1_issue_pair(const In* rf, int64_t stride, int64_t n_rows, int64_t pair, In* dst,
-                                              uint64_t* bar) {
-  constexpr int N = 1 << LOGN;
-  constexpr unsigned ROWB = N * sizeof(In);
-  const int64_t ra = 2 * pair;
-  const int nr = ra + 1 < n_rows ? 2 : 1;
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(k1_su32(bar)), "r"(nr * ROWB) : "memory");
-  for (int r = 0; r < nr; ++r)
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                 ::"r"(k1_su32(dst + r * N)), "l"(rf + (ra + r) * stride), "r"(ROWB), "r"(k1_su32(bar)) : "memory");
-}
-
-template <typename In, int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 8) analytic_stream_kernel(const In* __restrict__ rf, int64_t stride,
-                                                                        float scale, cplx<float>* __restrict__ out,
-                                                                        int64_t n_rows, int32_t* __restrict__ support) {
-  using R = float;
-  using C = cplx<R>;
-  constexpr int N = 1 << LOGN, NT = N / 8;
-  constexpr bool LAST_IN_REGS = (LOGN % 3) == 0;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  In* stage = reinterpret_cast<In*>(smem_raw);  // [2 buffers][2 rows][N]
-  C* s = reinterpret_cast<C*>(smem_raw + 4 * (size_t)N * sizeof(In));
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ int first_nz[2][2], last_nz[2][2];
-  const int tid = threadIdx.x;
-  const int64_t n_pairs = (n_rows + 1) / 2;
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(k1_su32(&bar[0])));
-    asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(k1_su32(&bar[1])));
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (tid < 2) { first_nz[0][tid] = N; last_nz[0][tid] = -1; }
-  __syncthreads();
-  if (tid == 0 && (int64_t)blockIdx.x < n_pairs) k1_issue_pair<In, LOGN>(rf, stride, n_rows, blockIdx.x, stage, &bar[0]);
-  const R invN = R(1) / R(N);
-  int it = 0;
-  for (int64_t pair = blockIdx.x; pair < n_pairs; pair += gridDim.x, ++it) {
-    const int b = it & 1;
-    const int64_t nxt = pair + gridDim.x;
-    if (tid == 0 && nxt < n_pairs) {
-      // the other buffer was last read in iteration it - 1, which ended at a barrier
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      k1_issue_pair<In, LOGN>(rf, stride, n_rows, nxt, stage + (size_t)(b ^ 1) * 2 * N, &bar[b ^ 1]);
-    }
-    const int64_t ra = 2 * pair;
-    const bool has_b = ra + 1 < n_rows;
-    const In* st_a = stage + (size_t)b * 2 * N;
-    const In* st_b = st_a + N;
-    k1_bar_wait(&bar[b], (unsigned)(it >> 1) & 1u);
-    C v[8];
-    int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int n = tid + k * NT;
-      const R xa = R(load_as_double(st_a + n)) * scale;
-      const R xb = has_b ? R(load_as_double(st_b + n)) * scale : R(0);
-      if (xa != R(0)) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
-      if (xb != R(0)) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
-      v[k].x = xa;
-      v[k].y = xb;
-    }
-    if (support) {  // slot b was reset in iteration it - 2 (or the prologue) before a barrier
-      if (lo_a < N) atomicMin(&first_nz[b][0], lo_a);
-      if (hi_a >= 0) atomicMax(&last_nz[b][0], hi_a);
-      if (lo_b < N) atomicMin(&first_nz[b][1], lo_b);
-      if (hi_b >= 0) atomicMax(&last_nz[b][1], hi_b);
-    }
-    pass8_fused<R, false, N, 1, false, true, false>(s, v, invN);  // inputs from registers
-    fused_rest<LOGN, 3, false>(s, v, invN);
-    pass8_fused<R, true, N, 1, true, true, true>(s, v, invN);     // Hilbert multiplier on load
-    fused_rest<LOGN, 3, true>(s, v, invN);
-    if constexpr (!LAST_IN_REGS) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = s[fpad(tid + k * NT)];
-    }
-    C* dst_a = out + ra * (int64_t)N;
-    C* dst_b = dst_a + N;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int n = tid + k * NT;
-      C a; a.x = R(load_as_double(st_a + n)) * scale; a.y = v[k].x;
-      dst_a[n] = a;
-      if (has_b) { C bb; bb.x = R(load_as_double(st_b + n)) * scale; bb.y = v[k].y; dst_b[n] = bb; }
-    }
-    if (support) {
-      __syncthreads();
-      if (tid == 0) {
-        for (int c = 0; c < (has_b ? 2 : 1); ++c) {
-          const bool any = last_nz[b][c] >= 0;
-          support[2 * (ra + c)] = any ? first_nz[b][c] : -1;
-          support[2 * (ra + c) + 1] = any ? last_nz[b][c] : -1;
-        }
-      }
-    }
-    if (tid < 2) { first_nz[b ^ 1][tid] = N; last_nz[b ^ 1][tid] = -1; }
-    __syncthreads();  // staging buffer b and s are free for the next pair
-  }
-}
 
 // ------------------------------------------- N = 4096: 64 x 64 in registers
 //
@@ -1195,21 +984,15 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
     constexpr int EPT = sizeof(R) == 4 ? 8 : 16;
     auto kern = delay ? analytic_pow2_kernel<R, In, true, EPT> : analytic_pow2_kernel<R, In, false, EPT>;
     if constexpr (sizeof(R) == 4) {
-      const bool aligned = (reinterpret_cast<uintptr_t>(rf) % 16 == 0) && ((stride * sizeof(In)) % 16 == 0) &&
-                           ((N * sizeof(In)) % 16 == 0);
-      static const int k1_mode = [] {
-        // 0 = fused (one CTA per pair), 1 = persistent TMA-staged, 2 (default): N = 2048 /
-        // 4096 / 8192 run as 32 x 64 / 64 x 64 / 64 x 128 four-steps in registers
-        // (analytic_r2048_kernel / analytic_r32_kernel / analytic_r8192_kernel)
-        const char* e = getenv("TIDAS_K1_MODE");
-        return e ? atoi(e) : 2;
-      }();
-      if (!delay && logN == 11 && k1_mode == 2) {
+      // N = 2048 / 4096 / 8192 (cfg1 / cfg2-3 / cfg5) run as 32 x 64 / 64 x 64 / 64 x 128
+      // four-step FFTs in registers (analytic_r2048_kernel / analytic_r32_kernel /
+      // analytic_r8192_kernel); other lengths take the shared-memory Stockham kernel
+      if (!delay && logN == 11) {
         TIDAS_CUDA_CHECK(launch_pdl(analytic_r2048_kernel<In>, dim3((unsigned)((n_rows + 1) / 2)), dim3(64), 0, st,
                                     rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
         return TIDAS_OK;
       }
-      if (!delay && logN == 13 && k1_mode == 2) {
+      if (!delay && logN == 13) {
         auto kr = analytic_r8192_kernel<In>;
         const size_t smem8 = sizeof(float2) * 128 * 65;
         TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8));
@@ -1217,54 +1000,11 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
                                     (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
         return TIDAS_OK;
       }
-      if (!delay && logN == 12 && k1_mode == 2) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)((n_rows + 1) / 2));
-        cfg.blockDim = dim3(128);
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        TIDAS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, analytic_r32_kernel<In>, rf, stride, (float)scale,
-                                            reinterpret_cast<cplx<float>*>(out), n_rows, support));
-        TIDAS_LAUNCH_CHECK();
+      if (!delay && logN == 12) {
+        TIDAS_CUDA_CHECK(launch_pdl(analytic_r32_kernel<In>, dim3((unsigned)((n_rows + 1) / 2)), dim3(128), 0, st,
+                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
         return TIDAS_OK;
       }
-      if (!delay && logN >= 11 && logN <= 13 && aligned && sizeof(In) <= 4 && k1_mode >= 1 &&
-          !getenv("TIDAS_K1_GENERIC")) {
-        auto ks = logN == 11 ? analytic_stream_kernel<In, 11>
-                             : (logN == 12 ? analytic_stream_kernel<In, 12> : analytic_stream_kernel<In, 13>);
-        const size_t smem_s = smem + 4 * (size_t)N * sizeof(In);
-        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
-        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(ks, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        int per_sm = 0, sms = 0;
-        TIDAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, N / 8, smem_s));
-        TIDAS_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        const int64_t pairs = (n_rows + 1) / 2;
-        const int64_t grid = std::min<int64_t>(pairs, (int64_t)std::max(per_sm, 1) * sms);
-        ks<<<(unsigned)grid, N / 8, smem_s, st>>>(rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out),
-                                                  n_rows, support);
-        TIDAS_LAUNCH_CHECK();
-        return TIDAS_OK;
-      }
-      if (!delay && logN >= 11 && logN <= 13 && !getenv("TIDAS_K1_GENERIC")) {
-        const int64_t ctasf = (n_rows + 1) / 2;
-        auto kf = logN == 11 ? analytic_fused_kernel<In, 11>
-                             : (logN == 12 ? analytic_fused_kernel<In, 12> : analytic_fused_kernel<In, 13>);
-        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        kf<<<(unsigned)ctasf, N / 8, smem, st>>>(rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out),
-                                                 n_rows, support);
-        TIDAS_LAUNCH_CHECK();
-        return TIDAS_OK;
-      }
-    }
-    if constexpr (sizeof(R) == 4) {  // compile-time FFT schedule for the common lengths
-      if (!delay && logN == 11) kern = analytic_pow2_kernel<R, In, false, EPT, 11>;
-      if (!delay && logN == 12) kern = analytic_pow2_kernel<R, In, false, EPT, 12>;
-      if (!delay && logN == 13) kern = analytic_pow2_kernel<R, In, false, EPT, 13>;
     }
     TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));

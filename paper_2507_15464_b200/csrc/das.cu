@@ -12,7 +12,7 @@
 //   value = (1-f) |C(k0)| + f |C(k0+1)|
 // so each (pixel, channel) reads three consecutive complex samples.
 //
-// Layout / schedule (B200, default variant — case 0 of the variant table):
+// Layout / schedule (B200, FP32 path):
 //   * CTA = 8 consumer warps + 1 producer warp, 3 CTAs per SM. The consumers
 //     cover 32 depths x 8 columns; a warp covers 4 depths x 8 columns, so the
 //     16 lanes of a half-warp (2 depths x 8 columns) read taps within ~16
@@ -197,14 +197,34 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
 // (producer). Buffer b is guarded by full[b] (copy landed, tx-count) and
 // empty[b] (all 8 consumer warps done); consumers never meet at a CTA barrier
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
-template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
-          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
-          bool U32 = false, int WZ = 8, bool ONE_TX = false, bool LPT = false>
-__global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams p,
-                                                                   const cplx<R>* __restrict__ A,
-                                                                   void* __restrict__ out_,
-                                                                   const __grid_constant__ CUtensorMap tmap) {
+// Per-precision tile / staging shape. FP32 (the throughput path): FB = 8 frames
+// per thread, warps of WZ = 4 depths x 8 columns, DG = 8 warp rows (CTA 32 x 8
+// pixels), TMA tensor boxes of [8 frames][CPB = 2 channels][256 samples],
+// 32-bit shared-window gathers, deepest-depth-tile-first dispatch (LPT). FP64
+// (the drop-in path, reference semantics): one frame, 1-channel bulk copies.
+// A fixed FB per precision keeps every frame's arithmetic independent of how
+// many frames share a launch: images are bit-identical under any batching or
+// sharding.
+template <typename R> struct DasShape;
+template <> struct DasShape<float> {
+  static constexpr int FB = 8, DG = 8, WZ = 4, WCAP = 254, CPB = 2;
+  static constexpr bool TMAP = true, U32 = true, LPT = true;
+};
+template <> struct DasShape<double> {
+  static constexpr int FB = 1, DG = 4, WZ = 8, WCAP = DAS_WMAX, CPB = 1;
+  static constexpr bool TMAP = false, U32 = false, LPT = false;
+};
+constexpr int DAS_NW = 8;  // consumer warps per CTA (+ 1 producer warp)
+
+template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX>
+__global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasParams p,
+                                                                       const cplx<R>* __restrict__ A,
+                                                                       void* __restrict__ out_,
+                                                                       const __grid_constant__ CUtensorMap tmap) {
   using C = cplx<R>;
+  using S = DasShape<R>;
+  constexpr int FB = S::FB, DG = S::DG, WZ = S::WZ, WCAP = S::WCAP, CPB = S::CPB, NW = DAS_NW;
+  constexpr bool TMAP = S::TMAP, U32 = S::U32, LPT = S::LPT;
   constexpr int DAS_WSTRIDE = WCAP + 2;  // per-frame window stride (elements, even)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   C* win = reinterpret_cast<C*>(smem_raw);  // [DAS_NBUF][FB][DAS_WSTRIDE]
@@ -333,7 +353,7 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
     const int w_lo = rw[0], w_hi = rw[1];
     if (w_hi < w_lo || c_lo > c_hi) continue;  // CTA-uniform
     const int W = w_hi - w_lo + 1;
-    const bool staged = !DIRECT && W <= WCAP;
+    const bool staged = W <= WCAP;
     // element e of a staged window is sample (s0 + e) mod N of the channel row
     // (s0 even: every bulk copy is 16-byte aligned); per frame one or two
     // (wrap-around) bulk copies
@@ -349,7 +369,7 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
     constexpr int SLOT = FB * CPB * DAS_WSTRIDE;  // elements per buffer: [FB][CPB][WSTRIDE]
 
     if (producer) {
-      if (staged && lane == 0 && DIAG != 1) {
+      if (staged && lane == 0) {
         const int seg0 = s0 < 0 ? s0 + p.N : s0;
         const int len0 = min(Wc, p.N - seg0);
         // one tensor copy per block when the window does not wrap around the row
@@ -361,14 +381,13 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
           if (use > 0) mbar_wait(&empty[buf], (use - 1) & 1);
           const int n0 = c_lo + kb * CPB;
           C* dst = win + (size_t)buf * SLOT;
-          if (DIAG == 4) { mbar_arrive(&full[buf]); continue; }  // diag: no copy at all
           if (tensor) {
             mbar_expect_tx(&full[buf], (unsigned)(SLOT * sizeof(C)));
             tma_load_4d(dst, &tmap, s0, n0 + half, a, f0, &full[buf]);
             continue;
           }
           const int nc = min(CPB, c_hi - n0 + 1);
-          const int ncopy = DIAG == 3 ? 1 : nfb;  // diag: one frame only
+          const int ncopy = nfb;
           mbar_expect_tx(&full[buf], (unsigned)(nc * ncopy * Wc * sizeof(C)));
           for (int c = 0; c < nc; ++c) {
             const C* row = fbase + (int64_t)(n0 + c) * rowN;
@@ -391,14 +410,14 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
       // and one accumulator per frame carries the whole sum over transmits:
       //   (1 - f) C(k0) + f C(k0 + 1) = sum_n u_-1 A[j - 1] + u_0 A[j] + u_+1 A[j + 1]
       //   u_-1 = w1 (1 - f), u_0 = w0 (1 - f) + w1 f, u_+1 = w0 f
-      constexpr bool FOLD_IQ = sizeof(R) == 4 && F2 && OUT != TIDAS_OUT_ENVELOPE;
+      constexpr bool FOLD_IQ = sizeof(R) == 4 && OUT != TIDAS_OUT_ENVELOPE;
       auto accumulate = [&](const Tap<R>& t, int b, C am1, C a0, C ap1) {
         if constexpr (FOLD_IQ) {
           const float g = 1.0f - fr;
           const float um = t.w1 * g, up = t.w0 * fr, u0 = fmaf(t.w0, g, t.w1 * fr);
           acc_iq[b] = __ffma2_rn(make_float2(um, um), am1,
                                  __ffma2_rn(make_float2(u0, u0), a0, __ffma2_rn(make_float2(up, up), ap1, acc_iq[b])));
-        } else if constexpr (sizeof(R) == 4 && F2) {
+        } else if constexpr (sizeof(R) == 4) {
           // packed FP32 (FFMA2, sm_100): one instruction per complex multiply-add,
           // the same per-component roundings as the scalar form below
           const float2 w0 = make_float2(t.w0, t.w0), w1 = make_float2(t.w1, t.w1);
@@ -427,14 +446,14 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
       for (int kb = 0; kb < n_blk; ++kb) {
         const unsigned g = g0 + kb;
         const int buf = (int)(g % DAS_NBUF);
-        if (staged && DIAG != 1) mbar_wait_u32(full_u + 8u * buf, (g / DAS_NBUF) & 1);
+        if (staged) mbar_wait_u32(full_u + 8u * buf, (g / DAS_NBUF) & 1);
 #pragma unroll
         for (int c = 0; c < CPB; ++c, dnf += 1.0f) {
           const int n = c_lo + kb * CPB + c;
           if (n > c_hi) break;
           Tap<R> t;
           bool live = false;
-          if (DIAG < 2 && n >= wn_lo && n <= wn_hi) {
+          if (n >= wn_lo && n <= wn_hi) {
             bool in_ap = true;
             if (AP == TIDAS_AP_REF_BOXCAR) in_ap = active_px && n >= -ap_h && n < ap_h;
             if (sizeof(R) == 8) in_ap = in_ap && active_px && n >= n_lo && n <= n_hi;
@@ -485,7 +504,7 @@ __global__ void __launch_bounds__(32 * NW + 32, MINB) das_image_kernel(DasParams
         }
         if (staged) {
           __syncwarp();
-          if (DIAG != 1 && lane == 0) mbar_arrive_u32(empty_u + 8u * buf);
+          if (lane == 0) mbar_arrive_u32(empty_u + 8u * buf);
         }
       }
       if (active_px && !FOLD_IQ) {
@@ -533,16 +552,16 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
   out[i] = (x[ix] * sn + z[iz] * cs + origin) / c + z[iz] / c;
 }
 
-template <typename R, int AP, int OUT, int FB, int DAS_NBUF, int MINB = 3, bool DIRECT = false, int DG = 4,
-          int WCAP = DAS_WMAX, int DIAG = 0, int NW = 8, bool TMAP = false, int CPB = 1, bool F2 = true,
-          bool U32 = false, int WZ = 8, bool ONE_TX = false, bool LPT = false>
+template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
-  auto kern = das_image_kernel<R, AP, OUT, FB, DAS_NBUF, MINB, DIRECT, DG, WCAP, DIAG, NW, TMAP, CPB, F2, U32, WZ, ONE_TX, LPT>;
+  using S = DasShape<R>;
+  constexpr int FB = S::FB, DG = S::DG, WZ = S::WZ, WCAP = S::WCAP, CPB = S::CPB, NW = DAS_NW;
+  auto kern = das_image_kernel<R, AP, OUT, DAS_NBUF, MINB, ONE_TX>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
-  if (TMAP) {
-    static_assert(!TMAP || (sizeof(C) == 8 && WCAP + 2 <= 256), "tensor path: complex64, box <= 256");
+  if constexpr (S::TMAP) {
+    static_assert(sizeof(C) == 8 && WCAP + 2 <= 256, "tensor path: complex64, box <= 256");
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
       cudaDriverEntryPointQueryResult q;
@@ -565,7 +584,7 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
   constexpr int TZ = WZ * DG, TXC = (32 / WZ) * (NW / DG);
   dim3 grid((p.nz + TZ - 1) / TZ, (p.nx + TXC - 1) / TXC, (p.F + FB - 1) / FB);
   TIDAS_REQUIRE(grid.y <= 65535 && grid.z <= 65535, "pixel grid / frame batch too large");
-  if (LPT) {
+  if (S::LPT) {
     const long long total = (long long)grid.x * grid.y * grid.z;
     TIDAS_REQUIRE(total < (1LL << 31), "pixel grid / frame batch too large");
     grid = dim3((unsigned)total, 1, 1);
@@ -585,62 +604,22 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
   return TIDAS_OK;
 }
 
-// A fixed frame-batch width per precision (not chosen from F) keeps every
-// frame's arithmetic independent of how many frames share the launch, so
-// images are bit-identical under any batching or sharding (all float variants
-// below use FB = 8 except 73, which exists for timing only).
-// Tuning variants (TIDAS_DAS_VARIANT, for benchmarking only; default 0):
-//   0: FB 8, 2-channel TMA tensor boxes, 2 buffers, 3 CTAs/SM (27 warps: the
-//      kernel is latency-bound once the bank conflicts are gone), single-transmit
-//      loop compiled without live frame accumulators, CTAs dispatched deepest
-//      depth tile first (longest first: a short last wave; 5.13 us/frame; 55 = the
-//      same in the natural grid order, 5.31 us; 56 = 55 without the single-transmit
-//      specialisation, 5.70 us); multi-transmit / complex-output plans use 57 in
-//      the deepest-first order instead (cfg3 4338 against 3975 frames/s),
-//      FFMA2 accumulation, gathers as ld.shared on 32-bit window offsets, warps
-//      of 4 depths x 8 columns (a half-warp spans ~2 depths = ~8 + lateral
-//      samples: 1.0M instead of 16.1M bank conflicts per 64 frames with 8 x 4)
-//   73: FB 6, 3 buffers, 3 CTAs/SM   57: FB 8, 3 buffers, 2 CTAs/SM (5.99 us)
-//   (round-1 FB 4 / 16-warp / 1-channel-box variants were slower and are removed)
-//   58: 57 with 8 x 4 warps (6.12 us)   62: 2 x 16 warps (CTA 16 x 16)
-//   59: 58 with generic-pointer gathers   34: 59 with scalar FFMA (round-1 default)
-static int das_variant() {
-  static int v = [] {
-    const char* e = getenv("TIDAS_DAS_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
+// Buffers / occupancy per plan (measured on B200): single-transmit
+// envelope images (cfg1 / 2 / 5) compile the transmit loop without live frame
+// accumulators and run 2 window buffers at 3 CTAs / SM (the kernel is
+// latency-bound once the bank conflicts are gone); complex outputs (cfg3
+// coherent: folded accumulation, few registers) also run 2 buffers at 3 CTAs /
+// SM; multi-transmit envelope compounding keeps c0 / c1 and the frame
+// accumulators live across transmits and runs 3 buffers at 2 CTAs / SM. The
+// choice depends on the plan only, never on the frame count.
 template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   if constexpr (sizeof(R) == 8) {
-    return launch_das<R, AP, OUT, 1, 4>(p, A, out, st);
+    return launch_das<R, AP, OUT, 4, 3, false>(p, A, out, st);
   } else {
-    switch (das_variant()) {
-      case 34: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, false>(p, A, out, st);
-      case 55: return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true>(p, A, out, st);
-      case 56: return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
-      case 57: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
-      case 58: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, true, 8>(p, A, out, st);
-      case 73: return launch_das<R, AP, OUT, 6, 3, 3, false, 8, 254, 0, 8, true, 2, true, true, 4>(p, A, out, st);
-      case 62: return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 2>(p, A, out, st);
-      case 59: return launch_das<R, AP, OUT, 8, 3, 2, false, 4, 254, 0, 8, true, 2, true, false>(p, A, out, st);
-      default:
-        // measured best on B200: 8 frames per thread, TMA tensor boxes of [8 frames][2
-        // channels][256 samples], 2 buffers and 3 CTAs/SM for single-transmit envelope
-        // images (cfg1 / 2 / 5, single-transmit specialisation) and for complex outputs
-        // (cfg3 coherent: folded accumulation, 4512 against 4393 frames/s with 2 CTAs/SM);
-        // multi-transmit envelope compounding keeps c0 / c1 and the frame accumulators
-        // live across transmits and runs with 3 buffers at 2 CTAs/SM. The choice depends
-        // on the plan only, never on the frame count, so images stay bitwise
-        // batching-invariant.
-        if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1)
-          return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, true, true>(p, A, out, st);
-        if (OUT != TIDAS_OUT_ENVELOPE)  // folded complex accumulation: few registers, 3 CTAs/SM
-          return launch_das<R, AP, OUT, 8, 2, 3, false, 8, 254, 0, 8, true, 2, true, true, 4, false, true>(p, A, out, st);
-        return launch_das<R, AP, OUT, 8, 3, 2, false, 8, 254, 0, 8, true, 2, true, true, 4, false, true>(p, A, out, st);
-    }
+    if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1) return launch_das<R, AP, OUT, 2, 3, true>(p, A, out, st);
+    if (OUT != TIDAS_OUT_ENVELOPE) return launch_das<R, AP, OUT, 2, 3, false>(p, A, out, st);
+    return launch_das<R, AP, OUT, 3, 2, false>(p, A, out, st);
   }
 }
 

@@ -17,7 +17,6 @@
 // loads (tap loads are warp broadcasts). 129 taps -> 16 FMA per shared load.
 #include <algorithm>
 #include <cstdlib>
-#include <string>
 
 #include "common.cuh"
 
@@ -137,35 +136,27 @@ __global__ void rowconv_generic_kernel(const float* __restrict__ in, const float
 }
 
 template <bool ADJ>
-int launch_rowconv_tc(const float* in, const float* K, float* out, int64_t batch, int nz, int nx, int T,
-                      cudaStream_t st);
-template <bool ADJ>
 int launch_rowconv_tc1(const float* in, const float* K, float* out, int64_t batch, int nz, int nx, int T,
                       cudaStream_t st);
 
-// TIDAS_ROWCONV_PATH=simt forces the CUDA-core kernel (tests compare both paths)
-static bool rowconv_tc_enabled() {
-  // read per call (cheap next to a launch) so one process can compare both paths
-  const char* e = getenv("TIDAS_ROWCONV_PATH");
-  return !(e && std::string(e) == "simt");
-}
-
+// path: TIDAS_ROWCONV_AUTO (tensor cores when the shape fits, else CUDA cores),
+// TIDAS_ROWCONV_TENSOR (tensor cores or TIDAS_EUNSUPPORTED), TIDAS_ROWCONV_SIMT
 template <bool ADJ>
 static int launch_rowconv(const float* in, const float* K, float* out, int64_t batch, int nz, int nx,
-                          int T, cudaStream_t st) {
+                          int T, int path, cudaStream_t st) {
   TIDAS_REQUIRE(batch >= 0 && nz >= 0 && nx >= 0, "bad sizes");
   TIDAS_REQUIRE(T >= 1 && (T & 1) && T <= 255, "taps must be odd and in [1, 255]");
   if (batch == 0 || nz == 0 || nx == 0) return TIDAS_OK;  // empty (null data pointers allowed)
   TIDAS_REQUIRE(in && K && out, "null pointer");
-  // tensor cores (tcgen05, 3xTF32) for batches that fill the 128-map MMA tile
-  if (rowconv_tc_enabled() && batch >= 32) {
-    // tcgen05 paths: 128 maps per block (rowconv_tc1.cu) unless
-    // TIDAS_ROWCONV_TC=2p selects the 64-map x 2-phase kernel (rowconv_tc.cu)
-    const char* e = getenv("TIDAS_ROWCONV_TC");
-    const bool two_phase = e && std::string(e) == "2p";
-    const int rc = two_phase ? launch_rowconv_tc<ADJ>(in, K, out, batch, nz, nx, T, st)
-                             : launch_rowconv_tc1<ADJ>(in, K, out, batch, nz, nx, T, st);
-    if (rc != TIDAS_EUNSUPPORTED) return rc;
+  TIDAS_REQUIRE(path == TIDAS_ROWCONV_AUTO || path == TIDAS_ROWCONV_TENSOR || path == TIDAS_ROWCONV_SIMT,
+                "unknown row-convolution path %d", path);
+  // tensor cores (tcgen05, 3xTF32, rowconv_tc1.cu) for batches that fill the 128-map MMA tile
+  if (path != TIDAS_ROWCONV_SIMT && batch >= 32) {
+    const int rc = launch_rowconv_tc1<ADJ>(in, K, out, batch, nz, nx, T, st);
+    if (rc != TIDAS_EUNSUPPORTED || path == TIDAS_ROWCONV_TENSOR) return rc;
+  } else if (path == TIDAS_ROWCONV_TENSOR) {
+    set_error("tensor-core row convolution needs batch >= 32 (got %lld)", (long long)batch);
+    return TIDAS_EUNSUPPORTED;
   }
   const bool aligned = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
   if ((nx & 7) || !aligned) {
@@ -195,10 +186,16 @@ static int launch_rowconv(const float* in, const float* K, float* out, int64_t b
 
 extern "C" int tidas_rowconv_fwd_f32(const float* g, const float* K, float* y, int64_t batch,
                                      int32_t nz, int32_t nx, int32_t taps, void* stream) {
-  return tidas::launch_rowconv<false>(g, K, y, batch, nz, nx, taps, tidas::as_stream(stream));
+  return tidas::launch_rowconv<false>(g, K, y, batch, nz, nx, taps, TIDAS_ROWCONV_AUTO, tidas::as_stream(stream));
 }
 
 extern "C" int tidas_rowconv_adj_f32(const float* y, const float* K, float* g, int64_t batch,
                                      int32_t nz, int32_t nx, int32_t taps, void* stream) {
-  return tidas::launch_rowconv<true>(y, K, g, batch, nz, nx, taps, tidas::as_stream(stream));
+  return tidas::launch_rowconv<true>(y, K, g, batch, nz, nx, taps, TIDAS_ROWCONV_AUTO, tidas::as_stream(stream));
+}
+
+extern "C" int tidas_rowconv_f32(const float* in, const float* K, float* out, int64_t batch, int32_t nz,
+                                 int32_t nx, int32_t taps, int32_t adjoint, int32_t path, void* stream) {
+  return adjoint ? tidas::launch_rowconv<true>(in, K, out, batch, nz, nx, taps, path, tidas::as_stream(stream))
+                 : tidas::launch_rowconv<false>(in, K, out, batch, nz, nx, taps, path, tidas::as_stream(stream));
 }

@@ -58,7 +58,7 @@ template <bool ADJ>
 __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                   const __grid_constant__ CUtensorMap omap,
                                                                   const float* __restrict__ K, int batch, int nz,
-                                                                  int nx, int T, int units_per, int diag) {
+                                                                  int nx, int T, int units_per) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sbase = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   unsigned char* B_st = sbase;                        // [2 rows][40 KB]
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
           const int s0 = (int)((g0 + j) % RING);
           int slot = s0;
 #pragma unroll 1
-          for (int c = 0; c < (diag == 1 ? 0 : CHB); ++c) {
+          for (int c = 0; c < CHB; ++c) {
             const unsigned a_hi = COL_HI + (unsigned)slot * CH, a_lo = COL_LO + (unsigned)slot * CH;
             const unsigned bo = (unsigned)c * (B_ATOM >> 4);
             const bool first = (c == 0);
@@ -334,8 +334,7 @@ int launch_rowconv_tc1(const float* in, const float* K, float* out, int64_t batc
   const long long units = (long long)nz * ((batch + MAPS - 1) / MAPS);
   const int units_per = (int)((units + sms - 1) / sms);
   const int grid = (int)((units + units_per - 1) / units_per);
-  static const int diag = getenv("TIDAS_ROWCONV_DIAG") ? atoi(getenv("TIDAS_ROWCONV_DIAG")) : 0;
-  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, (int)batch, nz, nx, T, units_per, diag);
+  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, (int)batch, nz, nx, T, units_per);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
 }

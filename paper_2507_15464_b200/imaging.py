@@ -145,9 +145,19 @@ def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=Non
     rf = rf.contiguous()
     n = int(rf.shape[-1])
     rows = rf.numel() // n if n else 0
+    if prec not in ("f32", "f64"):
+        raise ValueError(f"prec must be 'f32' or 'f64', got {prec!r}")
     pc = _lib.PREC_F32 if prec == "f32" else _lib.PREC_F64
     if out is None:
         out = torch.empty(rf.shape, dtype=_COMPLEX[pc], device=rf.device)
+    # the kernel writes rows x n complex values into out: it must be exactly that
+    if out.dtype != _COMPLEX[pc] or tuple(out.shape) != tuple(rf.shape) or not out.is_contiguous() \
+            or out.device != rf.device:
+        raise ValueError(f"out must be a contiguous {_COMPLEX[pc]} tensor of shape {tuple(rf.shape)} "
+                         f"on {rf.device}, got {out.dtype} {tuple(out.shape)}")
+    if support is not None and (support.dtype != torch.int32 or support.numel() != 2 * rows
+                                or not support.is_contiguous() or support.device != rf.device):
+        raise ValueError(f"support must be a contiguous int32 tensor of {rows} x 2 on {rf.device}")
     _lib.check(L.tidas_rf_analytic(_lib.ptr(rf), _lib.DTYPE_CODE[rf.dtype], n, float(scale),
                                    _lib.ptr(out), pc, rows, n, _lib.ptr(support),
                                    _lib.stream_handle(stream)))
@@ -163,14 +173,25 @@ def das_from_analytic(analytic: torch.Tensor, plan: DasPlan, out=None, stream=No
     if tuple(analytic.shape[1:]) != (plan.n_angles, plan.n_el, plan.n_samples):
         raise ValueError(f"analytic shape {tuple(analytic.shape)} does not match the plan "
                          f"[F][{plan.n_angles}][{plan.n_el}][{plan.n_samples}]")
+    if not analytic.is_contiguous():
+        raise ValueError("analytic must be contiguous [F][A][E][N]")
+    dt = _COMPLEX[plan.prec_code] if plan.out == "iq" else _REAL[plan.prec_code]
     if out is None:
-        dt = _COMPLEX[plan.prec_code] if plan.out == "iq" else _REAL[plan.prec_code]
         out = torch.empty((F, plan.nz, plan.nx), dtype=dt, device=analytic.device)
+    _check_image_out(out, F, plan, dt, analytic.device)
     d = plan.desc(F)
     _lib.check(L.tidas_das_image(C.byref(d), _lib.ptr(analytic), _lib.ptr(plan.t_star),
                                  _lib.ptr(plan.x), _lib.ptr(plan.z), _lib.ptr(plan.ap_half),
                                  _lib.ptr(out), _lib.stream_handle(stream)))
     return out
+
+
+def _check_image_out(out: torch.Tensor, F: int, plan: DasPlan, dt, device) -> None:
+    # K2 stores F x nz x nx elements of dt: anything else would write out of bounds
+    if out.dtype != dt or tuple(out.shape) != (F, plan.nz, plan.nx) or not out.is_contiguous() \
+            or out.device != device:
+        raise ValueError(f"out must be a contiguous {dt} tensor of shape ({F}, {plan.nz}, {plan.nx}) on "
+                         f"{device}, got {out.dtype} {tuple(out.shape)} on {out.device}")
 
 
 class DasWorkspace:
@@ -201,10 +222,17 @@ def das_image(rf: torch.Tensor, plan: DasPlan, *, scale: float = 1.0, out=None,
     if rf.dim() != 4:
         raise ValueError("rf must be [F][A][E][N] or [F][E][N]")
     F = int(rf.shape[0])
+    if tuple(rf.shape[1:]) != (plan.n_angles, plan.n_el, plan.n_samples):
+        raise ValueError(f"rf shape {tuple(rf.shape)} does not match the plan "
+                         f"[F][{plan.n_angles}][{plan.n_el}][{plan.n_samples}]")
+    dt = _COMPLEX[plan.prec_code] if plan.out == "iq" else _REAL[plan.prec_code]
     if out is None:
-        dt = _COMPLEX[plan.prec_code] if plan.out == "iq" else _REAL[plan.prec_code]
         out = torch.empty((F, plan.nz, plan.nx), dtype=dt, device=rf.device)
+    _check_image_out(out, F, plan, dt, rf.device)
     ws = workspace or DasWorkspace(plan, rf.device)
+    if ws.plan is not plan and (tuple(ws.buf.shape[1:]) != (plan.n_angles, plan.n_el, plan.n_samples)
+                                or ws.buf.dtype != _COMPLEX[plan.prec_code]):
+        raise ValueError("workspace was built for a plan of another shape or precision")
     for f0 in range(0, F, ws.chunk):
         f1 = min(F, f0 + ws.chunk)
         an = ws.buf[: f1 - f0]

@@ -170,13 +170,44 @@ def tidas_psf(windowed_frame: RfFrame, fixed_delays: DelayProfile, theta: float,
               support: Optional[Tuple[int, int]] = None) -> Trace:
     """theta x fixed-profile delayed sum (tidas.py:317-353).
 
-    ``crop`` / ``support`` are accepted for signature compatibility: K3 is exact
-    on the full axis, which equals the reference's cropped result (the windowed
-    traces are zero outside the support)."""
+    ``crop`` (linear method) follows the reference's cropped path
+    (tidas.py:336-351): the traces are cut to [support0 - span, support1 + 2)
+    (span = ceil(-min delay * fs) + 2), each element is shifted with zero fill on
+    that segment — so a shift of at least the segment length raises ValueError
+    (das.py:87-88) — and the samples outside the segment are 0. ``support``
+    ([lo, hi) of the nonzero samples) defaults to the frame's scanned support;
+    an all-zero frame gives a zero trace. On the device: the traces are zeroed
+    outside the segment and K3 produces only the segment's samples, which is
+    bit-identical to the reference's per-segment shifts."""
     if not np.isfinite(theta):
         raise ValueError(f"theta must be finite, got {theta}")
-    s = _das.delayed_sum(windowed_frame, fixed_delays.element_indices, fixed_delays.delays, method)
-    return Trace(theta * s.samples, windowed_frame.sampling_frequency, windowed_frame.t0)
+    fs, n, t0 = windowed_frame.sampling_frequency, windowed_frame.n_samples, windowed_frame.t0
+    if not (crop and method == "linear"):
+        s = _das.delayed_sum(windowed_frame, fixed_delays.element_indices, fixed_delays.delays, method)
+        return Trace(theta * s.samples, fs, t0)
+    traces = np.asarray(windowed_frame.traces, float)
+    if support is None:
+        nonzero = np.flatnonzero(np.any(traces != 0.0, axis=0))
+        if nonzero.size == 0:
+            return Trace(np.zeros(n), fs, t0)
+        support = (int(nonzero[0]), int(nonzero[-1]) + 1)
+    delays = np.asarray(fixed_delays.delays, float)
+    span = int(np.ceil(-delays.min() * fs)) + 2
+    lo = max(int(support[0]) - span, 0)
+    hi = min(int(support[1]) + 2, n)
+    shifts = (delays * fs)[None, :]
+    _count(len(delays))
+    # the reference shifts a segment of hi - lo samples (das.py:87-88 on that length)
+    _das._check_shifts(shifts, max(hi - lo, 0))
+    out = torch.zeros((1, n), dtype=torch.float64, device=_das._device())
+    if hi > lo:
+        x_d = _to_dev(traces)
+        x_d[:, :lo] = 0.0
+        x_d[:, hi:] = 0.0
+        half = traces.shape[0] // 2
+        rows = (np.asarray(fixed_delays.element_indices).astype(np.int64) + half)[None, :]
+        _delayed_sums_dev(x_d, rows, shifts, np.array([lo]), np.array([hi]), out=out)
+    return Trace(theta * out[0].cpu().numpy(), fs, t0)
 
 
 def theta_row_aligned(reference_depth: float, depth_grid, config: ProbeConfig,
@@ -241,7 +272,8 @@ def tidas_line(frame: RfFrame, fixed_delays: DelayProfile, thetas: Sequence[floa
 # ------------------------------------------------------------ row operator
 
 
-def _rowconv(fn_name: str, x: torch.Tensor, K: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+def _rowconv(adjoint: bool, x: torch.Tensor, K: torch.Tensor, out=None, stream=None,
+             path: str = "auto") -> torch.Tensor:
     L = _lib.lib()
     if x.dtype != torch.float32 or K.dtype != torch.float32:
         raise ValueError("row convolution works on float32 maps and kernels")
@@ -256,20 +288,35 @@ def _rowconv(fn_name: str, x: torch.Tensor, K: torch.Tensor, out=None, stream=No
     K = K.contiguous()
     if out is None:
         out = torch.empty_like(x)
+    else:
+        if squeeze and out.dim() == 2:
+            out = out.unsqueeze(0)
+        if out.dtype != torch.float32 or out.shape != x.shape or not out.is_contiguous() \
+                or out.device != x.device:
+            raise ValueError(f"out must be a contiguous float32 tensor of shape {tuple(x.shape)}")
+        # the kernels read x rows after writing out rows: in-place is not supported
+        xs, xe = x.data_ptr(), x.data_ptr() + x.numel() * 4
+        os_, oe = out.data_ptr(), out.data_ptr() + out.numel() * 4
+        if xs < oe and os_ < xe:
+            raise ValueError("out must not overlap the input maps")
     B, nz, nx = x.shape
-    _lib.check(getattr(L, fn_name)(_lib.ptr(x), _lib.ptr(K), _lib.ptr(out), B, nz, nx,
-                                   int(K.shape[1]), _lib.stream_handle(stream)))
+    if path not in _lib.ROWCONV_PATHS:
+        raise ValueError(f"path must be one of {sorted(_lib.ROWCONV_PATHS)}, got {path!r}")
+    _lib.check(L.tidas_rowconv_f32(_lib.ptr(x), _lib.ptr(K), _lib.ptr(out), B, nz, nx, int(K.shape[1]),
+                                   int(adjoint), _lib.ROWCONV_PATHS[path], _lib.stream_handle(stream)))
     return out[0] if squeeze else out
 
 
-def tidas_rowconv(g: torch.Tensor, K: torch.Tensor, out=None, stream=None) -> torch.Tensor:
-    """K6 forward: y[b,i,x] = sum_k K[i,k] g[b,i,x+k-H] (zero outside)."""
-    return _rowconv("tidas_rowconv_fwd_f32", g, K, out, stream)
+def tidas_rowconv(g: torch.Tensor, K: torch.Tensor, out=None, stream=None, path: str = "auto") -> torch.Tensor:
+    """K6 forward: y[b,i,x] = sum_k K[i,k] g[b,i,x+k-H] (zero outside).
+    ``path``: "auto" (tensor cores when the shape fits), "tensor" or "simt"."""
+    return _rowconv(False, g, K, out, stream, path)
 
 
-def tidas_rowconv_adjoint(y: torch.Tensor, K: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+def tidas_rowconv_adjoint(y: torch.Tensor, K: torch.Tensor, out=None, stream=None,
+                          path: str = "auto") -> torch.Tensor:
     """K7 adjoint: g[b,i,x] = sum_k K[i,k] y[b,i,x-k+H]."""
-    return _rowconv("tidas_rowconv_adj_f32", y, K, out, stream)
+    return _rowconv(True, y, K, out, stream, path)
 
 
 def lateral_psfs(depths, taps: int, dx: float, *, n_el: int, pitch: float, fs: float, c: float,

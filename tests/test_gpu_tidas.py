@@ -60,29 +60,34 @@ def test_rowconv_cfg4_map_size_and_adjoint_identity(rng):
 # the 64-output block), short and full-width kernels. Tolerance: 2e-6 relative
 # L2 vs the float64 oracle (the split drops the lo*lo term and truncates lo,
 # ~2^-21 relative per product).
-@pytest.mark.parametrize("kernel", ["tc1", "2p"])  # 128-map blocks (default) / 64 maps x 2 phases
 @pytest.mark.parametrize("shape", [(128, 3, 256), (40, 5, 96), (33, 2, 32), (200, 3, 1024), (257, 2, 64)])
 @pytest.mark.parametrize("taps", [129, 31, 1])
-def test_rowconv_tensor_core_path_vs_oracle(shape, taps, kernel, rng, monkeypatch):
-    if kernel == "2p":
-        monkeypatch.setenv("TIDAS_ROWCONV_TC", "2p")
+def test_rowconv_tensor_core_path_vs_oracle(shape, taps, rng):
     B, nz, nx = shape
     g = sparse_maps(rng, B, nz, nx, 0.2)
     K = rng.standard_normal((nz, taps)).astype(np.float32)
     Kd, gd = torch.as_tensor(K).to(DEV), torch.as_tensor(g).to(DEV)
-    y = tb.tidas_rowconv(gd, Kd).cpu().numpy()
+    y = tb.tidas_rowconv(gd, Kd, path="tensor").cpu().numpy()
     assert od.rel_l2(y, ot.rowconv_fwd(g, K)) < 2e-6
-    a = tb.tidas_rowconv_adjoint(gd, Kd).cpu().numpy()
+    a = tb.tidas_rowconv_adjoint(gd, Kd, path="tensor").cpu().numpy()
     assert od.rel_l2(a, ot.rowconv_adj(g, K)) < 2e-6
 
 
-def test_rowconv_tensor_core_matches_cuda_core_path(rng, monkeypatch):
+def test_rowconv_tensor_path_rejects_small_batches(rng):
+    g = torch.zeros((8, 2, 64), device=DEV)
+    K = torch.zeros((2, 129), device=DEV)
+    with pytest.raises(NotImplementedError):
+        tb.tidas_rowconv(g, K, path="tensor")
+    with pytest.raises(ValueError):
+        tb.tidas_rowconv(g, K, out=g)  # in place is rejected
+
+
+def test_rowconv_tensor_core_matches_cuda_core_path(rng):
     B, nz, nx, T = 96, 16, 512, 129
     g = torch.as_tensor(sparse_maps(rng, B, nz, nx, 0.05)).to(DEV)
     K = torch.as_tensor(rng.standard_normal((nz, T)).astype(np.float32) / 8).to(DEV)
-    y_tc, a_tc = tb.tidas_rowconv(g, K), tb.tidas_rowconv_adjoint(g, K)
-    monkeypatch.setenv("TIDAS_ROWCONV_PATH", "simt")
-    y_s, a_s = tb.tidas_rowconv(g, K), tb.tidas_rowconv_adjoint(g, K)
+    y_tc, a_tc = tb.tidas_rowconv(g, K, path="tensor"), tb.tidas_rowconv_adjoint(g, K, path="tensor")
+    y_s, a_s = tb.tidas_rowconv(g, K, path="simt"), tb.tidas_rowconv_adjoint(g, K, path="simt")
     for u, v in ((y_tc, y_s), (a_tc, a_s)):
         assert (torch.linalg.norm((u - v).double()) / torch.linalg.norm(v.double())).item() < 2e-6
 

@@ -292,3 +292,36 @@ def test_oracle_line_metrics_golden(ref_vectors):
         om.width_at_half_max(-np.ones(8), 1.0)
     with pytest.raises(ValueError):
         om.width_at_half_max(np.linspace(0, 1, 8), 1.0)  # maximum at the edge
+
+
+# ---- round 2: the north-star imaging mode pinned to the reference's primitives
+
+
+def pw_frame_r2(seed):
+    """The seeded cfg2 speckle frame of make_golden_r2.py (float32-rounded)."""
+    from tests.setups import CFG2
+    rng = np.random.default_rng(int(seed))
+    sx, sz, a = osim.speckle(rng, CFG2["n_scat"], CFG2["region_x"], CFG2["region_z"])
+    rf = osim.synthesize(sx, sz, a, n_el=CFG2["n_el"], pitch=CFG2["pitch"], fs=CFG2["fs"], c=CFG2["c"],
+                         f0=CFG2["f0"], fbw=CFG2["fbw"], n_samples=CFG2["n_samples"], tx=("plane", 0.0))
+    return rf.astype(np.float32).astype(np.float64)
+
+
+def test_oracle_plane_wave_hann_gather_vs_reference_primitives():
+    """0-degree plane wave + pixel-centred Hann F#1.5 at 256 cfg2 pixels: the
+    oracle's analytic gather equals the reference's own composition (Hann weight x
+    das._delay_samples summed, metrics.envelope, np.interp at t* = 2z/c;
+    tests/golden/make_golden_r2.py)."""
+    from tests.setups import CFG2
+    g = dict(np.load(GOLDEN / "ref_vectors_r2.npz"))
+    rf = pw_frame_r2(g["PW_seed"])
+    A = od.analytic_signal(rf)[None]
+    xg, zg = np.linspace(*CFG2["x"], CFG2["nx"]), np.linspace(*CFG2["z"], CFG2["nz"])
+    got = []
+    for iz, ix in zip(g["PW_iz"], g["PW_ix"]):
+        x, z = xg[ix], zg[iz]
+        ts = geom.plane_wave_expected_arrival(np.array([[x]]), np.array([[z]]), 0.0, CFG2["n_el"],
+                                              CFG2["pitch"], CFG2["c"])[None]
+        got.append(od.das_image_vectorized(A, CFG2["fs"], 0.0, [x], [z], CFG2["pitch"], CFG2["c"], ts,
+                                           CFG2["f_number"])[0, 0])
+    assert _rel_to_max(got, g["PW_values"]) < 1e-12

@@ -49,12 +49,10 @@ def make_rf(name, c):
         a = rng.standard_normal((F, S))
         if c.get("n_bright"):
             a[:, c["n_scat"]:] = 20.0  # bright point targets
-    dt = torch.float64 if c["dtype"] == torch.float64 else torch.float32
-    rf = tb.synthesize_batch(sx, sz, a, angles=c["angles"], n_el=c["n_el"], pitch=c["pitch"], fs=c["fs"],
-                             c=1540.0, f0=c["f0"], fbw=c["fbw"], n_samples=c["N"], dtype=dt)
-    if c["dtype"] == torch.int16:
-        rf = torch.clamp(torch.round(rf * (1000.0 / rf.std())), -32768, 32767).to(torch.int16)
-    return rf
+    # cfg5: simulated in float32, each frame scaled to std 1000, rounded, clipped (library quantiser)
+    return tb.synthesize_batch(sx, sz, a, angles=c["angles"], n_el=c["n_el"], pitch=c["pitch"], fs=c["fs"],
+                               c=1540.0, f0=c["f0"], fbw=c["fbw"], n_samples=c["N"], dtype=c["dtype"],
+                               target_std=1000.0)
 
 
 def run_configs(names, steps=10, warmup=3, echo=False):
