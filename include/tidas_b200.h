@@ -170,6 +170,25 @@ int tidas_rowconv_f32(const float* in, const float* K, float* out, int64_t batch
                       int32_t nx, int32_t taps, int32_t adjoint, int32_t path, void* stream);
 
 /*
+ * K5 — per-depth tiDAS row kernels (north star (c), float64):
+ *   psf[i][k] = DAS pixel (0-degree plane wave, Hann F#, envelope) at
+ *               ((k - H) dx, depths[i]) of the echo of a unit scatterer at
+ *               (0, depths[i]) (simulate.py:193-259 model, one scatterer)
+ *   theta[i]  = <psf[r], psf[i]> / <psf[r], psf[r]>, r = centre row of i's block of
+ *               `neighbourhood` rows (0 if the denominator is 0)
+ *   K[i][k]   = (float) theta[i] psf[r][k]
+ * depths: double[nz] (device); psf: double[nz][taps] (device scratch, also an
+ * output); K: float[nz][taps]; theta: double[nz] (may be NULL). n_samples even.
+ * Nearest reference: estimate_theta_aligned (tidas.py:286-314) and
+ * theta_row_aligned (tidas.py:464-490), generalised from the axial profile to
+ * the lateral PSF row.
+ */
+int tidas_build_row_kernels(const double* depths, int32_t nz, int32_t taps, double dx, int32_t n_el,
+                            double pitch, double fs, double c, double f0, double fbw, double f_number,
+                            int32_t n_samples, int32_t neighbourhood, double* psf, float* K,
+                            double* theta, void* stream);
+
+/*
  * RF synthesis (simulate.py:193-259 model), for seeded inputs:
  *   out[f][a][e][k] += sum_s w_se pulse(k/fs - tau_se),
  *   tau_se = t_tx[f][a][s] + hypot(x_s - x_e, z_s) / c,  w_se = amp_s (z_s / r_se if spreading)

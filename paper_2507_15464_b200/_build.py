@@ -15,7 +15,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtidas_b200.so"
-SOURCES = ["api.cu", "analytic.cu", "das.cu", "rowconv.cu", "rowconv_tc1.cu", "tidas_ops.cu", "simulate.cu", "sweep.cu", "metrics.cu"]
+SOURCES = ["api.cu", "analytic.cu", "das.cu", "rowconv.cu", "rowconv_tc1.cu", "rowkernels.cu", "tidas_ops.cu", "simulate.cu", "sweep.cu", "metrics.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-ftz=true",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]

@@ -59,6 +59,8 @@ SIGNATURES = {
     "tidas_line_sidelobes": ([_P, C.c_int, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P], C.c_int),
     "tidas_synthesize": ([_P, _P, _P, _P, _I32, _I32, _I32, _I32, _D, _D, _D, _D, _D, _I32,
                           _I32, _P, C.c_int, _P], C.c_int),
+    "tidas_build_row_kernels": ([_P, _I32, _I32, _D, _I32, _D, _D, _D, _D, _D, _D, _I32, _I32, _P, _P, _P, _P],
+                                C.c_int),
     "tidas_frame_std": ([_P, C.c_int, _I64, _I64, _P, _P], C.c_int),
     "tidas_quantize_i16": ([_P, C.c_int, _I64, _I64, _P, _D, _P, _P], C.c_int),
 }

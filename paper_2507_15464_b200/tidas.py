@@ -31,7 +31,7 @@ from . import imaging
 from .das import Trace, _count, _delayed_sums_dev, _to_dev, _window_read
 from .geometry import ApertureRule, DelayProfile, ProbeConfig, rx_aperture, rx_delay_profile
 from .metrics import fwhm, window_bounds
-from .simulate import RfFrame, ScattererSet, synthesize_frame, tx_arrival_times, synthesize_batch
+from .simulate import RfFrame, ScattererSet, synthesize_frame, tx_arrival_times
 
 __all__ = ["TimeWindow", "ThetaMatrix", "fwhm_window", "window_signals", "estimate_theta_aligned",
            "tidas_psf", "theta_row_aligned", "tidas_line", "build_row_kernels", "lateral_psfs",
@@ -319,52 +319,48 @@ def tidas_rowconv_adjoint(y: torch.Tensor, K: torch.Tensor, out=None, stream=Non
     return _rowconv(True, y, K, out, stream, path)
 
 
+def _row_kernels_dev(depths, taps: int, dx: float, *, n_el: int, pitch: float, fs: float, c: float,
+                     f0: float, fbw: float, f_number: float, n_samples: int, neighbourhood: int):
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    z = torch.as_tensor(np.ascontiguousarray(np.asarray(depths, dtype=np.float64))).to(dev)
+    nz = int(z.numel())
+    psf = torch.empty((nz, taps), dtype=torch.float64, device=dev)
+    K = torch.empty((nz, taps), dtype=torch.float32, device=dev)
+    theta = torch.empty(nz, dtype=torch.float64, device=dev)
+    _lib.check(L.tidas_build_row_kernels(_lib.ptr(z), nz, int(taps), float(dx), int(n_el), float(pitch), float(fs),
+                                         float(c), float(f0), float(fbw), float(f_number), int(n_samples),
+                                         int(neighbourhood), _lib.ptr(psf), _lib.ptr(K), _lib.ptr(theta),
+                                         _lib.stream_handle()))
+    return K, theta, psf
+
+
 def lateral_psfs(depths, taps: int, dx: float, *, n_el: int, pitch: float, fs: float, c: float,
-                 f0: float, fbw: float, f_number: float, n_samples: int,
-                 prec: str = "f32", batch: int = 32) -> torch.Tensor:
-    """PSF[i][k]: DAS envelope (0-degree plane wave, Hann F#) at (xi_k, z_i) of the
-    RF of a unit scatterer at (0, z_i); xi_k = (k - H) dx. Runs the GPU synthesis
-    and the K1/K2 image path on batches of depth rows (each batch images its own
-    rows' depths; the diagonal is kept)."""
-    z = np.asarray(depths, dtype=float)
-    H = (taps - 1) // 2
-    xi = (np.arange(taps) - H) * dx
-    dt = torch.float32 if prec == "f32" else torch.float64
-    out = torch.empty((len(z), taps), dtype=dt, device=torch.device("cuda", torch.cuda.current_device()))
-    for i0 in range(0, len(z), batch):
-        zb = z[i0:i0 + batch]
-        B = len(zb)
-        rf = synthesize_batch(np.zeros((B, 1)), zb[:, None], np.ones((B, 1)), angles=[0.0], n_el=n_el,
-                              pitch=pitch, fs=fs, c=c, f0=f0, fbw=fbw, n_samples=n_samples, dtype=dt)
-        plan = imaging.plane_wave_plan(n_el=n_el, pitch=pitch, fs=fs, c=c, n_samples=n_samples,
-                                       x=xi, z=zb, angles=[0.0], f_number=f_number, prec=prec)
-        img = imaging.das_image(rf, plan)  # [B][B][taps]
-        idx = torch.arange(B, device=img.device)
-        out[i0:i0 + B] = img[idx, idx]
-    return out
+                 f0: float, fbw: float, f_number: float, n_samples: int) -> torch.Tensor:
+    """PSF[i][k] (float64): DAS envelope (0-degree plane wave, Hann F#) at
+    (xi_k, z_i) of the RF of a unit scatterer at (0, z_i); xi_k = (k - H) dx.
+    K5 (tidas_build_row_kernels): one CTA per depth row, the echo synthesised in
+    shared memory and its analytic signal evaluated at the tapped samples by the
+    exact discrete Hilbert kernel — no RF frame is materialised."""
+    return _row_kernels_dev(depths, taps, dx, n_el=n_el, pitch=pitch, fs=fs, c=c, f0=f0, fbw=fbw,
+                            f_number=f_number, n_samples=n_samples, neighbourhood=1)[2]
 
 
 def build_row_kernels(depths, taps: int, dx: float, *, n_el: int, pitch: float, fs: float,
                       c: float, f0: float, fbw: float, f_number: float, n_samples: int,
                       neighbourhood: int = 8) -> Tuple[torch.Tensor, torch.Tensor]:
-    """K5 — per-depth tiDAS row kernels K [nz][taps] (float32) and theta [nz].
+    """K5 — per-depth tiDAS row kernels K [nz][taps] (float32) and theta [nz] (float64).
 
     The lateral PSF of the reference row r(i) (centre of i's block of
     ``neighbourhood`` rows) is reused for every row of the block — the tiDAS
     time-invariance assumption (§tiDAS) applied laterally — and scaled by
     theta_i = <PSF_r, PSF_i> / <PSF_r, PSF_r>, the least-squares weight of
     estimate_theta_aligned (tidas.py:311-314); a zero denominator gives theta 0
-    (tidas.py:455-457, experiments.py:399-402)."""
-    psf = lateral_psfs(depths, taps, dx, n_el=n_el, pitch=pitch, fs=fs, c=c, f0=f0, fbw=fbw,
-                       f_number=f_number, n_samples=n_samples).double()
-    n = psf.shape[0]
-    i = torch.arange(n, device=psf.device)
-    r = torch.clamp((i // neighbourhood) * neighbourhood + neighbourhood // 2, max=n - 1)
-    a = psf[r]
-    den = (a * a).sum(1)
-    num = (a * psf).sum(1)
-    theta = torch.where(den > 0, num / torch.where(den > 0, den, torch.ones_like(den)), torch.zeros_like(den))
-    return (theta[:, None] * a).float().contiguous(), theta
+    (tidas.py:455-457, experiments.py:399-402). One C-ABI call
+    (tidas_build_row_kernels), two kernels, nothing on the host."""
+    K, theta, _ = _row_kernels_dev(depths, taps, dx, n_el=n_el, pitch=pitch, fs=fs, c=c, f0=f0, fbw=fbw,
+                                   f_number=f_number, n_samples=n_samples, neighbourhood=neighbourhood)
+    return K, theta
 
 
 def rasterize(xs, zs, amps, xgrid, zgrid) -> np.ndarray:

@@ -21,6 +21,7 @@ Sets (keys by prefix):
   a caller-supplied narrower support, the full-length path, and the
   short-segment ValueError.
 * ``WS_``: ``window_signals`` (tidas.py:150-168) nonzero bounds and row sums.
+* ``TA_``: ``estimate_theta_aligned`` at the inputs of ref test_tidas.py:338.
 
 Usage:  python tests/golden/make_golden_r2.py
 """
@@ -128,6 +129,18 @@ def crop_golden(T, vec) -> None:
     vec["WS_raises"] = np.array(raises)
 
 
+def theta_aligned_golden(T, vec) -> None:
+    """ref test_tidas.py:338 inputs: the reference's own theta (its brute-force
+    golden-section check resolves theta only to ~1e-8, see tests/test_gpu_refsuite.py)."""
+    from tidas.tidas import TimeWindow, estimate_theta_aligned
+    probe, rx, tx = T.ProbeConfig(), T.FNumber(1.0), T.Kossoff(0.6)
+    frame = T.synthesize_frame(T.ScattererSet.on_axis([28e-3]), 25e-3, probe, tx)
+    w = TimeWindow(T.expected_arrival_time((0.0, 28e-3), frame, probe), 1e-7)
+    fixed = T.rx_delay_profile(25e-3, T.rx_aperture(25e-3, rx, probe), probe)
+    true = T.rx_delay_profile(28e-3, T.rx_aperture(28e-3, rx, probe), probe)
+    vec["TA_theta28"] = estimate_theta_aligned(frame, w, fixed, true)
+
+
 def main() -> None:
     sys.path.insert(0, str(REF / "src"))
     import tidas as T
@@ -135,6 +148,7 @@ def main() -> None:
     pw_hann_golden(T, vec)
     no_head_zero_golden(T, vec)
     crop_golden(T, vec)
+    theta_aligned_golden(T, vec)
     np.savez_compressed(HERE / "ref_vectors_r2.npz", **vec)
     print("wrote", HERE / "ref_vectors_r2.npz")
 

@@ -8,7 +8,9 @@ pkg/tests/conftest.py (default probe, FNumber(1.0) receive, Kossoff(0.6)
 transmit, one scatterer at the 25 mm focus). Host-only cases live in
 tests/test_refsuite_host.py.
 
-Expected-red cases: none. Skipped: test_tidas.py:321 (DepthGrid belongs to
+Expected-red cases: none; one tolerance is restated — test_tidas.py:338
+asserts abs=1e-8 against a golden-section search that resolves theta only to
+~2e-8 (see test_estimate_theta_aligned). Skipped: test_tidas.py:321 (DepthGrid belongs to
 experiments.py, out of scope) and test_tidas.py:287's multi-process variant
 (``workers`` is accepted; the GPU batches all cells, asserted identical below).
 """
@@ -19,6 +21,7 @@ from scipy.optimize import minimize_scalar
 import paper_2507_15464_b200 as T
 from paper_2507_15464_b200.das import delayed_sum, target_delays
 from paper_2507_15464_b200.tidas import estimate_theta_aligned, theta_row_aligned
+from tests.conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 FS = 50e6
@@ -324,9 +327,21 @@ def test_estimate_theta_aligned(probe, tx, rx):  # ref: test_tidas.py:331, :338
     a = delayed_sum(frame, fixed.element_indices, fixed.delays).samples
     b = delayed_sum(frame, true.element_indices, true.delays).samples
     lo, hi = T.window_bounds(frame.n_samples, frame.t0, frame.sampling_frequency, w.center, w.half_width)
-    best = minimize_scalar(lambda v: float(np.sum((v * a[lo:hi] - b[lo:hi]) ** 2)), bracket=(0.0, 1.0, 4.0),
-                           method="golden", options={"xtol": 1e-12})
-    assert th == pytest.approx(best.x, abs=1e-8)
+    obj = lambda v: float(np.sum((v * a[lo:hi] - b[lo:hi]) ** 2))  # noqa: E731
+    best = minimize_scalar(obj, bracket=(0.0, 1.0, 4.0), method="golden", options={"xtol": 1e-12})
+    # The reference asserts abs=1e-8 against this golden-section search, but the
+    # search cannot resolve theta that finely: the objective is flat to float
+    # precision within sqrt(eps f* / <a,a>) of the minimiser (~2e-8 here; the
+    # reference's own search lands 5.4e-9 from its theta, ours 1.3e-8 on
+    # ulp-level different frames). Asserted instead: the search to its
+    # resolution, the closed-form minimiser to 1e-12, and the reference's own
+    # theta on these inputs (tests/golden/ref_vectors_r2.npz) to 1e-12.
+    aa, ab = float(a[lo:hi] @ a[lo:hi]), float(a[lo:hi] @ b[lo:hi])
+    res = np.sqrt(np.finfo(float).eps * obj(ab / aa) / aa)
+    assert th == pytest.approx(best.x, abs=max(1e-8, 2 * res))
+    assert th == pytest.approx(ab / aa, rel=1e-12)
+    g2 = dict(np.load(GOLDEN / "ref_vectors_r2.npz"))
+    assert th == pytest.approx(float(g2["TA_theta28"]), rel=1e-12)
 
 
 def test_tidas_line_contracts(probe, rx, tx, focal, focal_window):  # ref: test_tidas.py:359, :365, :377, :388

@@ -141,13 +141,14 @@ def test_lateral_psfs_and_row_kernels_cfg1():
     dx = x[1] - x[0]
     kw = _psf_case(cfg, z, 129, dx)
     sub = z[::16]
-    got = tb.lateral_psfs(sub, 129, dx, **kw).double().cpu().numpy()
+    got = tb.lateral_psfs(sub, 129, dx, **kw).cpu().numpy()
     ref = ot.lateral_psfs(sub, 129, dx, **kw)
-    assert od.rel_l2(got, ref) < 1e-5
+    # K5 is float64 end to end (exact discrete Hilbert kernel instead of the FFT)
+    assert got.dtype == np.float64 and od.rel_l2(got, ref) < 1e-10
     K, th = tb.build_row_kernels(sub, 129, dx, neighbourhood=4, **kw)
     Kref, thref = ot.build_row_kernels_from_psfs(ref, 4)
-    assert od.rel_l2(K.double().cpu().numpy(), Kref) < 1e-5
-    np.testing.assert_allclose(th.cpu().numpy(), thref, rtol=1e-4)
+    assert K.dtype == torch.float32 and od.rel_l2(K.double().cpu().numpy(), Kref) < 1e-7
+    np.testing.assert_allclose(th.cpu().numpy(), thref, rtol=1e-9)
 
 
 def test_cfg1_das_vs_tidas_image_error_matches_oracle():
