@@ -9,7 +9,10 @@ reference's index-gathered, worker-count-invariant sweeps
 from __future__ import annotations
 
 import os
-from typing import Optional, Tuple
+import socket
+import subprocess
+import sys
+from typing import Optional, Sequence, Tuple
 
 import torch
 import torch.distributed as dist
@@ -28,6 +31,26 @@ def env_rank_world() -> Tuple[int, int, int]:
     """(rank, world_size, local_rank) from the torchrun environment (1 process if unset)."""
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(n: int, script: str, argv: Sequence[str], env: Optional[dict] = None) -> int:
+    """Run ``script argv`` as ``n`` ranks on this node under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) and return its exit code —
+    what ``bench.py --gpus N`` does when it was not started by torchrun."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", script, *argv]
+    return subprocess.call(cmd, env=dict(os.environ, **(env or {})))
+
+
+def needs_relaunch(requested: int) -> bool:
+    """True when N > 1 ranks were asked for but this process is not one of them."""
+    return requested > 1 and "WORLD_SIZE" not in os.environ
 
 
 def init(backend: Optional[str] = None) -> Tuple[int, int]:

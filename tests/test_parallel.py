@@ -93,3 +93,20 @@ def test_pipelined_gather_two_ranks(n_local, sub):
     for r in (0, 1):
         assert res[r][0] == want
         assert res[r][1] == chunks
+
+
+def test_relaunch_spawns_ranks_like_bench():
+    """``bench.py --gpus N`` outside torchrun re-launches itself as N ranks
+    (parallel.relaunch over torch.distributed.run, 127.0.0.1): the same path,
+    on gloo, with the bench's pipelined and padded gathers."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    script = Path(__file__).resolve().parent / "spawn_worker.py"
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(script), "2"], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert lines == [{"world": 2, "ok": True}]
+
