@@ -41,7 +41,7 @@ constexpr int TMEM_COLS = 512;
 constexpr int B_ROWS = 2 * NOUT;         // 64: hi rows 0-31, lo rows 32-63
 constexpr int B_ATOM = B_ROWS * 128;     // 8 KB per K-atom of B
 constexpr int B_BYTES = CHB * B_ATOM;    // 40 KB per row buffer
-constexpr int NTHREADS = 512;            // 2 x 4 converters, 4 epilogue, MMA, TMA (+2 idle)
+constexpr int NTHREADS = 512;            // 2 x 4 converters, 4 epilogue, MMA, TMA, 2 B builders
 constexpr int CONV_SET1 = 12;
 constexpr int NSTAGE = 3;                // A stages (chunk pairs) in shared memory
 constexpr int A_STAGE = MAPS * 2 * CH * 4;   // 32 KB: [128 maps][2 chunks][32 inputs]
@@ -58,7 +58,7 @@ template <bool ADJ>
 __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                   const __grid_constant__ CUtensorMap omap,
                                                                   const float* __restrict__ K, int batch, int nz,
-                                                                  int nx, int T, int units_per) {
+                                                                  int nx, int T, int units_per, bool mm) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sbase = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   unsigned char* B_st = sbase;                        // [2 rows][40 KB]
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
   __shared__ __align__(8) uint64_t a_full[NSTAGE], a_empty[NSTAGE];
   __shared__ __align__(8) uint64_t c_full[RING], c_free[RING];
   __shared__ __align__(8) uint64_t mma_done[2], d_empty[2];
-  __shared__ __align__(8) uint64_t row_done[2];
+  __shared__ __align__(8) uint64_t row_done[2], b_full[2];
   __shared__ unsigned tmem_base_s;
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
       bar_init(&mma_done[k], 1);
       bar_init(&d_empty[k], 4);
       bar_init(&row_done[k], 1);
+      bar_init(&b_full[k], 2);  // one arrival per builder warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -126,26 +127,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
     long long gc = 0;   // chunks (all sets)
     long long gs0 = 0;  // TMA stage index of the segment's first pair
     for (int r = 0; r < rows_mine; ++r) {
-      const int row = row0 + r;
-      if (set == 0) {
-        // B[r & 1] was last read by the MMAs of row r - 2; the MMA warp's first
-        // block of a row waits on chunks converted by set 0 after this build
-        if (r >= 2) bar_wait(&row_done[r & 1], (unsigned)(((r - 2) >> 1) & 1));
-        unsigned char* Bb = B_st + (r & 1) * B_BYTES;
-        for (int e = quarter * 32 + lane; e < NOUT * KSPAN; e += 128) {
-          const int rr = e / KSPAN, u = e - rr * KSPAN;
-          const int k = u - rr;           // padded tap index in [0, 128]
-          const int kt = k - (HALO - H);  // original tap
-          float w = 0.f;
-          if (k >= 0 && k <= 2 * HALO && kt >= 0 && kt < T) w = K[(long long)row * T + (ADJ ? (T - 1 - kt) : kt)];
-          const unsigned h = tf32_rna(w);
-          const unsigned l = tf32_rna(w - __uint_as_float(h));
-          *reinterpret_cast<unsigned*>(Bb + b_offset(rr, u)) = h;
-          *reinterpret_cast<unsigned*>(Bb + b_offset(rr + NOUT, u)) = l;
-        }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        __syncwarp();
-      }
       for (int mb = mb_lo(r); mb < mb_hi(r); ++mb, gs0 += NSG) {
         for (int q = 0; q < NQ; ++q, ++gc) {
           if ((int)(gc & 1) != set) continue;
@@ -157,7 +138,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
           const long long gs = gs0 + (q >> 1);
           const int st = (int)(gs % NSTAGE), piece = q & 1;
           bar_wait(&a_full[st], (unsigned)((gs / NSTAGE) & 1));
-          const int L = 2 * m + piece;  // 128-byte line in the stage
+          // stage layout [128 maps][2 chunks][128 B] (256-byte DRAM runs per map) or,
+          // maps-major (mm), [2 chunks][128 maps][128 B]: then the 8 lanes of a
+          // quarter-warp read 8 consecutive lines = 8 distinct 16-byte bank groups
+          // (the map-major lines are 2 apart: 2-way bank conflicts)
+          const int L = mm ? piece * MAPS + m : 2 * m + piece;
           const unsigned char* rowp = A_st + st * A_STAGE + L * 128;
           float v[32];
 #pragma unroll
@@ -212,7 +197,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
             __syncwarp();
           }
-          const int L = 2 * lane + piece;
+          const int L = mm ? piece * 32 + lane : 2 * lane + piece;  // slab line (layout as the A stages)
           unsigned char* rowp = slab + L * 128;
 #pragma unroll
           for (int k = 0; k < 8; ++k)
@@ -222,13 +207,40 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
             // TMA clips maps >= batch and (odd n_xb) the unused second block
-            if (lane == 0) tma_store_4d(&omap, slab, j - piece, row, mb * MAPS + qw * 32);
+            if (lane == 0) {
+              if (mm) tma_store_4d(&omap, slab, mb * MAPS + qw * 32, j - piece, row);
+              else tma_store_4d(&omap, slab, j - piece, row, mb * MAPS + qw * 32);
+            }
           }
         }
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     __syncwarp();
+  } else if (warp == 10 || warp == 11) {
+    // ===== B builders: the row's 32 x 160 Toeplitz block as TF32 hi / lo K-atoms,
+    // one row ahead of the MMAs (double-buffered), off the converters' path
+    const int t0 = (warp - 10) * 32 + lane;
+    for (int r = 0; r < rows_mine; ++r) {
+      const int row = row0 + r;
+      // B[r & 1] was last read by the MMAs of row r - 2
+      if (r >= 2) bar_wait(&row_done[r & 1], (unsigned)(((r - 2) >> 1) & 1));
+      unsigned char* Bb = B_st + (r & 1) * B_BYTES;
+      for (int e = t0; e < NOUT * KSPAN; e += 64) {
+        const int rr = e / KSPAN, u = e - rr * KSPAN;
+        const int k = u - rr;           // padded tap index in [0, 128]
+        const int kt = k - (HALO - H);  // original tap
+        float w = 0.f;
+        if (k >= 0 && k <= 2 * HALO && kt >= 0 && kt < T) w = K[(long long)row * T + (ADJ ? (T - 1 - kt) : kt)];
+        const unsigned h = tf32_rna(w);
+        const unsigned l = tf32_rna(w - __uint_as_float(h));
+        *reinterpret_cast<unsigned*>(Bb + b_offset(rr, u)) = h;
+        *reinterpret_cast<unsigned*>(Bb + b_offset(rr + NOUT, u)) = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&b_full[r & 1]);
+    }
   } else if (warp == 9) {
     // ===== TMA producer: chunk pairs of 128 maps in consumption order
     if (lane == 0) {
@@ -241,7 +253,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
             if (gp >= NSTAGE) bar_wait(&a_empty[st], (unsigned)(((gp / NSTAGE) - 1) & 1));
             bar_expect_tx(&a_full[st], A_STAGE);
             // chunks 2u, 2u + 1 of the segment = input chunks 2u - 2, 2u - 1 of the row
-            tma_load_4d(A_st + st * A_STAGE, &tmap, 2 * u - 2, row, mb * MAPS, &a_full[st]);
+            if (mm) tma_load_4d(A_st + st * A_STAGE, &tmap, mb * MAPS, 2 * u - 2, row, &a_full[st]);
+            else tma_load_4d(A_st + st * A_STAGE, &tmap, 2 * u - 2, row, mb * MAPS, &a_full[st]);
           }
         }
       }
@@ -252,6 +265,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
     // N = 32 (A_lo B_hi) MMA into the block's 64 accumulator columns
     long long b = 0, g0 = 0;
     for (int r = 0; r < rows_mine; ++r) {
+      bar_wait(&b_full[r & 1], (unsigned)((r >> 1) & 1));  // the row's Toeplitz block is built
       const uint64_t db = smem_desc_sw128(su32(B_st + (r & 1) * B_BYTES));
       const unsigned b_lo32 = (unsigned)db, b_hi32 = (unsigned)(db >> 32);
       for (int mb = mb_lo(r); mb < mb_hi(r); ++mb, g0 += NQ) {
@@ -314,17 +328,31 @@ int launch_rowconv_tc1(const float* in, const float* K, float* out, int64_t batc
     TIDAS_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q));
     TIDAS_REQUIRE(q == cudaDriverEntryPointSuccess && encode, "cuTensorMapEncodeTiled unavailable");
   }
-  const cuuint64_t dims[4] = {(cuuint64_t)CH, (cuuint64_t)(nx / CH), (cuuint64_t)nz, (cuuint64_t)batch};
-  const cuuint64_t strides[3] = {(cuuint64_t)CH * 4, (cuuint64_t)nx * 4, (cuuint64_t)nz * nx * 4};
+  // view [row][chunk][map][32 inputs] of the [map][row][x] maps: a box of
+  // {32, 128 maps, 2 chunks, 1 row} lands as [2 chunks][128 maps][128 B]
+  // two views of the [map][row][x] maps, chosen per shape (measured on B200,
+  // DESIGN.md §4): map-major boxes {32, 2 chunks, 1 row, 128 maps} land as
+  // [128 maps][2 chunks][128 B] and read 256 contiguous bytes per map (large
+  // maps: cfg4 0.75 against 1.02 ms); maps-major boxes {32, 128 maps, 2
+  // chunks, 1 row} land as [2 chunks][128 maps][128 B], which the converter
+  // and epilogue warps access without bank conflicts (small maps, <= 1 MiB:
+  // cfg2 0.121 against 0.134 ms)
+  const bool mm = (int64_t)nz * nx <= (int64_t(1) << 18);
+  const cuuint64_t dims_mm[4] = {(cuuint64_t)CH, (cuuint64_t)batch, (cuuint64_t)(nx / CH), (cuuint64_t)nz};
+  const cuuint64_t strides_mm[3] = {(cuuint64_t)nz * nx * 4, (cuuint64_t)CH * 4, (cuuint64_t)nx * 4};
+  const cuuint64_t dims_m[4] = {(cuuint64_t)CH, (cuuint64_t)(nx / CH), (cuuint64_t)nz, (cuuint64_t)batch};
+  const cuuint64_t strides_m[3] = {(cuuint64_t)CH * 4, (cuuint64_t)nx * 4, (cuuint64_t)nz * nx * 4};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUtensorMap tmap, omap;
-  const cuuint32_t box[4] = {(cuuint32_t)CH, 2, 1, (cuuint32_t)MAPS};
-  if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in), dims, strides, box, estr,
+  const cuuint32_t box_mm[4] = {(cuuint32_t)CH, (cuuint32_t)MAPS, 2, 1}, box_m[4] = {(cuuint32_t)CH, 2, 1, (cuuint32_t)MAPS};
+  const cuuint32_t obox_mm[4] = {(cuuint32_t)CH, 32, 2, 1}, obox_m[4] = {(cuuint32_t)CH, 2, 1, 32};
+  if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in), mm ? dims_mm : dims_m,
+             mm ? strides_mm : strides_m, mm ? box_mm : box_m, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return TIDAS_EUNSUPPORTED;
-  const cuuint32_t obox[4] = {(cuuint32_t)CH, 2, 1, 32};
-  if (encode(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, dims, strides, obox, estr,
+  if (encode(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, mm ? dims_mm : dims_m, mm ? strides_mm : strides_m,
+             mm ? obox_mm : obox_m, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return TIDAS_EUNSUPPORTED;
@@ -334,7 +362,7 @@ int launch_rowconv_tc1(const float* in, const float* K, float* out, int64_t batc
   const long long units = (long long)nz * ((batch + MAPS - 1) / MAPS);
   const int units_per = (int)((units + sms - 1) / sms);
   const int grid = (int)((units + units_per - 1) / units_per);
-  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, (int)batch, nz, nx, T, units_per);
+  kern<<<grid, NTHREADS, smem, st>>>(tmap, omap, K, (int)batch, nz, nx, T, units_per, mm);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
 }

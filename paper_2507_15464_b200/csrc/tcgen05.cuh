@@ -47,18 +47,18 @@ __device__ unsigned long long g_rc_prof[16][16];  // [warp][wait site] cycles (l
 __device__ __forceinline__ void bar_expect_tx(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
-// 4-D view {32 inputs, nx / 32 chunks, nz rows, maps} of the maps tensor;
-// coordinates {0, chunk, row, map}; OOB -> zeros (loads) / clipped (stores)
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int chunk, int row, int m0,
+// 4-D tensor-map copies with coordinates {0, c1, c2, c3} (the caller's view
+// order); OOB -> zeros (loads) / clipped (stores)
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c1, int c2, int c3,
                                             uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
-      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(chunk), "r"(row), "r"(m0), "r"(su32(bar))
+      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
       : "memory");
 }
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int chunk, int row, int m0) {
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c1, int c2, int c3) {
   asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n"
-               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(su32(src)), "r"(0), "r"(chunk), "r"(row), "r"(m0)
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(su32(src)), "r"(0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
