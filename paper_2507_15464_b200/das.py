@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from . import imaging
-from .geometry import ApertureRule, ProbeConfig, element_positions, rx_aperture
+from .geometry import ApertureRule, ProbeConfig, aperture_half_counts, element_positions, rx_aperture
 from .simulate import RfFrame, tx_arrival_time, _focused_arrivals
 
 __all__ = ["Trace", "apply_fractional_delay", "delayed_sum", "das_psf", "das_value", "das_line",
@@ -178,24 +178,26 @@ def _window_bounds_arr(n, t0, fs, centers, half_width):
 
 def _pixels(frame: RfFrame, xs: np.ndarray, zs: np.ndarray, config: ProbeConfig,
             rx_rule: ApertureRule, envelope_half_width: Optional[float]) -> np.ndarray:
-    """DAS values of pixels (xs[p], zs[p]) of one frame, reference semantics."""
+    """DAS values of pixels (xs[p], zs[p]) of one frame, reference semantics.
+
+    Host geometry is vectorised over the pixels (the same float operations as
+    rx_aperture / target_delays per pixel, das.py:126-132, geometry.py:188-199)."""
     fs, c, t0 = frame.sampling_frequency, config.sound_speed, frame.t0
     n_el, N = frame.traces.shape
     half = n_el // 2
     P = len(zs)
     t_star = _focused_arrivals(xs, zs, frame.tx_focus_depth, frame.aperture, config) + zs / c
-    aps = [rx_aperture(z, rx_rule, config) for z in zs]
-    ap_half = np.array([len(a) // 2 for a in aps], dtype=np.int32)
+    ap_half = aperture_half_counts(zs, rx_rule, config).astype(np.int32)
     _count(int(np.sum(2 * ap_half)))
-    # per-pixel shifts (host, O(P x aperture)) for validation + the precondition
+    # per-pixel receive shifts [P][T] over the array-centred aperture, padded taps
+    # (beyond 2 * ap_half) point at a real row with shift 0 and are masked out
     T = int(2 * ap_half.max())
-    rows = np.zeros((P, T), np.int64)
-    shifts = np.zeros((P, T))
-    for p, (a, x, z) in enumerate(zip(aps, xs, zs)):
-        rows[p, :len(a)] = a + half
-        sh = target_delays((x, z), a, config) * fs
-        shifts[p, :len(a)] = sh
-        rows[p, len(a):] = half  # padding taps with zero weight (shift 0 on a real row)
+    j = np.arange(T)[None, :]
+    live = j < 2 * ap_half[:, None]
+    idx = np.where(live, j - ap_half[:, None], 0)
+    el_x = (idx + 0.5) * config.pitch
+    shifts = np.where(live, (zs[:, None] - np.hypot(xs[:, None] - el_x, zs[:, None])) / c * fs, 0.0)
+    rows = (idx + half).astype(np.int64)
     _check_shifts(shifts, N)
     x_d = _to_dev(np.asarray(frame.traces, float))
     if envelope_half_width is not None:
@@ -230,17 +232,13 @@ def _gather_exact(sup: np.ndarray, rows: np.ndarray, shifts: np.ndarray, counts,
     """SURVEY Appendix B.1 precondition: for every used channel with shift s,
     m = floor/ceil(s): m < 0 needs first_nonzero >= -m (no wrapped head sample),
     m >= 0 needs last_nonzero <= N - m - 2 (no wrapped tail sample)."""
-    for p in range(rows.shape[0]):
-        used = rows[p, : counts[p]]
-        first, last = sup[used, 0], sup[used, 1]
-        live = first >= 0
-        mlo = np.floor(shifts[p, : counts[p]])
-        mhi = np.ceil(shifts[p, : counts[p]])
-        if np.any(live & (mlo < 0) & (first < -mlo)):
-            return False
-        if np.any(live & (mhi >= 0) & (last > N - mhi - 2)):
-            return False
-    return True
+    used = np.arange(rows.shape[1])[None, :] < np.asarray(counts)[:, None]
+    first, last = sup[rows, 0], sup[rows, 1]
+    live = used & (first >= 0)
+    mlo, mhi = np.floor(shifts), np.ceil(shifts)
+    if np.any(live & (mlo < 0) & (first < -mlo)):
+        return False
+    return not np.any(live & (mhi >= 0) & (last > N - mhi - 2))
 
 
 def _interp_rows(env: torch.Tensor, pos: np.ndarray) -> np.ndarray:

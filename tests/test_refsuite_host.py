@@ -292,3 +292,15 @@ def test_frame_persistence(tmp_path):  # ref: test_simulate.py:193-225 (host fra
     bp.write_bytes(bp.read_bytes()[:-8])
     with pytest.raises(ValueError):
         T.load_frame(tmp_path / "frame_2.5mm")
+
+
+def test_vectorised_aperture_half_counts_equal_per_depth(probe):
+    """das_value / das_line compute every pixel's aperture at once
+    (geometry.aperture_half_counts); it must equal rx_aperture depth by depth."""
+    from paper_2507_15464_b200.geometry import aperture_half_count, aperture_half_counts
+    z = np.linspace(1e-6, 0.06, 1500)
+    for rule in (T.FNumber(1.0), T.FNumber(1.5), T.Kossoff(0.6), T.FixedCount(64), T.FixedCount(7)):
+        assert np.array_equal(aperture_half_counts(z, rule, probe),
+                              [aperture_half_count(v, rule, probe) for v in z])
+    with pytest.raises(TypeError):
+        aperture_half_counts(z, object(), probe)

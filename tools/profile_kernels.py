@@ -34,10 +34,15 @@ gen = torch.Generator(device="cuda").manual_seed(1)
 maps = (torch.rand((args.maps, 2048, 1024), device="cuda", generator=gen) < 0.02).float()
 K = torch.randn((2048, 129), device="cuda", generator=gen)
 y = torch.empty_like(maps)
+z4 = np.linspace(5e-3, 45e-3, 2048)
+dx4 = 38.4e-3 / 1023
+pk = dict(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"], f0=cfg["f0"], fbw=cfg["fbw"],
+          f_number=cfg["f_number"], n_samples=cfg["n_samples"])
 torch.cuda.synchronize()
 for _ in range(args.iters):
     tb.rf_analytic(rf, "f32", out=an)
     tb.das_from_analytic(an, plan, out=img)
     tb.tidas_rowconv(maps, K, out=y)
+    tb.build_row_kernels(z4, 129, dx4, neighbourhood=8, **pk)  # K5 at cfg4
 torch.cuda.synchronize()
 print("ok", float(img.sum()), float(y.abs().sum()))
