@@ -21,9 +21,11 @@
 //   H(x)[p] = sum_n x[n] h[(p - n) mod N],  h[m] = (2 / N) cot(pi m / N) (m odd), 0 (m even),
 // which equals IFFT(FFT(x) * -i sgn(k)) exactly — so no FFT and no frame
 // buffer: a depth row costs ~(channels in aperture) x taps x 3 x (pulse length)
-// FP64 FMAs against a [N] cot table in shared memory. A warp images one
-// lateral tap (lanes over channels, warp-shuffle channel sum).
+// FP64 FMAs against a [N] cot table in shared memory. Lanes own lateral taps,
+// warps stride over the channels, partial sums meet in shared memory.
 #include <math.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -31,9 +33,10 @@ namespace tidas {
 
 constexpr int K5_THREADS = 256;
 constexpr int K5_PMAX = 64;  // pulse samples per channel (8 sigma fs + 3 <= 64)
+constexpr int K5_GROUPS = 5;  // lateral taps per CTA: up to 5 x 32 = 160
 
 struct K5Params {
-  int nz, taps, n_el, N;
+  int nz, taps, n_el, N, table;
   double dx, pitch, fs, c, f0, sigma, f_number;
 };
 
@@ -41,7 +44,7 @@ __global__ void __launch_bounds__(K5_THREADS) row_psf_kernel(K5Params p, const d
                                                              double* __restrict__ psf) {
   extern __shared__ __align__(16) unsigned char k5_smem[];
   double* htab = reinterpret_cast<double*>(k5_smem);  // [N]
-  double* pulse = htab + p.N;                          // [n_el][K5_PMAX]
+  double* pulse = htab + p.table;                      // [n_el][K5_PMAX]
   int* n0 = reinterpret_cast<int*>(pulse + (size_t)p.n_el * K5_PMAX);  // [n_el] first sample
   int* len = n0 + p.n_el;                                              // [n_el] pulse length
   const int row = blockIdx.x;
@@ -78,7 +81,8 @@ __global__ void __launch_bounds__(K5_THREADS) row_psf_kernel(K5Params p, const d
   }
   __syncthreads();
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = K5_THREADS / 32;
   const int H = (p.taps - 1) / 2;
   const double a = z / (2.0 * p.f_number);
   const double tstar = (0.0 * 0.0 + z * 1.0 + 0.0) / p.c + z / p.c;  // plane_wave_arrivals_kernel, angle 0
@@ -86,11 +90,22 @@ __global__ void __launch_bounds__(K5_THREADS) row_psf_kernel(K5Params p, const d
   const bool valid = pos >= 0.0 && pos <= (double)(N - 1);
   const int k0 = valid ? (int)floor(pos) : 0;
   const double f = valid ? pos - floor(pos) : 0.0;
-  for (int k = warp; k < p.taps; k += nwarps) {
-    const double xi = (double)(k - H) * p.dx;
-    double c0r = 0.0, c0i = 0.0, c1r = 0.0, c1i = 0.0;
-    for (int e = lane; e < p.n_el && valid; e += 32) {
-      const double xe = ((double)(e - p.n_el / 2) + 0.5) * p.pitch;
+  // lanes own lateral taps (k = lane + 32 g), warps stride over the channels:
+  // the pulse sample x_e[n] is a broadcast and the Hilbert-table reads of
+  // neighbouring taps hit neighbouring entries (no bank conflicts); the warps'
+  // partial sums meet in shared memory
+  double acc[K5_GROUPS][4];
+#pragma unroll
+  for (int g = 0; g < K5_GROUPS; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0;
+  for (int e = warp; e < p.n_el && valid; e += NW) {
+    const double xe = ((double)(e - p.n_el / 2) + 0.5) * p.pitch;
+    const double* x = pulse + (size_t)e * K5_PMAX;
+    const int b = n0[e], L = len[e];
+#pragma unroll
+    for (int g = 0; g < K5_GROUPS; ++g) {
+      const int k = lane + 32 * g;
+      if (k >= p.taps) break;
+      const double xi = (double)(k - H) * p.dx;
       const double d = xe - xi;
       if (!(fabs(d) < a)) continue;
       const double w = 0.5 * (1.0 + cos(M_PI * d / a));
@@ -99,41 +114,52 @@ __global__ void __launch_bounds__(K5_THREADS) row_psf_kernel(K5Params p, const d
       double m, mu;
       if (fabs(s - nearest) < 1e-9) { m = nearest; mu = 0.0; }
       else { m = floor(s); mu = s - m; }
-      const double* x = pulse + (size_t)e * K5_PMAX;
-      const int b = n0[e], L = len[e];
-      // analytic samples at q = k0 - m - 1 + t, t = 0, 1, 2 (mod N)
-      double ar[3], ai[3];
+      // analytic samples at q_t = k0 - m - 1 + t, t = 0, 1, 2 (mod N): real part
+      // = the pulse sample, imaginary part = sum_n x[n] h[(q_t - b - n) mod N];
+      // the three sums share a sliding window of three table entries, so each
+      // pulse sample costs one table read and three FMAs
+      double ar[3], ai[3] = {0.0, 0.0, 0.0};
+      int q0 = (k0 - (int)m - 1) % N;
+      q0 = q0 < 0 ? q0 + N : q0;
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
-        int q = (k0 - (int)m - 1 + t) % N;
-        q = q < 0 ? q + N : q;
-        const int rel = q - b;
-        ar[t] = (rel >= 0 && rel < L) ? x[rel] : 0.0;
-        double hs = 0.0;
-        int idx = q - b;  // (q - n) for n = b, b + 1, ...: idx decreases by 1
-        idx %= N;
-        idx = idx < 0 ? idx + N : idx;
-        for (int n = 0; n < L; ++n) {
-          hs = fma(x[n], htab[idx], hs);
-          idx = idx == 0 ? N - 1 : idx - 1;
-        }
-        ai[t] = hs;
+        const int q = q0 + t >= N ? q0 + t - N : q0 + t;
+        ar[t] = (q - b >= 0 && q - b < L) ? x[q - b] : 0.0;
+      }
+      int j = (q0 - b) % N;
+      j = j < 0 ? j + N : j;
+      double h0 = htab[j], h1 = htab[j + 1 >= N ? j + 1 - N : j + 1], h2 = htab[j + 2 >= N ? j + 2 - N : j + 2];
+      for (int n = 0; n < L; ++n) {
+        const double xn = x[n];
+        ai[0] = fma(xn, h0, ai[0]);
+        ai[1] = fma(xn, h1, ai[1]);
+        ai[2] = fma(xn, h2, ai[2]);
+        h2 = h1;
+        h1 = h0;
+        j = j == 0 ? N - 1 : j - 1;
+        h0 = htab[j];
       }
       // C(k0) = (1 - mu) A[k0 - m] + mu A[k0 - m - 1]; C(k0 + 1) = (1 - mu) A[k0 - m + 1] + mu A[k0 - m]
-      c0r += w * ((1.0 - mu) * ar[1] + mu * ar[0]);
-      c0i += w * ((1.0 - mu) * ai[1] + mu * ai[0]);
-      c1r += w * ((1.0 - mu) * ar[2] + mu * ar[1]);
-      c1i += w * ((1.0 - mu) * ai[2] + mu * ai[1]);
+      acc[g][0] += w * ((1.0 - mu) * ar[1] + mu * ar[0]);
+      acc[g][1] += w * ((1.0 - mu) * ai[1] + mu * ai[0]);
+      acc[g][2] += w * ((1.0 - mu) * ar[2] + mu * ar[1]);
+      acc[g][3] += w * ((1.0 - mu) * ai[2] + mu * ai[1]);
     }
+  }
+  __syncthreads();  // the Hilbert table is no longer read: reuse it for the partial sums
+  double* part = htab;  // [NW][K5_GROUPS * 32][4]
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c0r += __shfl_xor_sync(0xffffffffu, c0r, o);
-      c0i += __shfl_xor_sync(0xffffffffu, c0i, o);
-      c1r += __shfl_xor_sync(0xffffffffu, c1r, o);
-      c1i += __shfl_xor_sync(0xffffffffu, c1i, o);
+  for (int g = 0; g < K5_GROUPS; ++g)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) part[((size_t)warp * K5_GROUPS * 32 + g * 32 + lane) * 4 + c] = acc[g][c];
+  __syncthreads();
+  for (int k = threadIdx.x; k < p.taps; k += blockDim.x) {
+    double c0r = 0.0, c0i = 0.0, c1r = 0.0, c1i = 0.0;
+    for (int w = 0; w < NW; ++w) {  // fixed order: deterministic
+      const double* q = part + ((size_t)w * K5_GROUPS * 32 + k) * 4;
+      c0r += q[0]; c0i += q[1]; c1r += q[2]; c1i += q[3];
     }
-    if (lane == 0)
-      psf[(size_t)row * p.taps + k] = valid ? (1.0 - f) * hypot(c0r, c0i) + f * hypot(c1r, c1i) : 0.0;
+    psf[(size_t)row * p.taps + k] = valid ? (1.0 - f) * hypot(c0r, c0i) + f * hypot(c1r, c1i) : 0.0;
   }
 }
 
@@ -168,7 +194,8 @@ extern "C" int tidas_build_row_kernels(const double* depths, int32_t nz, int32_t
                                        double f_number, int32_t n_samples, int32_t neighbourhood, double* psf,
                                        float* K, double* theta, void* stream) {
   using namespace tidas;
-  TIDAS_REQUIRE(nz >= 0 && taps >= 1 && (taps & 1), "taps must be odd and positive");
+  TIDAS_REQUIRE(nz >= 0 && taps >= 1 && (taps & 1) && taps <= 32 * K5_GROUPS,
+                "taps must be odd and in [1, %d]", 32 * K5_GROUPS);
   TIDAS_REQUIRE(n_el >= 2 && n_el % 2 == 0 && n_el <= 1024, "n_el must be even, in [2, 1024]");
   TIDAS_REQUIRE(n_samples >= 4 && n_samples % 2 == 0 && n_samples <= 16384,
                 "n_samples must be even and in [4, 16384] (even-length Hilbert kernel)");
@@ -179,10 +206,12 @@ extern "C" int tidas_build_row_kernels(const double* depths, int32_t nz, int32_t
   TIDAS_REQUIRE(depths && psf && K, "null pointer");
   K5Params p;
   p.nz = nz; p.taps = taps; p.n_el = n_el; p.N = n_samples;
+  p.table = (int)std::max<int64_t>(n_samples, (int64_t)(K5_THREADS / 32) * K5_GROUPS * 32 * 4);
   p.dx = dx; p.pitch = pitch; p.fs = fs; p.c = c; p.f0 = f0; p.f_number = f_number;
   p.sigma = sqrt(2.0 * log(2.0)) / (M_PI * fbw * f0);  // simulate.py:139-153
   TIDAS_REQUIRE(8.0 * p.sigma * fs + 3.0 <= (double)K5_PMAX, "pulse longer than %d samples", K5_PMAX);
-  const size_t smem = sizeof(double) * ((size_t)n_samples + (size_t)n_el * K5_PMAX) + 2 * sizeof(int) * n_el;
+  // the Hilbert table region doubles as the warps' partial-sum buffer afterwards
+  const size_t smem = sizeof(double) * ((size_t)p.table + (size_t)n_el * K5_PMAX) + 2 * sizeof(int) * n_el;
   TIDAS_REQUIRE(smem <= 227 * 1024, "n_samples / n_el too large for the shared-memory row builder");
   cudaStream_t st = as_stream(stream);
   TIDAS_CUDA_CHECK(cudaFuncSetAttribute(row_psf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
