@@ -21,11 +21,15 @@ for row in rows[2:]:
         i = hdr.index(m)
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[i]]
         tot += float(row[i].replace(",", "")) * scale
-    key = "K1" if "analytic" in name else "K2" if "das_image" in name else None
+    key = "K1" if "analytic" in name else "K2" if "das_image" in name else \
+        "RC" if "rowconv_tc1_kernel<0>" in name else None
     if key and key not in res:
-        res[key] = tot / frames
+        res[key] = tot if key == "RC" else tot / frames
 out_d = {"das_pipeline_bytes_per_frame": res["K1"] + res["K2"], "K1_bytes_per_frame": res["K1"],
          "K2_bytes_per_frame": res["K2"], "frames_per_launch": frames,
          "source": f"{rep} (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)"}
+if "RC" in res:
+    out_d.update(rowconv_cfg4_bytes_per_launch=res["RC"], rowconv_cfg4_algorithmic_bytes_per_launch=256 * 2048 * 1024 * 8,
+                 rowconv_source=f"{rep}: rowconv_tc1_kernel<fwd>, 256 cfg4 maps")
 open(out, "w").write(json.dumps(out_d, indent=1) + "\n")
 print(out_d)
