@@ -32,6 +32,9 @@ __global__ void init_twiddles_kernel() {
   g_tw32[k] = make_float2((float)cs, (float)sn);
 }
 
+// x * scale, or x when the ingest scale is 1 (a compile-time choice)
+template <bool SCALED> __device__ __forceinline__ float scaled(float x, float scale) { return SCALED ? x * scale : x; }
+
 template <typename In> __device__ __forceinline__ double load_as_double(const In* p) {
   return (double)(*p);
 }
@@ -291,7 +294,7 @@ template <bool INV> __device__ __forceinline__ void dft64_pair_dif(float2 (&w)[3
   dft32<INV>(v);  // slot j: output 2 sig32(j) + h
 }
 
-template <typename In>
+template <typename In, bool SCALED, bool SUPPORT>
 __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                            cplx<float>* __restrict__ out, int64_t n_rows,
                                                            int32_t* __restrict__ support) {
@@ -324,14 +327,18 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
-    v[p].x *= scale;
-    v[p].y *= scale;
+    if (SCALED) {
+      v[p].x *= scale;
+      v[p].y *= scale;
+    }
     const int n = t + 64 * (hi + 2 * p);
-    if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
-    if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    if (SUPPORT) {
+      if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+      if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    }
   }
-  __syncthreads();  // first_nz / last_nz initialised
-  if (support) {
+  if (SUPPORT) {
+    __syncthreads();  // first_nz / last_nz initialised
     if (lo_a < N) atomicMin(&first_nz[0], lo_a);
     if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
     if (lo_b < N) atomicMin(&first_nz[1], lo_b);
@@ -404,11 +411,11 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     const int n = t + 64 * (2 * sig32(j) + hi);
-    float2 a; a.x = (float)load_as_double(src_a + n) * scale; a.y = v[j].x;
+    float2 a; a.x = scaled<SCALED>((float)load_as_double(src_a + n), scale); a.y = v[j].x;
     dst_a[n] = a;
-    if (has_b) { float2 b; b.x = (float)load_as_double(src_b + n) * scale; b.y = v[j].y; dst_b[n] = b; }
+    if (has_b) { float2 b; b.x = scaled<SCALED>((float)load_as_double(src_b + n), scale); b.y = v[j].y; dst_b[n] = b; }
   }
-  if (support) {
+  if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int c = 0; c < (has_b ? 2 : 1); ++c) {
@@ -521,7 +528,7 @@ template <bool INV> __device__ __forceinline__ void dft128_quad_dif(float2 (&y)[
   dft64_pair_dif<INV>(w, v, q1);  // slot j: output m'' = 2 sig32(j) + q1 of the half-length inverse
 }
 
-template <typename In>
+template <typename In, bool SCALED, bool SUPPORT>
 __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                                 cplx<float>* __restrict__ out, int64_t n_rows,
                                                                 int32_t* __restrict__ support) {
@@ -560,14 +567,18 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
-    v[p].x *= scale;
-    v[p].y *= scale;
+    if (SCALED) {
+      v[p].x *= scale;
+      v[p].y *= scale;
+    }
     const int n = n1 + 64 * (mq + 4 * p);
-    if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
-    if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    if (SUPPORT) {
+      if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+      if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    }
   }
-  __syncthreads();  // first_nz / last_nz initialised
-  if (support) {
+  if (SUPPORT) {
+    __syncthreads();  // first_nz / last_nz initialised
     if (lo_a < N) atomicMin(&first_nz[0], lo_a);
     if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
     if (lo_b < N) atomicMin(&first_nz[1], lo_b);
@@ -642,11 +653,11 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     const int n = n1 + 64 * (mq + 4 * sig32(j));
-    float2 a; a.x = (float)load_as_double(src_a + n) * scale; a.y = v[j].x;
+    float2 a; a.x = scaled<SCALED>((float)load_as_double(src_a + n), scale); a.y = v[j].x;
     dst_a[n] = a;
-    if (has_b) { float2 b; b.x = (float)load_as_double(src_b + n) * scale; b.y = v[j].y; dst_b[n] = b; }
+    if (has_b) { float2 b; b.x = scaled<SCALED>((float)load_as_double(src_b + n), scale); b.y = v[j].y; dst_b[n] = b; }
   }
-  if (support) {
+  if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int c = 0; c < (has_b ? 2 : 1); ++c) {
@@ -666,7 +677,7 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
 // 32-point DFTs in one thread's registers (the forward's output slots feed the
 // inverse DFT-32 by register renaming, no data movement). Pair roles: column
 // n1 = 16 warp + (lane & 15), h = lane >> 4; row roles: k2 = threadIdx.x.
-template <typename In>
+template <typename In, bool SCALED, bool SUPPORT>
 __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                             cplx<float>* __restrict__ out, int64_t n_rows,
                                                             int32_t* __restrict__ support) {
@@ -700,14 +711,18 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
-    v[p].x *= scale;
-    v[p].y *= scale;
+    if (SCALED) {
+      v[p].x *= scale;
+      v[p].y *= scale;
+    }
     const int n = n1 + 32 * (hi + 2 * p);
-    if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
-    if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    if (SUPPORT) {
+      if (v[p].x != 0.0f) { lo_a = min(lo_a, n); hi_a = max(hi_a, n); }
+      if (v[p].y != 0.0f) { lo_b = min(lo_b, n); hi_b = max(hi_b, n); }
+    }
   }
-  __syncthreads();
-  if (support) {
+  if (SUPPORT) {
+    __syncthreads();  // first_nz / last_nz initialised
     if (lo_a < N) atomicMin(&first_nz[0], lo_a);
     if (hi_a >= 0) atomicMax(&last_nz[0], hi_a);
     if (lo_b < N) atomicMin(&first_nz[1], lo_b);
@@ -779,11 +794,11 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     const int n = n1 + 32 * (2 * sig32(j) + hi);
-    float2 a; a.x = (float)load_as_double(src_a + n) * scale; a.y = v[j].x;
+    float2 a; a.x = scaled<SCALED>((float)load_as_double(src_a + n), scale); a.y = v[j].x;
     dst_a[n] = a;
-    if (has_b) { float2 b; b.x = (float)load_as_double(src_b + n) * scale; b.y = v[j].y; dst_b[n] = b; }
+    if (has_b) { float2 b; b.x = scaled<SCALED>((float)load_as_double(src_b + n), scale); b.y = v[j].y; dst_b[n] = b; }
   }
-  if (support) {
+  if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int c = 0; c < (has_b ? 2 : 1); ++c) {
@@ -964,6 +979,15 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// the register four-step kernels are instantiated with / without the ingest
+// scale multiply and the support scan (only the drop-in's exactness check asks
+// for it), so the throughput path carries neither
+template <typename K>
+static K pick4(K plain, K support_only, K scaled_only, K both, double scale, const int32_t* support) {
+  const bool sc = scale != 1.0, su = support != nullptr;
+  return sc ? (su ? both : scaled_only) : (su ? support_only : plain);
+}
+
 template <typename R, typename In>
 static int launch_analytic(const In* rf, int64_t stride, double scale, void* out, int64_t n_rows,
                            int32_t N, int32_t* support, double shift, cudaStream_t st) {
@@ -988,12 +1012,15 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
       // four-step FFTs in registers (analytic_r2048_kernel / analytic_r32_kernel /
       // analytic_r8192_kernel); other lengths take the shared-memory Stockham kernel
       if (!delay && logN == 11) {
-        TIDAS_CUDA_CHECK(launch_pdl(analytic_r2048_kernel<In>, dim3((unsigned)((n_rows + 1) / 2)), dim3(64), 0, st,
+        auto k2 = pick4(analytic_r2048_kernel<In, false, false>, analytic_r2048_kernel<In, false, true>,
+                        analytic_r2048_kernel<In, true, false>, analytic_r2048_kernel<In, true, true>, scale, support);
+        TIDAS_CUDA_CHECK(launch_pdl(k2, dim3((unsigned)((n_rows + 1) / 2)), dim3(64), 0, st,
                                     rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
         return TIDAS_OK;
       }
       if (!delay && logN == 13) {
-        auto kr = analytic_r8192_kernel<In>;
+        auto kr = pick4(analytic_r8192_kernel<In, false, false>, analytic_r8192_kernel<In, false, true>,
+                        analytic_r8192_kernel<In, true, false>, analytic_r8192_kernel<In, true, true>, scale, support);
         const size_t smem8 = sizeof(float2) * 128 * 65;
         TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8));
         TIDAS_CUDA_CHECK(launch_pdl(kr, dim3((unsigned)((n_rows + 1) / 2)), dim3(256), smem8, st, rf, stride,
@@ -1001,7 +1028,9 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         return TIDAS_OK;
       }
       if (!delay && logN == 12) {
-        TIDAS_CUDA_CHECK(launch_pdl(analytic_r32_kernel<In>, dim3((unsigned)((n_rows + 1) / 2)), dim3(128), 0, st,
+        auto k4 = pick4(analytic_r32_kernel<In, false, false>, analytic_r32_kernel<In, false, true>,
+                        analytic_r32_kernel<In, true, false>, analytic_r32_kernel<In, true, true>, scale, support);
+        TIDAS_CUDA_CHECK(launch_pdl(k4, dim3((unsigned)((n_rows + 1) / 2)), dim3(128), 0, st,
                                     rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
         return TIDAS_OK;
       }
