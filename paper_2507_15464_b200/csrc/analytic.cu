@@ -370,13 +370,14 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
 #pragma unroll
   for (int p = 0; p < 32; ++p) v[p] = S[t * LP + hi + 2 * p];
   dft64_pair_dit<false>(v, w, h);  // w[2 i (+1)] = X[t + 64 k1], k1 = 16 h + i (+ 32)
-  // ---- Hilbert multiplier -i sgn(k) / N: slot 2 i positive, 2 i + 1 negative frequencies
+  // ---- Hilbert multiplier -i sgn(k): slot 2 i positive, 2 i + 1 negative frequencies
+  // (the 1 / N = 2^-12 is folded into the inverse twiddles below: exact)
   const float invN = 1.0f / (float)N;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const float2 p0 = w[2 * i], p1 = w[2 * i + 1];
-    w[2 * i] = make_float2(p0.y * invN, -p0.x * invN);
-    w[2 * i + 1] = make_float2(-p1.y * invN, p1.x * invN);
+    w[2 * i] = make_float2(p0.y, -p0.x);
+    w[2 * i + 1] = make_float2(-p1.y, p1.x);
   }
   if (t == 0 && !h) { w[0] = make_float2(0.0f, 0.0f); w[1] = make_float2(0.0f, 0.0f); }  // DC, Nyquist
   // ---- inverse, stage 1: over k1 for fixed k2 = t; slot j: Z[t, n2], n2 = 2 sig32(j) + h
@@ -386,7 +387,10 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
 #pragma unroll
     for (int c = 0; c < 4; ++c) { wa[c] = g_tw32[((t * (2 * c + hi)) & 4095) << SH]; wa[c].y = -wa[c].y; }
 #pragma unroll
-    for (int b = 0; b < 8; ++b) { wb[b] = g_tw32[((8 * t * b) & 4095) << SH]; wb[b].y = -wb[b].y; }
+    for (int b = 0; b < 8; ++b) {
+      wb[b] = g_tw32[((8 * t * b) & 4095) << SH];
+      wb[b] = make_float2(wb[b].x * invN, -wb[b].y * invN);
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int e2 = 2 * sig32(j);  // n2 = e2 + h: a = (e2 & 7) + h, b = e2 >> 3
@@ -612,13 +616,14 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
 #pragma unroll
   for (int p = 0; p < 32; ++p) v[p] = S[k2r * LP1 + hi + 2 * p];
   dft64_pair_dit<false>(v, y, h);  // y[2 i (+1)] = X[k2 + 128 k1], k1 = 16 h + i (+ 32)
-  // ---- Hilbert multiplier -i sgn(k) / N: slot 2 i positive, 2 i + 1 negative frequencies
+  // ---- Hilbert multiplier -i sgn(k): slot 2 i positive, 2 i + 1 negative frequencies
+  // (1 / N = 2^-13 folded into the inverse twiddles below: exact)
   const float invN = 1.0f / (float)N;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const float2 p0 = y[2 * i], p1 = y[2 * i + 1];
-    y[2 * i] = make_float2(p0.y * invN, -p0.x * invN);
-    y[2 * i + 1] = make_float2(-p1.y * invN, p1.x * invN);
+    y[2 * i] = make_float2(p0.y, -p0.x);
+    y[2 * i + 1] = make_float2(-p1.y, p1.x);
   }
   if (k2r == 0 && !h) { y[0] = make_float2(0.0f, 0.0f); y[1] = make_float2(0.0f, 0.0f); }  // DC, Nyquist
   // ---- inverse stage 1 (pairs): over k1 for fixed k2; slot j: Z[k2, n1], n1 = 2 sig32(j) + h
@@ -628,7 +633,10 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
 #pragma unroll
     for (int c = 0; c < 4; ++c) { wa[c] = g_tw32[((k2r * (2 * c + hi)) & 8191) << SH]; wa[c].y = -wa[c].y; }
 #pragma unroll
-    for (int b = 0; b < 8; ++b) { wb[b] = g_tw32[((8 * k2r * b) & 8191) << SH]; wb[b].y = -wb[b].y; }
+    for (int b = 0; b < 8; ++b) {
+      wb[b] = g_tw32[((8 * k2r * b) & 8191) << SH];
+      wb[b] = make_float2(wb[b].x * invN, -wb[b].y * invN);
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int e2 = 2 * sig32(j);
@@ -760,7 +768,7 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
 #pragma unroll
   for (int k1 = 0; k1 < 32; ++k1) {
     const float2 p0 = v[sig32_inv(k1)];
-    float2 r = (k1 < 16) ? make_float2(p0.y * invN, -p0.x * invN) : make_float2(-p0.y * invN, p0.x * invN);
+    float2 r = (k1 < 16) ? make_float2(p0.y, -p0.x) : make_float2(-p0.y, p0.x);  // 1 / N in the twiddles
     if (k2r == 0 && (k1 == 0 || k1 == 16)) r = make_float2(0.0f, 0.0f);  // DC, Nyquist
     w[k1] = r;
   }
@@ -771,7 +779,10 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
 #pragma unroll
     for (int a = 0; a < 8; ++a) { wa[a] = g_tw32[((k2r * a) & 2047) << SH]; wa[a].y = -wa[a].y; }
 #pragma unroll
-    for (int b = 0; b < 4; ++b) { wb[b] = g_tw32[((8 * k2r * b) & 2047) << SH]; wb[b].y = -wb[b].y; }
+    for (int b = 0; b < 4; ++b) {
+      wb[b] = g_tw32[((8 * k2r * b) & 2047) << SH];
+      wb[b] = make_float2(wb[b].x * invN, -wb[b].y * invN);
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int e = sig32(j), a = e & 7, b = e >> 3;

@@ -175,6 +175,8 @@ def das_from_analytic(analytic: torch.Tensor, plan: DasPlan, out=None, stream=No
                          f"[F][{plan.n_angles}][{plan.n_el}][{plan.n_samples}]")
     if not analytic.is_contiguous():
         raise ValueError("analytic must be contiguous [F][A][E][N]")
+    if analytic.device != plan.x.device:
+        raise ValueError(f"analytic is on {analytic.device} but the plan lives on {plan.x.device}")
     dt = _COMPLEX[plan.prec_code] if plan.out == "iq" else _REAL[plan.prec_code]
     if out is None:
         out = torch.empty((F, plan.nz, plan.nx), dtype=dt, device=analytic.device)
@@ -222,6 +224,8 @@ def das_image(rf: torch.Tensor, plan: DasPlan, *, scale: float = 1.0, out=None,
     if rf.dim() != 4:
         raise ValueError("rf must be [F][A][E][N] or [F][E][N]")
     F = int(rf.shape[0])
+    if rf.device != plan.x.device:
+        raise ValueError(f"rf is on {rf.device} but the plan lives on {plan.x.device}")
     if tuple(rf.shape[1:]) != (plan.n_angles, plan.n_el, plan.n_samples):
         raise ValueError(f"rf shape {tuple(rf.shape)} does not match the plan "
                          f"[F][{plan.n_angles}][{plan.n_el}][{plan.n_samples}]")

@@ -277,8 +277,8 @@ def _rowconv(adjoint: bool, x: torch.Tensor, K: torch.Tensor, out=None, stream=N
     L = _lib.lib()
     if x.dtype != torch.float32 or K.dtype != torch.float32:
         raise ValueError("row convolution works on float32 maps and kernels")
-    if not (x.is_cuda and K.is_cuda):
-        raise ValueError("maps and kernels must be CUDA tensors")
+    if not (x.is_cuda and K.is_cuda) or x.device != K.device:
+        raise ValueError("maps and kernels must be CUDA tensors on one device")
     squeeze = x.dim() == 2
     if squeeze:
         x = x.unsqueeze(0)
