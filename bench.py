@@ -56,6 +56,18 @@ CFG4 = dict(nz=2048, nx=1024, z=(5e-3, 45e-3), x=(-19.2e-3, 19.2e-3), taps=129, 
             neighbourhood=8)
 WORKLOAD = ("cfg2 (BASELINE.json configs[1]): DAS, 128 ch x 4096 f32 RF -> 512x256 px, Hann F#1.5, "
             "linear interp, envelope")
+DATA = ("synthetic: seeded speckle (2000 N(0,1) scatterers over 40x40 mm per frame), 0-degree plane-wave RF "
+        "(single-scattering model of simulate.py:193-259), float32")
+
+
+def workload_config(frames_per_gpu: int, world: int) -> dict:
+    """The workload identity both arms report (the reference arm's CPU sample
+    is described in its cpu_baseline)."""
+    return {"workload": WORKLOAD, "frames_per_step_per_gpu": frames_per_gpu,
+            "parallelism": f"frame-sharded dp{world}",
+            "l2": f"inputs larger than L2 ({frames_per_gpu * 2} MiB RF per GPU per step)",
+            "gather": (f"NCCL all_gather of images inside the step, pipelined per {SUB} frames with the DAS of "
+                       f"the next {SUB}") if world > 1 else "none"}
 
 
 def cpu_model() -> str:
@@ -235,10 +247,11 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded speckle, 2000 scatterers, 0-degree plane wave (oracle simulator)",
-            "config": {"workload": WORKLOAD, "device": "cpu (host cores, oracle port of the reference algorithm)"},
+            "data": DATA, "config": workload_config(args.frames, args.gpus),
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": "port",
-                             "sample": sample, "cpu_model": cpu_model()},
+                             "sample": sample + " (oracle simulator frame rounded to float32; float64 arithmetic; "
+                                                "host cores, oracle port of the reference algorithm)",
+                             "cpu_model": cpu_model()},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -574,12 +587,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic: seeded speckle (2000 N(0,1) scatterers over 40x40 mm per frame), "
-                    "0-degree plane-wave RF simulated on the device (float32)",
-            "config": {"workload": WORKLOAD, "frames_per_step_per_gpu": F, "parallelism": f"frame-sharded dp{world}",
-                       "l2": f"inputs larger than L2 ({F * 2} MiB RF per GPU per step)",
-                       "gather": f"NCCL all_gather of images inside the step, pipelined per {SUB} frames with the "
-                                 f"DAS of the next {SUB}" if world > 1 else "none"},
+            "data": DATA, "config": workload_config(F, world),
             "roofline": roofline, "k2_smem_roofline": k2_smem, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_e2e": launches_e2e, "clocks": clocks,
             "tidas": tidas, "theta_error_sweep": sweep, "other_configs": others,
