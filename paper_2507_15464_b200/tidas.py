@@ -215,7 +215,61 @@ def theta_row_aligned(reference_depth: float, depth_grid, config: ProbeConfig,
                       tx_focus_depth: Optional[float] = None, spreading: bool = True,
                       method: str = "linear", workers: int = 1) -> np.ndarray:
     """Aligned-window thetas of one reference profile over ``depth_grid``
-    (tidas.py:464-490). ``workers`` is accepted; the device runs the cells."""
+    (tidas.py:464-490). ``workers`` is accepted; the device runs the cells.
+
+    Every cell's frame is synthesised on the device and stays there (no host
+    round trip); the cells' window dot products are collected on the device and
+    read back once. Failed cells are NaN with the reference's warning."""
+    if method != "linear":  # spectral shifts: the per-cell reference composition
+        return _theta_row_per_cell(reference_depth, depth_grid, config, tx_rule, rx_rule,
+                                   window_half_width=window_half_width, tx_focus_depth=tx_focus_depth,
+                                   spreading=spreading, method=method)
+    from .simulate import _synthesize_frame_device
+    L = _lib.lib()
+    focus = reference_depth if tx_focus_depth is None else tx_focus_depth
+    fixed = rx_delay_profile(reference_depth, rx_aperture(reference_depth, rx_rule, config), config)
+    fs, c = config.sampling_frequency, config.sound_speed
+    depths = np.asarray(depth_grid, dtype=float)
+    dots = torch.zeros((len(depths), 2), dtype=torch.float64, device=_das._device())
+    failed = {}
+    keep = []  # argument tensors stay referenced until their launch is enqueued
+    for q, z in enumerate(depths):
+        try:
+            x_d, aperture = _synthesize_frame_device(ScattererSet.on_axis([z]), focus, config, tx_rule,
+                                                     spreading=spreading)
+            n = int(x_d.shape[1])
+            arrival = float(tx_arrival_times(np.array([z]), focus, aperture, config)[0]) + z / c
+            true = rx_delay_profile(z, rx_aperture(z, rx_rule, config), config)
+            half = x_d.shape[0] // 2
+            prof = []
+            for p_ in (fixed, true):
+                rows = (np.asarray(p_.element_indices).astype(np.int64) + half)[None, :]
+                prof.append(_delayed_sums_dev(x_d, rows, (np.asarray(p_.delays, float) * fs)[None, :]))
+            _count(len(fixed) + len(true))
+            lo, hi = window_bounds(n, 0.0, fs, arrival, window_half_width)
+            if hi <= lo:
+                raise ValueError("window lies outside the frame support")
+            lo_d = _to_dev(np.array([lo], np.int32), torch.int32)
+            hi_d = _to_dev(np.array([hi], np.int32), torch.int32)
+            _lib.check(L.tidas_window_dots_f64(_lib.ptr(prof[0]), _lib.ptr(prof[1]), n, _lib.ptr(lo_d),
+                                               _lib.ptr(hi_d), 1, _lib.ptr(dots[q]), _lib.stream_handle()))
+            keep.append((x_d, prof, lo_d, hi_d))
+        except (ValueError, ZeroDivisionError) as exc:
+            failed[q] = exc
+    ab, aa = dots.cpu().numpy().T  # the one device -> host read of the row
+    out = np.full(len(depths), np.nan)
+    for q, z in enumerate(depths):
+        if q not in failed and aa[q] == 0.0:
+            failed[q] = ZeroDivisionError("window missed the echo: fixed-profile sum has no energy")
+        if q in failed:
+            log.warning("aligned cell (ref %.4f, target %.4f): %s", reference_depth, z, failed[q])
+        else:
+            out[q] = float(ab[q]) / float(aa[q])
+    return out
+
+
+def _theta_row_per_cell(reference_depth, depth_grid, config, tx_rule, rx_rule, *, window_half_width,
+                        tx_focus_depth, spreading, method):
     focus = reference_depth if tx_focus_depth is None else tx_focus_depth
     fixed = rx_delay_profile(reference_depth, rx_aperture(reference_depth, rx_rule, config), config)
     out = []
