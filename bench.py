@@ -372,9 +372,26 @@ def main():
 
     for _ in range(args.warmup):
         step()
+
+    # the same step, untimed, around the timed region keeps the GPU under its
+    # load long enough for nvidia-smi's 100 ms samples; the step count is agreed
+    # over the ranks (every rank must issue the same collectives)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        step()
+    barrier()
+    per_step = max_over_ranks((time.perf_counter() - t0) / 3)
+    n_pre, n_post = max(1, int(0.6 / per_step)), max(1, int(0.4 / per_step))
     with Clocks(local) as clk:
+        for _ in range(n_pre):
+            step()
         ms_step = timed(step, args.steps, 0)
+        for _ in range(n_post):
+            step()
+        torch.cuda.synchronize()
     clocks = clk.summary()
+    clocks["window"] = "sampled every 100 ms over 0.6 s of the same step, the timed steps, and 0.4 s more"
     value = total_frames / (ms_step / 1e3)
     n_launch = -(-len(frames) // per_launch)
     launches = args.steps * n_launch * 2
