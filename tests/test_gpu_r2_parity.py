@@ -183,3 +183,34 @@ def test_das_image_rejects_mismatched_buffers():
     with pytest.raises(ValueError):
         tb.rf_analytic(rf, "f32", support=torch.zeros((3, 2), dtype=torch.int32, device=DEV))
     assert tb.das_image(rf, plan).shape == (2, 16, 16)
+
+
+# ------------------------------------------- guard bands around new outputs
+
+
+def test_k5_and_quantiser_write_only_their_outputs():
+    """Sentinel-filled guard bands after every output of tidas_build_row_kernels
+    and tidas_quantize_i16 stay untouched (odd sizes; compute-sanitizer is not
+    available on this pool)."""
+    from paper_2507_15464_b200 import _lib
+    L = _lib.lib()
+    nz, taps, pad = 7, 33, 64
+    z = torch.as_tensor(np.linspace(6e-3, 14e-3, nz), dtype=torch.float64, device=DEV)
+    psf = torch.full((nz * taps + pad,), 7.0, dtype=torch.float64, device=DEV)
+    K = torch.full((nz * taps + pad,), 7.0, dtype=torch.float32, device=DEV)
+    th = torch.full((nz + pad,), 7.0, dtype=torch.float64, device=DEV)
+    _lib.check(L.tidas_build_row_kernels(_lib.ptr(z), nz, taps, 0.15e-3, 32, 0.3e-3, 40e6, 1540.0, 5e6, 0.6, 1.5,
+                                         1024, 3, _lib.ptr(psf), _lib.ptr(K), _lib.ptr(th), _lib.stream_handle()))
+    torch.cuda.synchronize()
+    for buf, n in ((psf, nz * taps), (K, nz * taps), (th, nz)):
+        assert bool((buf[n:] == 7.0).all()) and bool(torch.isfinite(buf[:n]).all())
+    F, n = 3, 1001
+    x = torch.randn((F, n), dtype=torch.float32, device=DEV) * 50
+    out = torch.full((F * n + pad,), 1234, dtype=torch.int16, device=DEV)
+    std = tb.frame_std(x)
+    _lib.check(L.tidas_quantize_i16(_lib.ptr(x), _lib.F32, F, n, _lib.ptr(std), 1000.0, _lib.ptr(out),
+                                    _lib.stream_handle()))
+    torch.cuda.synchronize()
+    assert bool((out[F * n:] == 1234).all())
+    assert np.array_equal(out[:F * n].cpu().numpy().reshape(F, n),
+                          np.stack([osim.quantize_int16(r.astype(np.float64), 1000.0) for r in x.cpu().numpy()]))
