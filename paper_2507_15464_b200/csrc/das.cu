@@ -45,10 +45,7 @@
 
 namespace tidas {
 
-constexpr int DAS_WMAX = 400;  // staged window capacity (samples) per frame
-constexpr int DAS_NBUF_DEFAULT = 4;  // channel windows in flight (producer lead)
-
-constexpr int DAS_WSTRIDE = DAS_WMAX + 2;  // per-frame window stride (elements, even)
+constexpr int DAS_WMAX = 400;  // staged window capacity (samples) per frame of the FP64 path
 
 struct DasParams {
   int F, A, E, N, nx, nz;
