@@ -233,6 +233,47 @@ template <bool INV> __device__ __forceinline__ float2 tw64(float2 v, int e) {
 __host__ __device__ constexpr int sig32(int j) { return (j >> 2) + 8 * (j & 3); }
 __host__ __device__ constexpr int sig32_inv(int k) { return 4 * (k & 7) + (k >> 3); }
 
+// T^e, e = 0..7, from one table twiddle T (products of depth <= 3: a few
+// ulps). The four-step twiddles W^(n1 k2) of every register kernel are powers
+// of two per-thread table entries, W^n1 and W^(8 n1), loaded with the RF row
+// at kernel entry — no table reads (and no load latency) between the stages.
+__device__ __forceinline__ void tw_powers8(float2 T, float2 (&P)[8]) {
+  P[0] = make_float2(1.0f, 0.0f);
+  P[1] = T;
+  P[2] = cmul(T, T);
+  P[3] = cmul(P[2], T);
+  P[4] = cmul(P[2], P[2]);
+  P[5] = cmul(P[4], T);
+  P[6] = cmul(P[4], P[2]);
+  P[7] = cmul(P[4], P[3]);
+}
+__device__ __forceinline__ float2 conj_scaled(float2 a, float s) { return make_float2(a.x * s, -a.y * s); }
+
+// Output rows: complex (input real part, Hilbert part), the real parts re-read
+// (L2) in batches of 8 slots so that 16 loads are in flight before the stores.
+template <typename In, bool SCALED, typename IDX>
+__device__ __forceinline__ void store_analytic_pair(const In* src_a, const In* src_b, bool has_b, float scale,
+                                                    const float2 (&v)[32], cplx<float>* dst_a, cplx<float>* dst_b,
+                                                    IDX idx) {
+#pragma unroll
+  for (int j0 = 0; j0 < 32; j0 += 8) {
+    float ra[8], rb[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int n = idx(j0 + q);
+      ra[q] = (float)load_as_double(src_a + n);
+      rb[q] = has_b ? (float)load_as_double(src_b + n) : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int n = idx(j0 + q);
+      float2 a; a.x = scaled<SCALED>(ra[q], scale); a.y = v[j0 + q].x;
+      dst_a[n] = a;
+      if (has_b) { float2 b; b.x = scaled<SCALED>(rb[q], scale); b.y = v[j0 + q].y; dst_b[n] = b; }
+    }
+  }
+}
+
 template <bool INV> __device__ __forceinline__ void dft32(float2 (&v)[32]) {
   // m = q + 4 p (q < 4, p < 8), k = r + 8 s (r < 8, s < 4)
 #pragma unroll
@@ -318,6 +359,7 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   float2 v[32], w[32];
+  const float2 T1 = g_tw32[t << SH], T8 = g_tw32[((8 * t) & 4095) << SH];  // W4096^t, W4096^(8 t)
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
     const int n = t + 64 * (hi + 2 * p);
@@ -347,11 +389,11 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   // ---- forward, stage 1: thread (t = n1, h); w[2 i (+1)] = Y[n1, k2], k2 = 16 h + i (+ 32)
   dft64_pair_dit<false>(v, w, h);
   {  // W4096^(n1 k2), k2 = 16 h + i + 32 u = a + 8 b: a = i & 7, b = 2 h + (i >> 3) + 4 u
-    float2 wa[8], wb[4];
+    float2 wa[8], wb[4], q[8];
+    tw_powers8(T1, wa);  // W^(t a)
+    tw_powers8(T8, q);   // W^(8 t e)
 #pragma unroll
-    for (int a = 0; a < 8; ++a) wa[a] = g_tw32[((t * a) & 4095) << SH];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) wb[c] = g_tw32[((8 * t * (2 * hi + (c & 1) + 4 * (c >> 1))) & 4095) << SH];
+    for (int c = 0; c < 4; ++c) wb[c] = csel(h, q[2 + (c & 1) + 4 * (c >> 1)], q[(c & 1) + 4 * (c >> 1)]);
 #pragma unroll
     for (int i = 0; i < 16; ++i)
 #pragma unroll
@@ -383,14 +425,13 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   // ---- inverse, stage 1: over k1 for fixed k2 = t; slot j: Z[t, n2], n2 = 2 sig32(j) + h
   dft64_pair_dif<true>(w, v, h);
   {  // W4096^-(k2 n2), n2 = 2 sig32(j) + h = a + 8 b
-    float2 wa[4], wb[8];
+    float2 wa[4], wb[8], q[8];
+    tw_powers8(T1, q);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) { wa[c] = g_tw32[((t * (2 * c + hi)) & 4095) << SH]; wa[c].y = -wa[c].y; }
+    for (int c = 0; c < 4; ++c) wa[c] = conj_scaled(csel(h, q[2 * c + 1], q[2 * c]), 1.0f);  // W^-(t (2 c + h))
+    tw_powers8(T8, wb);
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      wb[b] = g_tw32[((8 * t * b) & 4095) << SH];
-      wb[b] = make_float2(wb[b].x * invN, -wb[b].y * invN);
-    }
+    for (int b = 0; b < 8; ++b) wb[b] = conj_scaled(wb[b], invN);  // W^-(8 t b) / N
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int e2 = 2 * sig32(j);  // n2 = e2 + h: a = (e2 & 7) + h, b = e2 >> 3
@@ -409,16 +450,9 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
     w[2 * i + 1] = S[t * LP + 16 * hi + i + 32];
   }
   dft64_pair_dif<true>(w, v, h);  // slot j: x[t + 64 (2 sig32(j) + h)]
-  // real parts = the inputs, re-read (L2)
   cplx<float>* dst_a = out + ra * (int64_t)N;
-  cplx<float>* dst_b = dst_a + N;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int n = t + 64 * (2 * sig32(j) + hi);
-    float2 a; a.x = scaled<SCALED>((float)load_as_double(src_a + n), scale); a.y = v[j].x;
-    dst_a[n] = a;
-    if (has_b) { float2 b; b.x = scaled<SCALED>((float)load_as_double(src_b + n), scale); b.y = v[j].y; dst_b[n] = b; }
-  }
+  store_analytic_pair<In, SCALED>(src_a, src_b, has_b, scale, v, dst_a, dst_a + N,
+                                  [&](int j) { return t + 64 * (2 * sig32(j) + hi); });
   if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -562,6 +596,9 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   float2 v[32], y[32];
   const int mq = q0i + 2 * q1i;
+  // W8192^n1, W8192^(8 n1) (forward, quad roles); W8192^k2, W8192^(8 k2) (inverse, pair roles)
+  const float2 T1 = g_tw32[n1 << SH], T8 = g_tw32[((8 * n1) & 8191) << SH];
+  const float2 U1 = g_tw32[k2r << SH], U8 = g_tw32[((8 * k2r) & 8191) << SH];
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
     const int n = n1 + 64 * (mq + 4 * p);
@@ -591,11 +628,16 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   // ---- forward stage 1 (quads): y[4 i + 2 u + t] = Y[n1, k2], k2 = 16 q1 + 8 q0 + i + 32 u + 64 t
   dft128_quad_dit(v, y, q0, q1);
   {  // W8192^(n1 k2), k2 = a + 8 b: a = i, b = q0 + 2 q1 + 4 u + 8 t
-    float2 wa[8], wb[4];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) wa[a] = g_tw32[((n1 * a) & 8191) << SH];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) wb[c] = g_tw32[((8 * n1 * (mq + 4 * c)) & 8191) << SH];
+    float2 wa[8], wb[4], q[8];
+    tw_powers8(T1, wa);  // W^(n1 a)
+    tw_powers8(T8, q);   // W^(8 n1 e), e < 8
+    // W^(8 n1 (mq + 4 c)) = W^(8 n1 mq) * {1, T8^4, T8^8, T8^12}
+    const float2 base = csel(q1, csel(q0, q[3], q[2]), csel(q0, q[1], q[0]));
+    const float2 t32 = q[4], t64 = cmul(q[4], q[4]);
+    wb[0] = base;
+    wb[1] = cmul(base, t32);
+    wb[2] = cmul(base, t64);
+    wb[3] = cmul(base, cmul(t64, t32));
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -629,14 +671,13 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   // ---- inverse stage 1 (pairs): over k1 for fixed k2; slot j: Z[k2, n1], n1 = 2 sig32(j) + h
   dft64_pair_dif<true>(y, v, h);
   {  // W8192^-(k2 n1), n1 = 2 sig32(j) + h = a + 8 b
-    float2 wa[4], wb[8];
+    float2 wa[4], wb[8], q[8];
+    tw_powers8(U1, q);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) { wa[c] = g_tw32[((k2r * (2 * c + hi)) & 8191) << SH]; wa[c].y = -wa[c].y; }
+    for (int c = 0; c < 4; ++c) wa[c] = conj_scaled(csel(h, q[2 * c + 1], q[2 * c]), 1.0f);  // W^-(k2 (2 c + h))
+    tw_powers8(U8, wb);
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      wb[b] = g_tw32[((8 * k2r * b) & 8191) << SH];
-      wb[b] = make_float2(wb[b].x * invN, -wb[b].y * invN);
-    }
+    for (int b = 0; b < 8; ++b) wb[b] = conj_scaled(wb[b], invN);  // W^-(8 k2 b) / N
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int e2 = 2 * sig32(j);
@@ -657,14 +698,8 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
     }
   dft128_quad_dif<true>(y, v, q0, q1);  // slot j: x[n1 + 64 (q0 + 2 q1 + 4 sig32(j))]
   cplx<float>* dst_a = out + ra * (int64_t)N;
-  cplx<float>* dst_b = dst_a + N;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int n = n1 + 64 * (mq + 4 * sig32(j));
-    float2 a; a.x = scaled<SCALED>((float)load_as_double(src_a + n), scale); a.y = v[j].x;
-    dst_a[n] = a;
-    if (has_b) { float2 b; b.x = scaled<SCALED>((float)load_as_double(src_b + n), scale); b.y = v[j].y; dst_b[n] = b; }
-  }
+  store_analytic_pair<In, SCALED>(src_a, src_b, has_b, scale, v, dst_a, dst_a + N,
+                                  [&](int j) { return n1 + 64 * (mq + 4 * sig32(j)); });
   if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -710,6 +745,9 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   float2 v[32], w[32];
+  // W2048^n1, W2048^(8 n1) (forward, pair roles); W2048^k2, W2048^(8 k2) (inverse, row roles)
+  const float2 T1 = g_tw32[n1 << SH], T8 = g_tw32[((8 * n1) & 2047) << SH];
+  const float2 U1 = g_tw32[k2r << SH], U8 = g_tw32[((8 * k2r) & 2047) << SH];
 #pragma unroll
   for (int p = 0; p < 32; ++p) {
     const int n = n1 + 32 * (hi + 2 * p);
@@ -739,11 +777,11 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   // forward stage 1 (pairs): w[2 i + u] = Y[n1, k2], k2 = 16 h + i + 32 u
   dft64_pair_dit<false>(v, w, h);
   {  // W2048^(n1 k2), k2 = a + 8 b: a = i & 7, b = 2 h + (i >> 3) + 4 u
-    float2 wa[8], wb[4];
+    float2 wa[8], wb[4], q[8];
+    tw_powers8(T1, wa);  // W^(n1 a)
+    tw_powers8(T8, q);   // W^(8 n1 e)
 #pragma unroll
-    for (int a = 0; a < 8; ++a) wa[a] = g_tw32[((n1 * a) & 2047) << SH];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) wb[c] = g_tw32[((8 * n1 * (2 * hi + (c & 1) + 4 * (c >> 1))) & 2047) << SH];
+    for (int c = 0; c < 4; ++c) wb[c] = csel(h, q[2 + (c & 1) + 4 * (c >> 1)], q[(c & 1) + 4 * (c >> 1)]);
 #pragma unroll
     for (int i = 0; i < 16; ++i)
 #pragma unroll
@@ -775,14 +813,13 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   // inverse stage 1 (rows): slot j: Z[k2, n1 = sig32(j)]
   dft32<true>(w);
   {  // W2048^-(k2 n1), n1 = a + 8 b
-    float2 wa[8], wb[4];
+    float2 wa[8], wb[4], q[8];
+    tw_powers8(U1, wa);
 #pragma unroll
-    for (int a = 0; a < 8; ++a) { wa[a] = g_tw32[((k2r * a) & 2047) << SH]; wa[a].y = -wa[a].y; }
+    for (int a = 0; a < 8; ++a) wa[a] = conj_scaled(wa[a], 1.0f);  // W^-(k2 a)
+    tw_powers8(U8, q);
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      wb[b] = g_tw32[((8 * k2r * b) & 2047) << SH];
-      wb[b] = make_float2(wb[b].x * invN, -wb[b].y * invN);
-    }
+    for (int b = 0; b < 4; ++b) wb[b] = conj_scaled(q[b], invN);  // W^-(8 k2 b) / N
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int e = sig32(j), a = e & 7, b = e >> 3;
@@ -801,14 +838,8 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   }
   dft64_pair_dif<true>(w, v, h);  // slot j: x[n1 + 32 (2 sig32(j) + h)]
   cplx<float>* dst_a = out + ra * (int64_t)N;
-  cplx<float>* dst_b = dst_a + N;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int n = n1 + 32 * (2 * sig32(j) + hi);
-    float2 a; a.x = scaled<SCALED>((float)load_as_double(src_a + n), scale); a.y = v[j].x;
-    dst_a[n] = a;
-    if (has_b) { float2 b; b.x = scaled<SCALED>((float)load_as_double(src_b + n), scale); b.y = v[j].y; dst_b[n] = b; }
-  }
+  store_analytic_pair<In, SCALED>(src_a, src_b, has_b, scale, v, dst_a, dst_a + N,
+                                  [&](int j) { return n1 + 32 * (2 * sig32(j) + hi); });
   if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {

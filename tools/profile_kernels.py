@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--iters", type=int, default=1)
 ap.add_argument("--frames", type=int, default=8)
 ap.add_argument("--maps", type=int, default=32)
+ap.add_argument("--map-shape", default="2048x1024", help="depth x lateral of the row-operator maps (cfg2: 512x256)")
 args = ap.parse_args()
 
 cfg = CFG2
@@ -31,8 +32,9 @@ plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=
 an = torch.empty((F, 1, cfg["n_el"], cfg["n_samples"]), dtype=torch.complex64, device="cuda")
 img = torch.empty((F, cfg["nz"], cfg["nx"]), device="cuda")
 gen = torch.Generator(device="cuda").manual_seed(1)
-maps = (torch.rand((args.maps, 2048, 1024), device="cuda", generator=gen) < 0.02).float()
-K = torch.randn((2048, 129), device="cuda", generator=gen)
+mz, mx = (int(v) for v in args.map_shape.split("x"))
+maps = (torch.rand((args.maps, mz, mx), device="cuda", generator=gen) < 0.02).float()
+K = torch.randn((mz, 129), device="cuda", generator=gen)
 y = torch.empty_like(maps)
 z4 = np.linspace(5e-3, 45e-3, 2048)
 dx4 = 38.4e-3 / 1023
