@@ -182,6 +182,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_u32(unsigned bar) {
   asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+// a value the compiler keeps in a register instead of re-deriving it inside
+// the channel loop (shared-window bases otherwise cost ~10 uniform-datapath
+// instructions per channel: S2UR SR_CgaCtaId + address arithmetic)
+__device__ __forceinline__ unsigned pinned(unsigned x) {
+  unsigned r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+// one elected lane of the (converged) warp arrives on the barrier
+__device__ __forceinline__ void mbar_arrive_elected_u32(unsigned bar) {
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n @e mbarrier.arrive.shared.b64 _, [%0];\n}\n"
+               ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -435,11 +448,11 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
       // channels outside every lane's aperture skip the tap math (warp-uniform)
       const int wn_lo = __reduce_min_sync(0xffffffffu, active_px ? n_lo : INT_MAX);
       const int wn_hi = __reduce_max_sync(0xffffffffu, active_px ? n_hi : INT_MIN);
-      const unsigned full_u = smem_u32(&full[0]), empty_u = smem_u32(&empty[0]);
+      const unsigned full_u = pinned(smem_u32(&full[0])), empty_u = pinned(smem_u32(&empty[0]));
       const C* win_lane = win - s0;  // + buf * SLOT + (b * CPB + c) * WSTRIDE + j
       // U32: the same window addressed as a 32-bit shared-window offset (no generic-to-shared
       // conversion per channel); element e of buffer b at win_u32 + 8 (b * SLOT + e)
-      const unsigned win_u32 = smem_u32(win) - 8u * (unsigned)s0;
+      const unsigned win_u32 = pinned(smem_u32(win) - 8u * (unsigned)s0);
       for (int kb = 0; kb < n_blk; ++kb) {
         const unsigned g = g0 + kb;
         const int buf = (int)(g % DAS_NBUF);
@@ -501,7 +514,7 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
         }
         if (staged) {
           __syncwarp();
-          if (lane == 0) mbar_arrive_u32(empty_u + 8u * buf);
+          mbar_arrive_elected_u32(empty_u + 8u * buf);
         }
       }
       if (active_px && !FOLD_IQ) {
