@@ -71,9 +71,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
   __shared__ unsigned tmem_base_s;
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  RC_PROF_DECL
   const int n_mb = (batch + MAPS - 1) / MAPS;
   const int n_xb = nx / CH;                 // 32-output blocks per row (nx % 32 == 0)
-  const int NQ = n_xb + CHB - 1;            // chunks per (row, map block) segment
+  // only the row's own input chunks 0 .. n_xb - 1 are loaded, converted and
+  // multiplied: the halo chunks outside the row are zeros, so block j's MMAs
+  // cover input chunks max(0, j - 2) .. min(n_xb - 1, j + 2) (cfg2-size rows:
+  // 12 -> 8 chunks per segment, 40 -> 34 chunk MMA groups per row)
+  const int NQ = n_xb;                      // chunks per (row, map block) segment
   const int NSG = (NQ + 1) / 2;             // chunk pairs (TMA stages) per segment
   const int H = (T - 1) / 2;
 
@@ -132,12 +137,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
           if ((int)(gc & 1) != set) continue;
           const int slot = (int)(gc % RING);
           if (gc >= RING) {
-            bar_wait(&c_free[slot], (unsigned)(((gc / RING) - 1) & 1));
+            RC_WAIT(1, &c_free[slot], (unsigned)(((gc / RING) - 1) & 1));
             fence_after();
           }
           const long long gs = gs0 + (q >> 1);
           const int st = (int)(gs % NSTAGE), piece = q & 1;
-          bar_wait(&a_full[st], (unsigned)((gs / NSTAGE) & 1));
+          RC_WAIT(2, &a_full[st], (unsigned)((gs / NSTAGE) & 1));
           // stage layout [128 maps][2 chunks][128 B] (256-byte DRAM runs per map) or,
           // maps-major (mm), [2 chunks][128 maps][128 B]: then the 8 lanes of a
           // quarter-warp read 8 consecutive lines = 8 distinct 16-byte bank groups
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
       for (int mb = mb_lo(r); mb < mb_hi(r); ++mb) {
         for (int j = 0; j < n_xb; ++j, ++b) {
           const int dbuf = (int)(b & 1);
-          bar_wait(&mma_done[dbuf], (unsigned)((b >> 1) & 1));
+          RC_WAIT(3, &mma_done[dbuf], (unsigned)((b >> 1) & 1));
           fence_after();
           float v[32], v1[32];
           tmem_ld32(tmem + lane_addr + COL_D + dbuf * DCOLS, v);
@@ -224,7 +229,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
     for (int r = 0; r < rows_mine; ++r) {
       const int row = row0 + r;
       // B[r & 1] was last read by the MMAs of row r - 2
-      if (r >= 2) bar_wait(&row_done[r & 1], (unsigned)(((r - 2) >> 1) & 1));
+      if (r >= 2) RC_WAIT(0, &row_done[r & 1], (unsigned)(((r - 2) >> 1) & 1));
       unsigned char* Bb = B_st + (r & 1) * B_BYTES;
       for (int e = t0; e < NOUT * KSPAN; e += 64) {
         const int rr = e / KSPAN, u = e - rr * KSPAN;
@@ -250,11 +255,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
         for (int mb = mb_lo(r); mb < mb_hi(r); ++mb) {
           for (int u = 0; u < NSG; ++u, ++gp) {
             const int st = (int)(gp % NSTAGE);
-            if (gp >= NSTAGE) bar_wait(&a_empty[st], (unsigned)(((gp / NSTAGE) - 1) & 1));
+            if (gp >= NSTAGE) RC_WAIT(4, &a_empty[st], (unsigned)(((gp / NSTAGE) - 1) & 1));
             bar_expect_tx(&a_full[st], A_STAGE);
-            // chunks 2u, 2u + 1 of the segment = input chunks 2u - 2, 2u - 1 of the row
-            if (mm) tma_load_4d(A_st + st * A_STAGE, &tmap, mb * MAPS, 2 * u - 2, row, &a_full[st]);
-            else tma_load_4d(A_st + st * A_STAGE, &tmap, 2 * u - 2, row, mb * MAPS, &a_full[st]);
+            // input chunks 2u, 2u + 1 of the row (an odd n_xb: the last pair's second is OOB)
+            if (mm) tma_load_4d(A_st + st * A_STAGE, &tmap, mb * MAPS, 2 * u, row, &a_full[st]);
+            else tma_load_4d(A_st + st * A_STAGE, &tmap, 2 * u, row, mb * MAPS, &a_full[st]);
           }
         }
       }
@@ -264,44 +269,56 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
     // ===== MMA issuer: per K-step one N = 64 (A_hi [B_hi | B_lo]) and one
     // N = 32 (A_lo B_hi) MMA into the block's 64 accumulator columns
     long long b = 0, g0 = 0;
+    int wslot = 0;
+    unsigned wphase = 0;
     for (int r = 0; r < rows_mine; ++r) {
-      bar_wait(&b_full[r & 1], (unsigned)((r >> 1) & 1));  // the row's Toeplitz block is built
+      RC_WAIT(7, &b_full[r & 1], (unsigned)((r >> 1) & 1));  // the row's Toeplitz block is built
       const uint64_t db = smem_desc_sw128(su32(B_st + (r & 1) * B_BYTES));
       const unsigned b_lo32 = (unsigned)db, b_hi32 = (unsigned)(db >> 32);
       for (int mb = mb_lo(r); mb < mb_hi(r); ++mb, g0 += NQ) {
+        int slot_i0 = (int)(g0 % RING);  // ring slot of the block's first chunk i0
         for (int j = 0; j < n_xb; ++j, ++b) {
-          for (int c = (j == 0 ? 0 : CHB - 1); c < CHB; ++c) {
-            const long long g = g0 + j + c;
-            bar_wait(&c_full[(int)(g % RING)], (unsigned)((g / RING) & 1));
+          // block j reads input chunks i0 .. i1 (B K-atom c = i - j + 2)
+          const int i0 = max(0, j - 2), i1 = min(n_xb - 1, j + 2);
+          for (int i = (j == 0 ? 0 : i1); i <= i1; ++i) {
+            if (j > 0 && j + 2 > n_xb - 1) break;  // no new chunk for the row's last blocks
+            RC_WAIT(5, &c_full[wslot], wphase);     // chunks are awaited in ring order
+            if (++wslot == RING) { wslot = 0; wphase ^= 1u; }
           }
-          if (b >= 2) bar_wait(&d_empty[b & 1], (unsigned)(((b - 2) >> 1) & 1));
+          if (b >= 2) RC_WAIT(6, &d_empty[b & 1], (unsigned)(((b - 2) >> 1) & 1));
           fence_after();
           const unsigned d = COL_D + (unsigned)(b & 1) * DCOLS;
-          const int s0 = (int)((g0 + j) % RING);
-          int slot = s0;
+          int slot = slot_i0;
 #pragma unroll 1
-          for (int c = 0; c < CHB; ++c) {
+          for (int i = i0; i <= i1; ++i, slot = (slot + 1 == RING) ? 0 : slot + 1) {
             const unsigned a_hi = COL_HI + (unsigned)slot * CH, a_lo = COL_LO + (unsigned)slot * CH;
-            const unsigned bo = (unsigned)c * (B_ATOM >> 4);
-            const bool first = (c == 0);
+            const unsigned bo = (unsigned)(i - j + 2) * (B_ATOM >> 4);
+            const bool first = (i == i0);
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               const unsigned kb = b_lo32 + bo + (unsigned)t * 2;  // +32 bytes of K per step
               mma_tf32_id<IDESC64>(d, a_hi + t * 8, kb, b_hi32, !(first && t == 0));
               mma_tf32_id<IDESC32>(d, a_lo + t * 8, kb, b_hi32, true);
             }
-            slot = (slot + 1 == RING) ? 0 : slot + 1;
           }
           mma_commit_warp(&mma_done[b & 1]);
-          mma_commit_warp(&c_free[s0]);  // chunk j has no later reader
-          if (j == n_xb - 1)
-            for (int c = 1; c < CHB; ++c) mma_commit_warp(&c_free[(s0 + c) % RING]);
+          // chunk i's last reader is block min(i + 2, n_xb - 1)
+          if (j < n_xb - 1) {
+            if (j >= 2) {
+              mma_commit_warp(&c_free[slot_i0]);  // chunk i0 = j - 2
+              slot_i0 = (slot_i0 + 1 == RING) ? 0 : slot_i0 + 1;
+            }
+          } else {
+            for (int i = i0, sl = slot_i0; i <= i1; ++i, sl = (sl + 1 == RING) ? 0 : sl + 1)
+              mma_commit_warp(&c_free[sl]);
+          }
           __syncwarp();
         }
       }
       mma_commit_warp(&row_done[r & 1]);
     }
   }
+  RC_PROF_FLUSH(warp)
   fence_before();
   __syncthreads();
   fence_after();

@@ -60,7 +60,10 @@ def test_rowconv_cfg4_map_size_and_adjoint_identity(rng):
 # the 64-output block), short and full-width kernels. Tolerance: 2e-6 relative
 # L2 vs the float64 oracle (the split drops the lo*lo term and truncates lo,
 # ~2^-21 relative per product).
-@pytest.mark.parametrize("shape", [(128, 3, 256), (40, 5, 96), (33, 2, 32), (200, 3, 1024), (257, 2, 64)])
+# Every chunk-count edge of the halo-free chunk schedule (a block reads input
+# chunks max(0, j - 2) .. min(n_xb - 1, j + 2)): n_xb = 1, 2, 3, 4, 5, 8, 32.
+@pytest.mark.parametrize("shape", [(128, 3, 256), (40, 5, 96), (33, 2, 32), (200, 3, 1024), (257, 2, 64),
+                                   (96, 2, 128), (64, 3, 160)])
 @pytest.mark.parametrize("taps", [129, 31, 1])
 def test_rowconv_tensor_core_path_vs_oracle(shape, taps, rng):
     B, nz, nx = shape

@@ -41,5 +41,6 @@ for name, (B, nz, nx) in {"cfg4": (256, 2048, 1024), "cfg2": (512, 512, 256)}.it
     tfd = t(lambda: tb.tidas_rowconv(y, K, out=a, path="tensor"))  # forward on dense input (y)
     byt = B * nz * nx * 8 + K.numel() * 4
     print(json.dumps({"lib": sys.argv[1] if len(sys.argv) > 1 else "default", name: {"fwd_ms": tf, "adj_ms": ta, "fwd_frac": byt / tf / 1e6 / HBM,
-                             "adj_frac": byt / ta / 1e6 / HBM, "fwd_dense_ms": tfd, "maps_per_s_fwd": B / tf * 1e3}}), flush=True)
+                             "adj_frac": byt / ta / 1e6 / HBM, "fwd_dense_ms": tfd, "maps_per_s_fwd": B / tf * 1e3,
+                             "checksum_fwd": float(a.double().abs().sum())}}), flush=True)
     del x, y, a
