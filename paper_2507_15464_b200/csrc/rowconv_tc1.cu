@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
   __shared__ __align__(8) uint64_t mma_done[2], d_empty[2];
   __shared__ __align__(8) uint64_t row_done[2], b_full[2];
   __shared__ unsigned tmem_base_s;
+  __shared__ float Kt[2 * HALO + 4];  // the B builders' staged taps of the current row
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   RC_PROF_DECL
@@ -224,23 +225,48 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
     __syncwarp();
   } else if (warp == 10 || warp == 11) {
     // ===== B builders: the row's 32 x 160 Toeplitz block as TF32 hi / lo K-atoms,
-    // one row ahead of the MMAs (double-buffered), off the converters' path
-    const int t0 = (warp - 10) * 32 + lane;
+    // one row ahead of the MMAs (double-buffered), off the converters' path. The
+    // row's taps are staged once in shared memory (one coalesced read of K);
+    // warp 10 / 11 then build the even / odd Toeplitz rows, lane = column within
+    // a K-atom (32 consecutive words of one swizzled 128-byte line: no bank conflicts)
+    const int half = warp - 10;
+    // padded taps k = 64 i + 32 half + lane (i < 3, k <= 128) of a row, loaded one
+    // row ahead into registers so the K read latency overlaps the current build
+    auto load_taps = [&](int row, float (&kr)[3]) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int k = 64 * i + half * 32 + lane, kt = k - (HALO - H);
+        kr[i] = (row < nz && k <= 2 * HALO && kt >= 0 && kt < T)
+                    ? K[(long long)row * T + (ADJ ? (T - 1 - kt) : kt)] : 0.f;
+      }
+    };
+    float kr[3];
+    load_taps(row0, kr);
     for (int r = 0; r < rows_mine; ++r) {
       const int row = row0 + r;
+      // stage taps: Kt[k], padded tap k in [0, 128], zero outside the kernel
+      named_bar_sync(1, 64);  // the previous row's build has finished reading Kt
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int k = 64 * i + half * 32 + lane;
+        if (k <= 2 * HALO) Kt[k] = kr[i];
+      }
+      named_bar_sync(1, 64);
+      if (r + 1 < rows_mine) load_taps(row + 1, kr);
       // B[r & 1] was last read by the MMAs of row r - 2
       if (r >= 2) RC_WAIT(0, &row_done[r & 1], (unsigned)(((r - 2) >> 1) & 1));
       unsigned char* Bb = B_st + (r & 1) * B_BYTES;
-      for (int e = t0; e < NOUT * KSPAN; e += 64) {
-        const int rr = e / KSPAN, u = e - rr * KSPAN;
-        const int k = u - rr;           // padded tap index in [0, 128]
-        const int kt = k - (HALO - H);  // original tap
-        float w = 0.f;
-        if (k >= 0 && k <= 2 * HALO && kt >= 0 && kt < T) w = K[(long long)row * T + (ADJ ? (T - 1 - kt) : kt)];
-        const unsigned h = tf32_rna(w);
-        const unsigned l = tf32_rna(w - __uint_as_float(h));
-        *reinterpret_cast<unsigned*>(Bb + b_offset(rr, u)) = h;
-        *reinterpret_cast<unsigned*>(Bb + b_offset(rr + NOUT, u)) = l;
+#pragma unroll 1
+      for (int rr = half; rr < NOUT; rr += 2) {
+#pragma unroll
+        for (int atom = 0; atom < CHB; ++atom) {
+          const int k = atom * CH + lane - rr;  // padded tap of column u = 32 atom + lane
+          const float w = (k >= 0 && k <= 2 * HALO) ? Kt[k] : 0.f;
+          const unsigned h = tf32_rna(w);
+          const unsigned l = tf32_rna(w - __uint_as_float(h));
+          *reinterpret_cast<unsigned*>(Bb + b_offset(rr, atom * CH + lane)) = h;
+          *reinterpret_cast<unsigned*>(Bb + b_offset(rr + NOUT, atom * CH + lane)) = l;
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
@@ -288,6 +314,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
           if (b >= 2) RC_WAIT(6, &d_empty[b & 1], (unsigned)(((b - 2) >> 1) & 1));
           fence_after();
           const unsigned d = COL_D + (unsigned)(b & 1) * DCOLS;
+#ifdef TIDAS_RC_PROF
+          const long long t_issue = clock64();
+#endif
           int slot = slot_i0;
 #pragma unroll 1
           for (int i = i0; i <= i1; ++i, slot = (slot + 1 == RING) ? 0 : slot + 1) {
@@ -301,6 +330,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowconv_tc1_kernel(const __grid_c
               mma_tf32_id<IDESC32>(d, a_lo + t * 8, kb, b_hi32, true);
             }
           }
+#ifdef TIDAS_RC_PROF
+          rc_prof[8] += (unsigned long long)(clock64() - t_issue);
+#endif
           mma_commit_warp(&mma_done[b & 1]);
           // chunk i's last reader is block min(i + 2, n_xb - 1)
           if (j < n_xb - 1) {

@@ -33,13 +33,13 @@ int main(int argc, char** argv) {
   cudaMemcpyFromSymbol(z, tidas::tcx::g_rc_prof, sizeof(z));
   const double gbs = 2.0 * B * nz * nx * 4 / (ms * 1e-3) / 1e9;
   printf("B=%d nz=%d nx=%d rc=%d  %.4f ms  %.0f GB/s (%s)\n", B, nz, nx, rc, ms, gbs, cudaGetErrorString(cudaGetLastError()));
-  const char* site[10] = {"row_done", "c_free", "a_full", "mma_done", "a_empty", "c_full", "d_empty", "b_full", "-", "TOTAL"};
+  const char* site[10] = {"row_done", "c_free", "a_full", "mma_done", "a_empty", "c_full", "d_empty", "b_full", "issue", "TOTAL"};
   const char* role[16] = {"conv0", "conv1", "conv2", "conv3", "epi0", "epi1", "epi2", "epi3", "mma", "tma",
                           "bld0", "bld1", "conv4", "conv5", "conv6", "conv7"};
   for (int w = 0; w < 16; ++w) {
     printf("%-6s", role[w]);
     const double tot = (double)z[w][9];
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < 9; ++k)
       if (z[w][k]) printf("  %s %4.1f%%", site[k], 100.0 * z[w][k] / tot);
     printf("  | total %.0f cyc/CTA\n", tot / 148);
   }
