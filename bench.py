@@ -66,7 +66,8 @@ def workload_config(frames_per_gpu: int, world: int) -> dict:
     return {"workload": WORKLOAD, "frames_per_step_per_gpu": frames_per_gpu,
             "parallelism": f"frame-sharded dp{world}",
             "l2": f"inputs larger than L2 ({frames_per_gpu * 2} MiB RF per GPU per step)",
-            "gather": (f"NCCL all_gather of images inside the step, pipelined per {SUB} frames with the DAS of "
+            "gather": (f"NCCL all_gather_into_tensor of images inside the step (chunk-major, no staging copy), "
+                       f"pipelined per {SUB} frames with the DAS of "
                        f"the next {SUB}") if world > 1 else "none"}
 
 
@@ -368,7 +369,7 @@ def main():
         else:
             # the all-gather of sub-chunk c (async NCCL over NVLink) overlaps K1 + K2 of c + 1
             parallel.pipelined_gather(lambda c0, c1: tb.das_image(rf[c0:c1], plan, out=img[c0:c1], workspace=ws),
-                                      len(frames), gathered, sub=SUB)
+                                      len(frames), gathered, sub=SUB, layout="chunk_major")
 
     for _ in range(args.warmup):
         step()

@@ -87,16 +87,25 @@ def gather_images(local: torch.Tensor, n_units: int, out: Optional[torch.Tensor]
     return res if out is None else out.copy_(res)
 
 
-def pipelined_gather(compute, n_local: int, out: torch.Tensor, sub: int, group=None) -> torch.Tensor:
+def pipelined_gather(compute, n_local: int, out: torch.Tensor, sub: int, group=None,
+                     layout: str = "rank_major") -> torch.Tensor:
     """Compute the local units in sub-chunks and all-gather each one as soon as
     it exists, so NVLink moves chunk c while the kernels compute chunk c + 1.
 
     ``compute(c0, c1)`` returns this rank's units [c0, c1) as a tensor
     [c1 - c0][...] (enqueued on the current stream). Every rank holds the same
-    ``n_local`` units; ``out`` [world * n_local][...] receives them in global
-    (rank-major) order. Each gather is an async NCCL ``all_gather`` ordered
-    after the compute that produced its chunk; the call returns once the
-    current stream waits for all of them."""
+    ``n_local`` units; ``out`` [world * n_local][...] receives all of them. Each
+    gather is an async NCCL collective ordered after the compute that produced
+    its chunk; the call returns once the current stream waits for all of them.
+
+    layout "rank_major": global order (unit f of rank r at ``r * n_local + f``);
+    NCCL's list all-gather stages through a flat buffer and copies out.
+    layout "chunk_major": chunk [c0, c1) of every rank lands in the contiguous
+    slice ``out[world * c0 : world * c1]`` (rank r at ``world * c0 + r * (c1 - c0)``,
+    see ``chunk_major_index``) by ``all_gather_into_tensor`` straight into
+    ``out`` — no staging buffer, no copy kernel."""
+    if layout not in ("rank_major", "chunk_major"):
+        raise ValueError(f"layout must be 'rank_major' or 'chunk_major', got {layout!r}")
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if out.shape[0] != world * n_local:
         raise ValueError(f"out holds {out.shape[0]} units, expected world * n_local = {world * n_local}")
@@ -108,8 +117,21 @@ def pipelined_gather(compute, n_local: int, out: torch.Tensor, sub: int, group=N
             if part.data_ptr() != out[c0:c1].data_ptr():
                 out[c0:c1].copy_(part)
             continue
-        views = [out[r * n_local + c0: r * n_local + c1] for r in range(world)]
-        works.append(dist.all_gather(views, part.contiguous(), group=group, async_op=True))
+        if layout == "chunk_major":
+            works.append(dist.all_gather_into_tensor(out[world * c0: world * c1], part.contiguous(), group=group,
+                                                     async_op=True))
+        else:
+            views = [out[r * n_local + c0: r * n_local + c1] for r in range(world)]
+            works.append(dist.all_gather(views, part.contiguous(), group=group, async_op=True))
     for w in works:
         w.wait()
     return out
+
+
+def chunk_major_index(f: int, n_local: int, world: int, sub: int) -> int:
+    """Position in a ``pipelined_gather(layout="chunk_major")`` output of global
+    unit ``f`` (rank ``f // n_local``, local unit ``f % n_local``)."""
+    r, i = divmod(int(f), n_local)
+    c0 = (i // sub) * sub
+    c1 = min(n_local, c0 + sub)
+    return world * c0 + r * (c1 - c0) + (i - c0)

@@ -30,11 +30,16 @@ def main() -> int:
     local = torch.stack([frame_image(f) for f in range(a, b)])
     out = torch.empty((per_rank * world, 2, 3))
     parallel.pipelined_gather(lambda c0, c1: local[c0:c1], b - a, out, sub=2)
+    # the bench's zero-copy chunk-major layout
+    out_cm = torch.empty((per_rank * world, 2, 3))
+    parallel.pipelined_gather(lambda c0, c1: local[c0:c1], b - a, out_cm, sub=2, layout="chunk_major")
+    cm_ok = all(torch.equal(out_cm[parallel.chunk_major_index(f, per_rank, world, 2)], frame_image(f))
+                for f in range(per_rank * world))
     fixed = 7                                      # strong (cfg3 / cfg5): fixed batch, ragged shards
     c0, c1 = parallel.shard_range(fixed, rank, world)
     loc2 = torch.stack([frame_image(f) for f in range(c0, c1)])
     full = parallel.gather_images(loc2, fixed)
-    ok = bool(torch.equal(out, torch.stack([frame_image(f) for f in range(per_rank * world)])) and
+    ok = bool(cm_ok and torch.equal(out, torch.stack([frame_image(f) for f in range(per_rank * world)])) and
               torch.equal(full, torch.stack([frame_image(f) for f in range(fixed)])))
     oks = [None] * world
     dist.all_gather_object(oks, ok)

@@ -58,7 +58,7 @@ def test_gather_two_ranks_matches_single_process(n_units):
     assert res[0] == want and res[1] == want
 
 
-def _pipelined_worker(rank, world, port, n_local, sub, q):
+def _pipelined_worker(rank, world, port, n_local, sub, q, layout="rank_major"):
     from paper_2507_15464_b200.parallel import pipelined_gather
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -70,7 +70,7 @@ def _pipelined_worker(rank, world, port, n_local, sub, q):
         return torch.stack([torch.full((2, 3), float(f0 + f)) for f in range(c0, c1)])
 
     out = torch.empty((world * n_local, 2, 3))
-    pipelined_gather(compute, n_local, out, sub)
+    pipelined_gather(compute, n_local, out, sub, layout=layout)
     q.put((rank, out.numpy().tolist(), calls))
     dist.barrier()
     dist.destroy_process_group()
@@ -93,6 +93,29 @@ def test_pipelined_gather_two_ranks(n_local, sub):
     for r in (0, 1):
         assert res[r][0] == want
         assert res[r][1] == chunks
+
+
+@pytest.mark.parametrize("n_local,sub", [(8, 3), (6, 6), (5, 1), (7, 64)])
+def test_pipelined_gather_chunk_major_two_ranks(n_local, sub):
+    """The bench's zero-copy layout: each sub-chunk all-gathered straight into a
+    contiguous slice of the output; chunk_major_index maps global units."""
+    from paper_2507_15464_b200.parallel import chunk_major_index
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipelined_worker, args=(r, 2, port, n_local, sub, q, "chunk_major"))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r: (o, c) for r, o, c in (q.get(timeout=120) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        out = res[r][0]
+        assert sorted(row[0][0] for row in out) == [float(f) for f in range(2 * n_local)]
+        for f in range(2 * n_local):
+            assert out[chunk_major_index(f, n_local, 2, sub)][0][0] == float(f)
 
 
 def test_relaunch_spawns_ranks_like_bench():
