@@ -99,7 +99,19 @@ typedef struct {
   double f_number;    /* Hann: half-width z / (2 f_number) */
   int32_t out_mode;   /* enum tidas_out */
   int32_t prec;       /* enum tidas_prec: analytic / out element precision */
+  int32_t window;     /* largest per-tile sample window of the plan (tidas_das_window);
+                         0 = unknown: the widest FP32 staging box (256 samples) is used.
+                         A too-small value is still exact (wider tiles gather from global). */
 } tidas_das_desc_t;
+
+/*
+ * Plan sizing for K2: *max_window (device int32) = the largest sample window
+ * [min k0 - 1, max(k0 - floor(s_min)) + 1] of any FP32 pixel tile over all
+ * transmits — the same window logic K2 runs. Called once per plan; K2 then
+ * stages windows in the narrowest compiled TMA box that holds it.
+ */
+int tidas_das_window(const tidas_das_desc_t* desc, const double* t_star, const double* x,
+                     const double* z, const int32_t* ap_half, int32_t* max_window, void* stream);
 
 /*
  *   analytic : [F][A][n_el][N] complex (from tidas_rf_analytic, same prec)

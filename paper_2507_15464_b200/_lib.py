@@ -30,7 +30,7 @@ class DasDesc(C.Structure):
         ("n_samples", C.c_int32), ("nx", C.c_int32), ("nz", C.c_int32),
         ("pitch", C.c_double), ("c", C.c_double), ("fs", C.c_double), ("t0", C.c_double),
         ("aperture", C.c_int32), ("f_number", C.c_double), ("out_mode", C.c_int32),
-        ("prec", C.c_int32),
+        ("prec", C.c_int32), ("window", C.c_int32),
     ]
 
 
@@ -43,6 +43,7 @@ SIGNATURES = {
     "tidas_spectral_shift_f64": ([_P, _I64, _I32, _D, _P, _P], C.c_int),
     "tidas_plane_wave_arrivals": ([_P, _I32, _P, _I32, _P, _I32, _I32, _D, _D, _P, _P], C.c_int),
     "tidas_das_image": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "tidas_das_window": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P], C.c_int),
     "tidas_delayed_sum_f64": ([_P, _I32, _I32, _P, _P, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "tidas_window_envelope_f64": ([_P, _I32, _P, _P, _P, _P, _P, _I32, _P, _P], C.c_int),
     "tidas_window_dots_f64": ([_P, _P, _I32, _P, _P, _I32, _P, _P], C.c_int),

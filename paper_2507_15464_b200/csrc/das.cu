@@ -49,6 +49,7 @@ constexpr int DAS_WMAX = 400;  // staged window capacity (samples) per frame of 
 
 struct DasParams {
   int F, A, E, N, nx, nz;
+  int window;  // largest per-CTA sample window of the plan (tidas_das_window), 0 = unknown
   double pitch, c, fs, t0, f_number;
   const int32_t* ap_half;
   const double* t_star;
@@ -226,14 +227,67 @@ template <> struct DasShape<double> {
 };
 constexpr int DAS_NW = 8;  // consumer warps per CTA (+ 1 producer warp)
 
-template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX>
+// Receive aperture [n_lo, n_hi] of a pixel (channel offsets from the array
+// centre; n_lo > n_hi: none), the boxcar half count, and m_min: one below the
+// most negative receive shift (samples), so the pixel's taps j = k0 - m lie in
+// [k0 - 1, k0 - m_min + 1] for every channel of its aperture. Shared by K2 and
+// the plan's window sizing (das_window_kernel), so both see the same windows.
+template <int AP>
+__device__ __forceinline__ void pixel_aperture(const DasParams& p, bool pix, int iz, double x, double zm,
+                                               int& n_lo, int& n_hi, int& ap_h, int& m_min) {
+  const int half = p.E / 2;
+  n_lo = half;
+  n_hi = -half - 1;
+  ap_h = 0;
+  double dxmax = 0.0;
+  if (pix) {
+    if (AP == TIDAS_AP_HANN) {
+      const double a = zm / (2.0 * p.f_number);
+      n_lo = (int)floor((x - a) / p.pitch - 0.5);  // one extra each side: the
+      n_hi = (int)ceil((x + a) / p.pitch - 0.5);   // predicate |dx| < a decides
+      dxmax = a;
+    } else {
+      ap_h = p.ap_half[iz];
+      n_lo = -ap_h;
+      n_hi = ap_h - 1;
+    }
+    n_lo = max(n_lo, -half);
+    n_hi = min(n_hi, half - 1);
+    if (n_lo <= n_hi) {
+      dxmax = fmin(dxmax > 0.0 ? dxmax : 1e300,
+                   fmax(fabs(((double)n_lo + 0.5) * p.pitch - x), fabs(((double)n_hi + 0.5) * p.pitch - x)));
+    }
+  }
+  const double s_min = (zm - hypot(dxmax, zm)) / p.c * p.fs;
+  m_min = (int)floor(s_min) - 1;  // one sample of slack for FP32 rounding
+}
+
+// Arrival of transmit a at pixel (iz, ix) split into an integer sample index and
+// a fraction in float64; false when t* falls off the trace (np.interp's 0)
+template <typename R>
+__device__ __forceinline__ bool pixel_arrival(const DasParams& p, bool pix, int a, int iz, int ix, int& k0, R& fr) {
+  k0 = 0;
+  fr = R(0);
+  if (!pix) return false;
+  const double pos = (p.t_star[((int64_t)a * p.nz + iz) * p.nx + ix] - p.t0) * p.fs;
+  if (!((pos >= 0.0) && (pos <= (double)(p.N - 1)))) return false;
+  const double fl = floor(pos);
+  k0 = (int)fl;
+  fr = (R)(pos - fl);
+  return true;
+}
+
+// WCAP_T: the staging box holds WCAP_T + 2 samples per (frame, channel); CTAs
+// whose window is wider gather from global memory instead (slow, exact). The
+// plan's measured window picks the narrowest compiled box that holds it.
+template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX, int WCAP_T>
 __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasParams p,
                                                                        const cplx<R>* __restrict__ A,
                                                                        void* __restrict__ out_,
                                                                        const __grid_constant__ CUtensorMap tmap) {
   using C = cplx<R>;
   using S = DasShape<R>;
-  constexpr int FB = S::FB, DG = S::DG, WZ = S::WZ, WCAP = S::WCAP, CPB = S::CPB, NW = DAS_NW;
+  constexpr int FB = S::FB, DG = S::DG, WZ = S::WZ, WCAP = WCAP_T, CPB = S::CPB, NW = DAS_NW;
   constexpr bool TMAP = S::TMAP, U32 = S::U32, LPT = S::LPT;
   constexpr int DAS_WSTRIDE = WCAP + 2;  // per-frame window stride (elements, even)
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -271,31 +325,9 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
   PixelGeo<R> geo;
   geo.init(p, x, zm);
 
-  // receive aperture of this pixel and the largest lateral offset inside it
-  int n_lo = half, n_hi = -half - 1, ap_h = 0;
-  double dxmax = 0.0;
-  if (pix) {
-    if (AP == TIDAS_AP_HANN) {
-      const double a = zm / (2.0 * p.f_number);
-      n_lo = (int)floor((x - a) / p.pitch - 0.5);  // one extra each side: the
-      n_hi = (int)ceil((x + a) / p.pitch - 0.5);   // predicate |dx| < a decides
-      dxmax = a;
-    } else {
-      ap_h = p.ap_half[iz];
-      n_lo = -ap_h;
-      n_hi = ap_h - 1;
-    }
-    n_lo = max(n_lo, -half);
-    n_hi = min(n_hi, half - 1);
-    if (n_lo <= n_hi) {
-      dxmax = fmin(dxmax > 0.0 ? dxmax : 1e300,
-                   fmax(fabs(((double)n_lo + 0.5) * p.pitch - x), fabs(((double)n_hi + 0.5) * p.pitch - x)));
-    }
-  }
-  // most negative receive shift of the pixel (samples): its taps j = k0 - m lie
-  // in [k0, k0 - floor(s_min)] for every channel of the aperture
-  const double s_min = (zm - hypot(dxmax, zm)) / p.c * p.fs;
-  const int m_min = (int)floor(s_min) - 1;  // one sample of slack for FP32 rounding
+  // receive aperture of this pixel and its most negative shift
+  int n_lo, n_hi, ap_h, m_min;
+  pixel_aperture<AP>(p, pix, iz, x, zm, n_lo, n_hi, ap_h, m_min);
 
   if (tid == 0) {
     red[0] = INT_MAX;
@@ -337,18 +369,9 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   for (int a = 0; a < n_tx; ++a) {
     // arrival split into integer index + fraction in float64
-    int k0 = 0;
-    R fr = R(0);
-    bool vpos = false;
-    if (pix) {
-      const double pos = (p.t_star[((int64_t)a * p.nz + iz) * p.nx + ix] - p.t0) * p.fs;
-      vpos = (pos >= 0.0) && (pos <= (double)(p.N - 1));
-      if (vpos) {
-        const double fl = floor(pos);
-        k0 = (int)fl;
-        fr = (R)(pos - fl);
-      }
-    }
+    int k0;
+    R fr;
+    const bool vpos = pixel_arrival<R>(p, pix, a, iz, ix, k0, fr);
     const bool active_px = pix && vpos && n_lo <= n_hi;
     // CTA tap window of this transmit, the same for every channel
     int* rw = red + 2 + 2 * (a & 1);
@@ -547,6 +570,39 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
   }
 }
 
+// The plan's largest per-CTA sample window over all transmits, for the FP32
+// tile shape (WZ x DG depths x 32 / WZ columns): K2's own window logic
+// (pixel_aperture, pixel_arrival), one CTA per pixel tile, max into *out.
+template <int AP>
+__global__ void __launch_bounds__(256) das_window_kernel(DasParams p, int32_t* __restrict__ out) {
+  using S = DasShape<float>;
+  constexpr int WZ = S::WZ, WX = 32 / WZ;
+  __shared__ int lo_s, hi_s;
+  const int lane = threadIdx.x, wid = threadIdx.y;  // 8 warps = the consumer warps of K2
+  const int iz = blockIdx.x * (WZ * S::DG) + wid * WZ + lane / WX;
+  const int ix = blockIdx.y * WX + lane % WX;
+  const bool pix = (iz < p.nz) && (ix < p.nx);
+  const double x = pix ? p.xg[ix] : 0.0;
+  const double zm = pix ? p.zg[iz] : 1.0;
+  int n_lo, n_hi, ap_h, m_min;
+  pixel_aperture<AP>(p, pix, iz, x, zm, n_lo, n_hi, ap_h, m_min);
+  int wmax = 0;
+  for (int a = 0; a < p.A; ++a) {
+    int k0;
+    float fr;
+    const bool active = pixel_arrival<float>(p, pix, a, iz, ix, k0, fr) && n_lo <= n_hi;
+    if (threadIdx.x == 0 && threadIdx.y == 0) { lo_s = INT_MAX; hi_s = INT_MIN; }
+    __syncthreads();
+    const int wl = __reduce_min_sync(0xffffffffu, active ? k0 - 1 : INT_MAX);
+    const int wh = __reduce_max_sync(0xffffffffu, active ? k0 - m_min + 1 : INT_MIN);
+    if (lane == 0) { atomicMin(&lo_s, wl); atomicMax(&hi_s, wh); }
+    __syncthreads();
+    if (hi_s >= lo_s) wmax = max(wmax, hi_s - lo_s + 1);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && threadIdx.y == 0 && wmax > 0) atomicMax(out, wmax);
+}
+
 __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double* z, int nz,
                                            const double* angles, int na, int n_el, double pitch,
                                            double c, double* out) {
@@ -562,12 +618,12 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
   out[i] = (x[ix] * sn + z[iz] * cs + origin) / c + z[iz] / c;
 }
 
-template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX>
+template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX, int WCAP = DasShape<R>::WCAP>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
   using S = DasShape<R>;
-  constexpr int FB = S::FB, DG = S::DG, WZ = S::WZ, WCAP = S::WCAP, CPB = S::CPB, NW = DAS_NW;
-  auto kern = das_image_kernel<R, AP, OUT, DAS_NBUF, MINB, ONE_TX>;
+  constexpr int FB = S::FB, DG = S::DG, WZ = S::WZ, CPB = S::CPB, NW = DAS_NW;
+  auto kern = das_image_kernel<R, AP, OUT, DAS_NBUF, MINB, ONE_TX, WCAP>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if constexpr (S::TMAP) {
@@ -622,14 +678,25 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
 // SM; multi-transmit envelope compounding keeps c0 / c1 and the frame
 // accumulators live across transmits and runs 3 buffers at 2 CTAs / SM. The
 // choice depends on the plan only, never on the frame count.
+template <typename R, int AP, int OUT, int WCAP>
+static int dispatch_fb_box(const DasParams& p, const void* A, void* out, cudaStream_t st) {
+  if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1) return launch_das<R, AP, OUT, 2, 3, true, WCAP>(p, A, out, st);
+  if (OUT != TIDAS_OUT_ENVELOPE) return launch_das<R, AP, OUT, 2, 3, false, WCAP>(p, A, out, st);
+  return launch_das<R, AP, OUT, 3, 2, false, WCAP>(p, A, out, st);
+}
+
+// FP32 staging boxes: the narrow one (200 samples) whenever the plan's windows
+// fit it — fewer TMA bytes (L2 -> shared memory) beside the same gathers:
+// cfg2 K2 4.74 -> 4.66 us/frame, cfg1 / cfg3 / cfg5 +0.7-1.6% (all fit)
+constexpr int DAS_WCAP_NARROW = 198;
+
 template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   if constexpr (sizeof(R) == 8) {
     return launch_das<R, AP, OUT, 4, 3, false>(p, A, out, st);
   } else {
-    if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1) return launch_das<R, AP, OUT, 2, 3, true>(p, A, out, st);
-    if (OUT != TIDAS_OUT_ENVELOPE) return launch_das<R, AP, OUT, 2, 3, false>(p, A, out, st);
-    return launch_das<R, AP, OUT, 3, 2, false>(p, A, out, st);
+    if (p.window > 0 && p.window <= DAS_WCAP_NARROW) return dispatch_fb_box<R, AP, OUT, DAS_WCAP_NARROW>(p, A, out, st);
+    return dispatch_fb_box<R, AP, OUT, DasShape<R>::WCAP>(p, A, out, st);
   }
 }
 
@@ -671,11 +738,38 @@ extern "C" int tidas_das_image(const tidas_das_desc_t* d, const void* analytic, 
   p.nx = d->nx; p.nz = d->nz;
   p.pitch = d->pitch; p.c = d->c; p.fs = d->fs; p.t0 = d->t0; p.f_number = d->f_number;
   p.ap_half = ap_half; p.t_star = t_star; p.xg = x; p.zg = z;
+  p.window = d->window;
   cudaStream_t st = as_stream(stream);
   if (d->prec == TIDAS_PREC_F32) return dispatch_ap<float>(d, p, analytic, out, st);
   if (d->prec == TIDAS_PREC_F64) return dispatch_ap<double>(d, p, analytic, out, st);
   set_error("unknown precision %d", d->prec);
   return TIDAS_EINVAL;
+}
+
+extern "C" int tidas_das_window(const tidas_das_desc_t* d, const double* t_star, const double* x,
+                                const double* z, const int32_t* ap_half, int32_t* max_window, void* stream) {
+  using namespace tidas;
+  TIDAS_REQUIRE(d && t_star && x && z && max_window, "null pointer");
+  TIDAS_REQUIRE(d->n_el >= 2 && d->n_el % 2 == 0, "n_el must be even and >= 2");
+  TIDAS_REQUIRE(d->n_angles >= 1 && d->nx >= 0 && d->nz >= 0, "bad sizes");
+  TIDAS_REQUIRE(d->aperture != TIDAS_AP_REF_BOXCAR || ap_half, "REF_BOXCAR needs ap_half");
+  TIDAS_REQUIRE(d->aperture == TIDAS_AP_HANN || d->aperture == TIDAS_AP_REF_BOXCAR, "unknown aperture %d",
+                d->aperture);
+  cudaStream_t st = as_stream(stream);
+  TIDAS_CUDA_CHECK(cudaMemsetAsync(max_window, 0, sizeof(int32_t), st));
+  if (d->nx == 0 || d->nz == 0) return TIDAS_OK;
+  DasParams p;
+  memset(&p, 0, sizeof(p));
+  p.A = d->n_angles; p.E = d->n_el; p.N = d->n_samples; p.nx = d->nx; p.nz = d->nz;
+  p.pitch = d->pitch; p.c = d->c; p.fs = d->fs; p.t0 = d->t0; p.f_number = d->f_number;
+  p.ap_half = ap_half; p.t_star = t_star; p.xg = x; p.zg = z;
+  using S = DasShape<float>;
+  const dim3 grid((d->nz + S::WZ * S::DG - 1) / (S::WZ * S::DG), (d->nx + 32 / S::WZ - 1) / (32 / S::WZ));
+  TIDAS_REQUIRE(grid.y <= 65535, "pixel grid too large");
+  if (d->aperture == TIDAS_AP_HANN) das_window_kernel<TIDAS_AP_HANN><<<grid, dim3(32, 8), 0, st>>>(p, max_window);
+  else das_window_kernel<TIDAS_AP_REF_BOXCAR><<<grid, dim3(32, 8), 0, st>>>(p, max_window);
+  TIDAS_LAUNCH_CHECK();
+  return TIDAS_OK;
 }
 
 extern "C" int tidas_plane_wave_arrivals(const double* x, int32_t nx, const double* z, int32_t nz,

@@ -52,6 +52,7 @@ class DasPlan:
     ap_half: Optional[torch.Tensor] = None
     chunk_bytes: int = 1 << 30
     _desc: Optional[_lib.DasDesc] = field(default=None, repr=False)
+    _window: Optional[int] = field(default=None, repr=False)
 
     @property
     def n_angles(self) -> int:
@@ -83,7 +84,30 @@ class DasPlan:
             d.aperture, d.f_number = _lib.AP_REF_BOXCAR, 1.0
         d.out_mode = OUT_MODES[self.out]
         d.prec = self.prec_code
+        d.window = self.window() if self.prec == "f32" else 0
         return d
+
+    def window(self) -> int:
+        """Largest per-tile sample window of the plan (tidas_das_window, the
+        same logic K2 runs), measured once: K2 stages windows in the narrowest
+        TMA box that holds it."""
+        if self._window is None:
+            d = _lib.DasDesc()
+            d.n_frames, d.n_angles, d.n_el, d.n_samples = 0, self.n_angles, self.n_el, self.n_samples
+            d.nx, d.nz = self.nx, self.nz
+            d.pitch, d.c, d.fs, d.t0 = self.pitch, self.c, self.fs, self.t0
+            if self.aperture[0] == "hann":
+                d.aperture, d.f_number = _lib.AP_HANN, float(self.aperture[1])
+            else:
+                d.aperture, d.f_number = _lib.AP_REF_BOXCAR, 1.0
+            w = torch.zeros(1, dtype=torch.int32, device=self.x.device)
+            with torch.cuda.device(self.x.device):
+                _lib.check(_lib.lib().tidas_das_window(
+                    C.byref(d), _lib.ptr(self.t_star), _lib.ptr(self.x), _lib.ptr(self.z),
+                    _lib.ptr(self.ap_half) if self.ap_half is not None else None, _lib.ptr(w),
+                    _lib.stream_handle()))
+                self._window = int(w.item())
+        return self._window
 
 
 def _dev(a, dtype, device) -> torch.Tensor:

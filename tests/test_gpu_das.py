@@ -325,3 +325,85 @@ def test_file_ingest_to_images_through_host_pipeline(tmp_path):
     pipe.synchronize()
     ref = tb.das_image(torch.as_tensor(np.stack(rfs)).to(DEV), plan).cpu()
     assert torch.equal(out, ref)
+
+
+# ------------------------------------------- plan window sizing (TMA staging box)
+
+
+def _tile_windows_numpy(cfg, x, z, angles=(0.0,)):
+    """Restatement of K2's per-tile sample window (das.cu pixel_aperture /
+    pixel_arrival) over tiles of 32 depths x 8 columns: max over tiles and transmits."""
+    half = cfg["n_el"] // 2
+    X, Z = np.meshgrid(x, z)
+    wmax = 0
+    for ang in angles:
+        ts = (X * np.sin(ang) + Z * np.cos(ang) + 0.5 * (cfg["n_el"] - 1) * cfg["pitch"] * abs(np.sin(ang))) \
+            / cfg["c"] + Z / cfg["c"]
+        pos = ts * cfg["fs"]
+        k0 = np.floor(pos).astype(np.int64)
+        a = Z / (2 * cfg["f_number"])
+        n_lo = np.maximum(np.floor((X - a) / cfg["pitch"] - 0.5).astype(int), -half)
+        n_hi = np.minimum(np.ceil((X + a) / cfg["pitch"] - 0.5).astype(int), half - 1)
+        dxm = np.minimum(a, np.maximum(np.abs((n_lo + 0.5) * cfg["pitch"] - X), np.abs((n_hi + 0.5) * cfg["pitch"] - X)))
+        m_min = np.floor((Z - np.hypot(dxm, Z)) / cfg["c"] * cfg["fs"]).astype(np.int64) - 1
+        act = (pos >= 0) & (pos <= cfg["n_samples"] - 1) & (n_lo <= n_hi)
+        for i in range(0, Z.shape[0], 32):
+            for j in range(0, Z.shape[1], 8):
+                m = act[i:i + 32, j:j + 8]
+                if m.any():
+                    lo = (k0[i:i + 32, j:j + 8][m] - 1).min()
+                    hi = (k0[i:i + 32, j:j + 8] - m_min[i:i + 32, j:j + 8])[m].max() + 1
+                    wmax = max(wmax, int(hi - lo + 1))
+    return wmax
+
+
+def test_plan_window_matches_restatement_and_boxes_are_bitwise_equal():
+    """tidas_das_window == the numpy restatement of K2's tile windows (cfg2 grid:
+    194 samples, fits the 200-sample box); images from the narrow and the wide
+    (256) staging box are bitwise identical and match the oracle."""
+    cfg = CFG2
+    rf, _ = speckle_rf(cfg, seed=11, n_scat=400)
+    rf = rf[None].astype(np.float32)
+    x, z = grid(cfg)
+    img, ref, plan = _plane_case(cfg, rf, cfg["nz"], cfg["nx"])
+    assert plan.window() == _tile_windows_numpy(cfg, x, z) == 194
+    assert rel_l2(img, ref) <= FP32_TOL
+    plan._window = 0  # unknown: the widest box
+    wide = tb.das_image(torch.as_tensor(rf).to(DEV), plan).cpu().numpy()
+    assert np.array_equal(img, wide)
+
+
+@pytest.mark.parametrize("nz, forced", [(384, None), (384, 100), (512, 100)])
+def test_plan_window_wide_and_underestimated(nz, forced):
+    """A grid whose tile windows exceed the narrow box (nz = 384: ~238 samples)
+    takes the wide box; an underestimated window (forced) picks the narrow box
+    and the wider tiles gather from global memory — exact either way."""
+    cfg = CFG2
+    rf, _ = speckle_rf(cfg, seed=12, n_scat=300)
+    rf = rf[None].astype(np.float32)
+    x, z = grid(cfg, nz, 64)
+    plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                              n_samples=rf.shape[-1], x=x, z=z, f_number=cfg["f_number"])
+    assert plan.window() == _tile_windows_numpy(cfg, x, z)
+    if nz == 384:
+        assert 198 < plan.window() <= 254
+    if forced is not None:
+        plan._window = forced
+    img = tb.das_image(torch.as_tensor(rf).to(DEV), plan).cpu().numpy()
+    A = od.analytic_signal(np.asarray(rf[0], float))
+    ref = od.das_image_vectorized(A, cfg["fs"], 0.0, x, z, cfg["pitch"], cfg["c"],
+                                  plane_t_star(cfg, x, z, (0.0,)), cfg["f_number"])
+    assert rel_l2(img[0], ref) <= FP32_TOL
+
+
+def test_plan_window_cfg3_steered_and_cfg5():
+    """Steered transmits (cfg3, 11 angles) and the cfg5 grid: the device window
+    equals the restatement (and both fit the narrow box)."""
+    for cfg, angles in ((CFG3, CFG3["angles"]), (CFG5, (0.0,))):
+        x, z = grid(cfg)
+        plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                                  n_samples=cfg["n_samples"], x=x, z=z, angles=angles,
+                                  f_number=cfg["f_number"], out="coherent" if len(angles) > 1 else "envelope")
+        w = plan.window()
+        assert w == _tile_windows_numpy(cfg, x, z, angles)
+        assert 0 < w <= 198

@@ -118,7 +118,11 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--configs", default="cfg1,cfg3,cfg5")
+    ap.add_argument("--lib", default=None, help="a variant libtidas_b200.so (tools/build_variant.sh)")
     args = ap.parse_args()
+    if args.lib:
+        from paper_2507_15464_b200 import _lib
+        _lib.load(Path(args.lib))
     print(json.dumps(run_configs(args.configs.split(","), args.steps, args.warmup, echo=True)))
 
 
