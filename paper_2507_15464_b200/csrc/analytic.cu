@@ -211,7 +211,7 @@ template <bool INV> __device__ __forceinline__ float2 tw64(float2 v, int e) {
   else if (q == 2) { c = -cs.x; s = cs.y; }
   else { c = cs.y; s = cs.x; }
   if (INV) s = -s;
-  return make_float2(v.x * c - v.y * s, v.x * s + v.y * c);
+  return cmul_k(v, make_float2(c, s), make_float2(-s, c));
 }
 
 // ------------------------- N = 4096, 128 threads: 32 values per thread
@@ -502,7 +502,7 @@ template <bool INV> __device__ __forceinline__ float2 tw128(float2 v, int e) {
   else if (q == 2) { c = -cs.x; s = cs.y; }
   else { c = cs.y; s = cs.x; }
   if (INV) s = -s;
-  return make_float2(v.x * c - v.y * s, v.x * s + v.y * c);
+  return cmul_k(v, make_float2(c, s), make_float2(-s, c));
 }
 
 __device__ __forceinline__ float2 shfl8(float2 a) {

@@ -54,12 +54,22 @@ template <typename R> using cplx = typename cplx_t<R>::type;
 template <typename C> __host__ __device__ __forceinline__ C cmake(double re, double im) {
   C r; r.x = re; r.y = im; return r;
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+// FP32 complex arithmetic on the packed sm_100 pipes (FADD2 / FMUL2 / FFMA2):
+// one instruction per complex add, two per complex multiply (a.x b + a.y (i b):
+// one product rounded, the other fused, as the scalar form contracts). The
+// swaps and signs of a multiplication by +-i fold into FADD2's operand
+// modifiers when the translation unit is built without -ftz (analytic.cu,
+// _build.py); with -ftz the compiler materialises negated copies instead.
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x)));
+}
+// a * (c + i s) for a constant twiddle given as (c, s) and its rotation (-s, c)
+__device__ __forceinline__ float2 cmul_k(float2 a, float2 cs, float2 rot) {
+  return __ffma2_rn(make_float2(a.x, a.x), cs, __fmul2_rn(make_float2(a.y, a.y), rot));
 }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);

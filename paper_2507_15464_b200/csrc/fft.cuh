@@ -70,10 +70,14 @@ template <bool INV, typename R> __device__ __forceinline__ cplx<R> w16(cplx<R> v
     default: cr = R(0); ci = R(0); break;
   }
   if (INV) ci = -ci;
-  cplx<R> r;
-  r.x = v.x * cr - v.y * ci;
-  r.y = v.x * ci + v.y * cr;
-  return r;
+  if constexpr (sizeof(R) == 4) {
+    return cmul_k(v, make_float2(cr, ci), make_float2(-ci, cr));
+  } else {
+    cplx<R> r;
+    r.x = v.x * cr - v.y * ci;
+    r.y = v.x * ci + v.y * cr;
+    return r;
+  }
 }
 
 template <bool INV, typename R> __device__ __forceinline__ void dft8(cplx<R>* v) {
