@@ -1,7 +1,9 @@
 """cfg2 DAS (K1 + K2) over 256 frames at different chunk sizes (frames per
 K1 / K2 launch): small chunks keep the analytic intermediate L2-resident
 (less DRAM traffic), large chunks shorten the kernels' last-wave tails.
-python tools/das_chunk_sweep.py [chunk ...]"""
+python tools/das_chunk_sweep.py [--sustain] [chunk ...]
+--sustain: 1.5 s of load before a 1 s timed window (the bench's power-capped
+steady state) and the median SM clock over the window (NVML)."""
 import json
 import sys
 from pathlib import Path
@@ -20,7 +22,24 @@ sx, sz, a = bench.frame_scatterers(cfg, range(F))
 rf = tb.synthesize_batch(sx, sz, a, angles=[0.0], dtype=torch.float32,
                          **{k: cfg[k] for k in ("n_el", "pitch", "fs", "c", "f0", "fbw", "n_samples")})
 img = torch.empty((F, cfg["nz"], cfg["nx"]), device="cuda")
-chunks = [int(c) for c in sys.argv[1:]] or [8, 16, 24, 32, 64, 128, 256]
+sustain = "--sustain" in sys.argv
+chunks = [int(c) for c in sys.argv[1:] if c != "--sustain"] or [8, 16, 24, 32, 64, 128, 256]
+
+
+def sm_clock_sampler():
+    import threading
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    samples, stop = [], threading.Event()
+
+    def run():
+        while not stop.is_set():
+            samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            stop.wait(0.05)
+    th = threading.Thread(target=run, daemon=True)
+    th.start()
+    return samples, stop, th
 for ch in chunks:
     plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
                               n_samples=cfg["n_samples"], x=x, z=z, f_number=cfg["f_number"])
@@ -30,12 +49,26 @@ for ch in chunks:
     for _ in range(3):
         tb.das_image(rf, plan, out=img, workspace=ws)
     torch.cuda.synchronize()
+    n_it, clk = 10, None
+    if sustain:
+        import statistics
+        import time
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 1.5:
+            tb.das_image(rf, plan, out=img, workspace=ws)
+            torch.cuda.synchronize()
+        n_it = 600
+        samples, stop, th = sm_clock_sampler()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(10):
+    for _ in range(n_it):
         tb.das_image(rf, plan, out=img, workspace=ws)
     e1.record()
     torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) / 10 / F * 1e3
-    print(json.dumps({"chunk_frames": ch, "us_per_frame": us, "frames_per_s": 1e6 / us}), flush=True)
+    if sustain:
+        stop.set()
+        th.join()
+        clk = statistics.median(samples) if samples else None
+    us = e0.elapsed_time(e1) / n_it / F * 1e3
+    print(json.dumps({"chunk_frames": ch, "us_per_frame": us, "frames_per_s": 1e6 / us, "sm_mhz": clk}), flush=True)
     del ws
