@@ -89,3 +89,29 @@ def test_das_image_writes_stay_inside_the_output(frames):
     tb.das_image(rf, plan, out=out)
     assert bool((buf[:guard] == -3.0).all()) and bool((buf[-guard:] == -3.0).all())
     assert bool((out >= 0).all())  # envelopes
+
+
+@pytest.mark.parametrize("frames", [8, 5])
+def test_das_windows_wrapping_the_trace(frames):
+    """Pixels whose arrival lies at the very start (tile window below sample 0)
+    or end of the trace (window past N - 1): the producer's wrap-around bulk
+    copies (periodic indexing, as the analytic-signal gather of the oracle),
+    with a full and a partial frame batch, against the oracle."""
+    from oracle import das as od
+    from tests.setups import plane_t_star
+    c = CFG2
+    N = c["n_samples"]
+    z_end = (N - 1) * c["c"] / (2 * c["fs"])  # 0-degree plane wave: pos = 2 z fs / c
+    z = np.concatenate([np.linspace(0.005e-3, 1.0e-3, 40), np.linspace(z_end - 1.5e-3, z_end + 0.2e-3, 56)])
+    x = np.linspace(-6e-3, 6e-3, 24)
+    rng = np.random.default_rng(3)
+    rf = rng.standard_normal((frames, 1, c["n_el"], N)).astype(np.float32)
+    plan = tb.plane_wave_plan(n_el=c["n_el"], pitch=c["pitch"], fs=c["fs"], c=c["c"], n_samples=N,
+                              x=x, z=z, f_number=c["f_number"])
+    img = tb.das_image(torch.as_tensor(rf).to(DEV), plan).cpu().numpy()
+    ts = plane_t_star(c, x, z, (0.0,))
+    for f in range(frames):
+        A = od.analytic_signal(rf[f].astype(np.float64))
+        ref = od.das_image_vectorized(A, c["fs"], 0.0, x, z, c["pitch"], c["c"], ts, c["f_number"])
+        assert od.rel_l2(img[f], ref) <= 1e-5, f
+    assert img[:, -3:].max() == 0.0  # past the end of the trace: np.interp's right = 0
