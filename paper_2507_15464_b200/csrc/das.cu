@@ -578,9 +578,10 @@ __global__ void __launch_bounds__(256) das_window_kernel(DasParams p, int32_t* _
   using S = DasShape<float>;
   constexpr int WZ = S::WZ, WX = 32 / WZ;
   __shared__ int lo_s, hi_s;
+  constexpr int CG = DAS_NW / S::DG;                 // column groups of warps
   const int lane = threadIdx.x, wid = threadIdx.y;  // 8 warps = the consumer warps of K2
-  const int iz = blockIdx.x * (WZ * S::DG) + wid * WZ + lane / WX;
-  const int ix = blockIdx.y * WX + lane % WX;
+  const int iz = blockIdx.x * (WZ * S::DG) + (wid / CG) * WZ + lane / WX;
+  const int ix = blockIdx.y * (WX * CG) + (wid % CG) * WX + lane % WX;
   const bool pix = (iz < p.nz) && (ix < p.nx);
   const double x = pix ? p.xg[ix] : 0.0;
   const double zm = pix ? p.zg[iz] : 1.0;
@@ -764,7 +765,8 @@ extern "C" int tidas_das_window(const tidas_das_desc_t* d, const double* t_star,
   p.pitch = d->pitch; p.c = d->c; p.fs = d->fs; p.t0 = d->t0; p.f_number = d->f_number;
   p.ap_half = ap_half; p.t_star = t_star; p.xg = x; p.zg = z;
   using S = DasShape<float>;
-  const dim3 grid((d->nz + S::WZ * S::DG - 1) / (S::WZ * S::DG), (d->nx + 32 / S::WZ - 1) / (32 / S::WZ));
+  constexpr int TXC = (32 / S::WZ) * (DAS_NW / S::DG);  // tile columns
+  const dim3 grid((d->nz + S::WZ * S::DG - 1) / (S::WZ * S::DG), (d->nx + TXC - 1) / TXC);
   TIDAS_REQUIRE(grid.y <= 65535, "pixel grid too large");
   if (d->aperture == TIDAS_AP_HANN) das_window_kernel<TIDAS_AP_HANN><<<grid, dim3(32, 8), 0, st>>>(p, max_window);
   else das_window_kernel<TIDAS_AP_REF_BOXCAR><<<grid, dim3(32, 8), 0, st>>>(p, max_window);
