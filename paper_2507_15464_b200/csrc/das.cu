@@ -14,17 +14,19 @@
 //
 // Layout / schedule (B200, FP32 path):
 //   * CTA = 8 consumer warps + 1 producer warp, 3 CTAs per SM. The consumers
-//     cover 32 depths x 8 columns; a warp covers 4 depths x 8 columns, so the
-//     16 lanes of a half-warp (2 depths x 8 columns) read taps within ~16
-//     samples of each other: nearby columns share taps (broadcast) and few
-//     lanes sit 16 samples (one bank period of complex64) apart. Each thread owns one pixel for FB = 8
+//     cover 16 depths x 16 columns (4 warp rows x 2 column groups); a warp
+//     covers 4 depths x 8 columns, so the 16 lanes of a half-warp (2 depths x
+//     8 columns) read taps within ~16 samples of each other: nearby columns
+//     share taps (broadcast) and few lanes sit 16 samples (one bank period of
+//     complex64) apart. Each thread owns one pixel for FB = 8
 //     frames, so the time-of-flight math (FP32, cancellation-free
 //     s = -dx^2 / (sqrt(dx^2 + z^2) + z) in sample units) is paid once per
 //     (pixel, channel) and reused for 8 frames.
 //   * The CTA's sample window per transmit (taps of its 256 pixels lie in
-//     [min k0 - 1, max (k0 - floor(s_min)) + 1], <= 256 samples, the same for
-//     every channel) is fetched by the producer warp as ONE TMA tensor copy
-//     per 2 channels: a box [8 frames][2 channels][256 samples] of the 4-D
+//     [min k0 - 1, max (k0 - floor(s_min)) + 1], the same for every channel;
+//     a square tile keeps it short: <= 131 samples at cfg1-5) is fetched by
+//     the producer warp as ONE TMA tensor copy per 2 channels: a box
+//     [8 frames][2 channels][136 or 256 samples, per plan] of the 4-D
 //     tensor map over the analytic RF [F][A][E][N] (complex64 as 8-byte
 //     elements). Two such buffers rotate under full / empty mbarriers (the
 //     consumers arrive per warp on "empty"), so no CTA-wide barrier sits in
@@ -203,14 +205,14 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
       " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity), "r"(1000000u) : "memory");
 }
 
-// Warp-specialised CTA: warps 0..7 own the 32 x 8 pixel tile (consumers),
+// Warp-specialised CTA: warps 0..7 own the 16 x 16 pixel tile (consumers),
 // warp 8 lane 0 streams the per-channel sample windows with TMA bulk copies
 // (producer). Buffer b is guarded by full[b] (copy landed, tx-count) and
 // empty[b] (all 8 consumer warps done); consumers never meet at a CTA barrier
 // inside the channel loop, so they drift up to DAS_NBUF channels apart.
 // Per-precision tile / staging shape. FP32 (the throughput path): FB = 8 frames
-// per thread, warps of WZ = 4 depths x 8 columns, DG = 8 warp rows (CTA 32 x 8
-// pixels), TMA tensor boxes of [8 frames][CPB = 2 channels][256 samples],
+// per thread, warps of WZ = 4 depths x 8 columns, DG = 4 warp rows x 2 column groups (CTA 16 x 16
+// pixels), TMA tensor boxes of [8 frames][CPB = 2 channels][136 / 256 samples],
 // 32-bit shared-window gathers, deepest-depth-tile-first dispatch (LPT). FP64
 // (the drop-in path, reference semantics): one frame, 1-channel bulk copies.
 // A fixed FB per precision keeps every frame's arithmetic independent of how
@@ -218,7 +220,7 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
 // sharding.
 template <typename R> struct DasShape;
 template <> struct DasShape<float> {
-  static constexpr int FB = 8, DG = 8, WZ = 4, WCAP = 254, CPB = 2;
+  static constexpr int FB = 8, DG = 4, WZ = 4, WCAP = 254, CPB = 2;
   static constexpr bool TMAP = true, U32 = true, LPT = true;
 };
 template <> struct DasShape<double> {
@@ -686,10 +688,13 @@ static int dispatch_fb_box(const DasParams& p, const void* A, void* out, cudaStr
   return launch_das<R, AP, OUT, 3, 2, false, WCAP>(p, A, out, st);
 }
 
-// FP32 staging boxes: the narrow one (200 samples) whenever the plan's windows
-// fit it — fewer TMA bytes (L2 -> shared memory) beside the same gathers:
-// cfg2 K2 4.74 -> 4.66 us/frame, cfg1 / cfg3 / cfg5 +0.7-1.6% (all fit)
-constexpr int DAS_WCAP_NARROW = 198;
+// FP32 staging boxes: the narrow one (136 samples) whenever the plan's tile
+// windows fit it (16 x 16-pixel tiles: cfg1 / 2 / 3 / 5 need 86 / 129 / 104 /
+// 131 samples). The window fill (L2 -> shared memory) is a large share of the
+// kernel's energy: under the board power limit, 32 x 8 tiles with a 200-sample
+// box ran cfg2 at 1897 MHz and 4.81 us/frame, 16 x 16 tiles with this box at
+// 1965 MHz and 4.67 us/frame (tools/power_probe.py)
+constexpr int DAS_WCAP_NARROW = 134;
 
 template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {

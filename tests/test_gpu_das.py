@@ -330,9 +330,12 @@ def test_file_ingest_to_images_through_host_pipeline(tmp_path):
 # ------------------------------------------- plan window sizing (TMA staging box)
 
 
+TILE_Z, TILE_X, NARROW = 16, 16, 134  # K2's FP32 tile and narrow-box capacity (das.cu)
+
+
 def _tile_windows_numpy(cfg, x, z, angles=(0.0,)):
     """Restatement of K2's per-tile sample window (das.cu pixel_aperture /
-    pixel_arrival) over tiles of 32 depths x 8 columns: max over tiles and transmits."""
+    pixel_arrival) over its 16 x 16-pixel tiles: max over tiles and transmits."""
     half = cfg["n_el"] // 2
     X, Z = np.meshgrid(x, z)
     wmax = 0
@@ -347,26 +350,27 @@ def _tile_windows_numpy(cfg, x, z, angles=(0.0,)):
         dxm = np.minimum(a, np.maximum(np.abs((n_lo + 0.5) * cfg["pitch"] - X), np.abs((n_hi + 0.5) * cfg["pitch"] - X)))
         m_min = np.floor((Z - np.hypot(dxm, Z)) / cfg["c"] * cfg["fs"]).astype(np.int64) - 1
         act = (pos >= 0) & (pos <= cfg["n_samples"] - 1) & (n_lo <= n_hi)
-        for i in range(0, Z.shape[0], 32):
-            for j in range(0, Z.shape[1], 8):
-                m = act[i:i + 32, j:j + 8]
+        for i in range(0, Z.shape[0], TILE_Z):
+            for j in range(0, Z.shape[1], TILE_X):
+                sl = (slice(i, i + TILE_Z), slice(j, j + TILE_X))
+                m = act[sl]
                 if m.any():
-                    lo = (k0[i:i + 32, j:j + 8][m] - 1).min()
-                    hi = (k0[i:i + 32, j:j + 8] - m_min[i:i + 32, j:j + 8])[m].max() + 1
+                    lo = (k0[sl][m] - 1).min()
+                    hi = (k0[sl] - m_min[sl])[m].max() + 1
                     wmax = max(wmax, int(hi - lo + 1))
     return wmax
 
 
 def test_plan_window_matches_restatement_and_boxes_are_bitwise_equal():
     """tidas_das_window == the numpy restatement of K2's tile windows (cfg2 grid:
-    194 samples, fits the 200-sample box); images from the narrow and the wide
+    129 samples, fits the 136-sample box); images from the narrow and the wide
     (256) staging box are bitwise identical and match the oracle."""
     cfg = CFG2
     rf, _ = speckle_rf(cfg, seed=11, n_scat=400)
     rf = rf[None].astype(np.float32)
     x, z = grid(cfg)
     img, ref, plan = _plane_case(cfg, rf, cfg["nz"], cfg["nx"])
-    assert plan.window() == _tile_windows_numpy(cfg, x, z) == 194
+    assert plan.window() == _tile_windows_numpy(cfg, x, z) == 129
     assert rel_l2(img, ref) <= FP32_TOL
     plan._window = 0  # unknown: the widest box
     wide = tb.das_image(torch.as_tensor(rf).to(DEV), plan).cpu().numpy()
@@ -375,7 +379,7 @@ def test_plan_window_matches_restatement_and_boxes_are_bitwise_equal():
 
 @pytest.mark.parametrize("nz, forced", [(384, None), (384, 100), (512, 100)])
 def test_plan_window_wide_and_underestimated(nz, forced):
-    """A grid whose tile windows exceed the narrow box (nz = 384: ~238 samples)
+    """A grid whose tile windows exceed the narrow box (nz = 384: ~150 samples)
     takes the wide box; an underestimated window (forced) picks the narrow box
     and the wider tiles gather from global memory — exact either way."""
     cfg = CFG2
@@ -386,7 +390,7 @@ def test_plan_window_wide_and_underestimated(nz, forced):
                               n_samples=rf.shape[-1], x=x, z=z, f_number=cfg["f_number"])
     assert plan.window() == _tile_windows_numpy(cfg, x, z)
     if nz == 384:
-        assert 198 < plan.window() <= 254
+        assert NARROW < plan.window() <= 254
     if forced is not None:
         plan._window = forced
     img = tb.das_image(torch.as_tensor(rf).to(DEV), plan).cpu().numpy()
@@ -406,4 +410,4 @@ def test_plan_window_cfg3_steered_and_cfg5():
                                   f_number=cfg["f_number"], out="coherent" if len(angles) > 1 else "envelope")
         w = plan.window()
         assert w == _tile_windows_numpy(cfg, x, z, angles)
-        assert 0 < w <= 198
+        assert 0 < w <= NARROW

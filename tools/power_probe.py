@@ -1,6 +1,6 @@
 """Board power and SM clock (NVML) in the power-capped steady state of the cfg2
 DAS kernels: K1 + K2, K1 alone, K2 alone (256 frames per call, 1.5 s of load
-then a 1 s window).  python tools/power_probe.py"""
+then a 1 s window).  python tools/power_probe.py [lib.so]"""
 import json
 import statistics
 import sys
@@ -15,6 +15,10 @@ import bench  # noqa: E402
 import paper_2507_15464_b200 as tb  # noqa: E402
 
 import pynvml  # noqa: E402
+
+if len(sys.argv) > 1:  # a variant library (tools/build_variant.sh)
+    from paper_2507_15464_b200 import _lib
+    _lib.load(Path(sys.argv[1]))
 
 pynvml.nvmlInit()
 H = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
