@@ -673,21 +673,6 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
   return TIDAS_OK;
 }
 
-// Buffers / occupancy per plan (measured on B200, DESIGN.md §4): single-transmit
-// envelope images (cfg1 / 2 / 5) compile the transmit loop without live frame
-// accumulators and run 2 window buffers at 3 CTAs / SM (the kernel is
-// latency-bound once the bank conflicts are gone); complex outputs (cfg3
-// coherent: folded accumulation, few registers) also run 2 buffers at 3 CTAs /
-// SM; multi-transmit envelope compounding keeps c0 / c1 and the frame
-// accumulators live across transmits and runs 3 buffers at 2 CTAs / SM. The
-// choice depends on the plan only, never on the frame count.
-template <typename R, int AP, int OUT, int WCAP>
-static int dispatch_fb_box(const DasParams& p, const void* A, void* out, cudaStream_t st) {
-  if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1) return launch_das<R, AP, OUT, 2, 3, true, WCAP>(p, A, out, st);
-  if (OUT != TIDAS_OUT_ENVELOPE) return launch_das<R, AP, OUT, 2, 3, false, WCAP>(p, A, out, st);
-  return launch_das<R, AP, OUT, 3, 2, false, WCAP>(p, A, out, st);
-}
-
 // FP32 staging boxes: the narrow one (136 samples) whenever the plan's tile
 // windows fit it (16 x 16-pixel tiles: cfg1 / 2 / 3 / 5 need 86 / 129 / 104 /
 // 131 samples). The window fill (L2 -> shared memory) is a large share of the
@@ -695,6 +680,25 @@ static int dispatch_fb_box(const DasParams& p, const void* A, void* out, cudaStr
 // box ran cfg2 at 1897 MHz and 4.81 us/frame, 16 x 16 tiles with this box at
 // 1965 MHz and 4.67 us/frame (tools/power_probe.py)
 constexpr int DAS_WCAP_NARROW = 134;
+
+// Buffers / occupancy per plan (measured on B200, DESIGN.md §4): single-transmit
+// envelope images (cfg1 / 2 / 5) compile the transmit loop without live frame
+// accumulators and run at 3 CTAs / SM (the kernel is latency-bound once the bank
+// conflicts are gone); complex outputs (cfg3 coherent: folded accumulation, few
+// registers) also run at 3 CTAs / SM — both with 3 window buffers in the narrow
+// box (3 x 17 KB per CTA; cfg2 K2 4.67 -> 4.55 us/frame, cfg3 +1%) and 2 in the
+// wide one (3 x 32 KB would leave room for 2 CTAs only); multi-transmit envelope
+// compounding keeps c0 / c1 and the frame accumulators live across transmits and
+// runs 3 buffers at 2 CTAs / SM. The choice depends on the plan only, never on
+// the frame count.
+template <typename R, int AP, int OUT, int WCAP>
+static int dispatch_fb_box(const DasParams& p, const void* A, void* out, cudaStream_t st) {
+  constexpr int NB = WCAP <= DAS_WCAP_NARROW ? 3 : 2;
+  if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1) return launch_das<R, AP, OUT, NB, 3, true, WCAP>(p, A, out, st);
+  if (OUT != TIDAS_OUT_ENVELOPE) return launch_das<R, AP, OUT, NB, 3, false, WCAP>(p, A, out, st);
+  return launch_das<R, AP, OUT, 3, 2, false, WCAP>(p, A, out, st);
+}
+
 
 template <typename R, int AP, int OUT>
 static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_t st) {
