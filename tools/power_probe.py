@@ -1,6 +1,7 @@
 """Board power and SM clock (NVML) in the power-capped steady state of the cfg2
 DAS kernels: K1 + K2, K1 alone, K2 alone (256 frames per call, 1.5 s of load
-then a 1 s window).  python tools/power_probe.py [lib.so]"""
+then a 1 s window).  python tools/power_probe.py [lib.so] [--rowconv]
+(--rowconv: the cfg4 row operator instead, microseconds per map)"""
 import json
 import statistics
 import sys
@@ -16,9 +17,10 @@ import paper_2507_15464_b200 as tb  # noqa: E402
 
 import pynvml  # noqa: E402
 
-if len(sys.argv) > 1:  # a variant library (tools/build_variant.sh)
+LIB = [a for a in sys.argv[1:] if not a.startswith("--")]
+if LIB:  # a variant library (tools/build_variant.sh)
     from paper_2507_15464_b200 import _lib
-    _lib.load(Path(sys.argv[1]))
+    _lib.load(Path(LIB[0]))
 
 pynvml.nvmlInit()
 H = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
@@ -40,9 +42,21 @@ def sample(stop, out):
         stop.wait(0.05)
 
 
-for name, fn in (("K1+K2", lambda: tb.das_image(rf, plan, out=img)),
-                 ("K1", lambda: tb.rf_analytic(rf, "f32", out=an)),
-                 ("K2", lambda: tb.das_from_analytic(an, plan, out=img))):
+cases = [("K1+K2", lambda: tb.das_image(rf, plan, out=img)),
+         ("K1", lambda: tb.rf_analytic(rf, "f32", out=an)),
+         ("K2", lambda: tb.das_from_analytic(an, plan, out=img))]
+if "--rowconv" in sys.argv:  # cfg4 row operator (256 maps): forward on sparse maps, adjoint on its dense output
+    del rf, an, img
+    g = torch.Generator(device="cuda").manual_seed(3)
+    maps = (torch.rand((256, 2048, 1024), device="cuda", generator=g) < 0.02).float() * \
+        torch.randn((256, 2048, 1024), device="cuda", generator=g)
+    Kr = torch.randn((2048, 129), device="cuda", generator=g) / 16
+    yv, av = torch.empty_like(maps), torch.empty_like(maps)
+    tb.tidas_rowconv(maps, Kr, out=yv)
+    F = 256  # per-call units: maps
+    cases = [("rowconv fwd (cfg4, sparse maps)", lambda: tb.tidas_rowconv(maps, Kr, out=yv)),
+             ("rowconv adj (cfg4, dense input)", lambda: tb.tidas_rowconv_adjoint(yv, Kr, out=av))]
+for name, fn in cases:
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < 1.5:
         fn()
