@@ -1,7 +1,8 @@
 """Board power and SM clock (NVML) in the power-capped steady state of the cfg2
 DAS kernels: K1 + K2, K1 alone, K2 alone (256 frames per call, 1.5 s of load
 then a 1 s window).  python tools/power_probe.py [lib.so] [--rowconv]
-(--rowconv: the cfg4 row operator instead, microseconds per map)"""
+(--rowconv: the cfg4 row operator instead, microseconds per map; --cfg5: the
+cfg5 DAS path, 64 int16 frames per call)"""
 import json
 import statistics
 import sys
@@ -45,6 +46,22 @@ def sample(stop, out):
 cases = [("K1+K2", lambda: tb.das_image(rf, plan, out=img)),
          ("K1", lambda: tb.rf_analytic(rf, "f32", out=an)),
          ("K2", lambda: tb.das_from_analytic(an, plan, out=img))]
+if "--cfg5" in sys.argv:  # cfg5: 64 int16 frames of 192 x 8192 -> 1024 x 1024 (µs per frame)
+    del rf, an, img
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    import numpy as np
+    from bench_configs import CFGS, make_rf
+    c5 = CFGS["cfg5"]
+    F = 64
+    rf = make_rf("cfg5", c5, list(range(F)))
+    plan = tb.plane_wave_plan(n_el=c5["n_el"], pitch=c5["pitch"], fs=c5["fs"], c=1540.0, n_samples=c5["N"],
+                              x=np.linspace(*c5["x"], c5["nx"]), z=np.linspace(*c5["z"], c5["nz"]),
+                              f_number=1.5)
+    an = tb.rf_analytic(rf, "f32")
+    img = torch.empty((F, c5["nz"], c5["nx"]), device="cuda")
+    cases = [("cfg5 K1+K2", lambda: tb.das_image(rf, plan, out=img)),
+             ("cfg5 K1", lambda: tb.rf_analytic(rf, "f32", out=an)),
+             ("cfg5 K2", lambda: tb.das_from_analytic(an, plan, out=img))]
 if "--rowconv" in sys.argv:  # cfg4 row operator (256 maps): forward on sparse maps, adjoint on its dense output
     del rf, an, img
     g = torch.Generator(device="cuda").manual_seed(3)
