@@ -114,7 +114,7 @@ class Clocks:
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw.instant,power.limit")
 
     def __init__(self, index: int):
         self.index, self.proc, self.path = index, None, None
@@ -143,14 +143,22 @@ class Clocks:
         if self.proc is None or not self.path:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         rows = [p for p in ([q.strip() for q in ln.split(",")] for ln in Path(self.path).read_text().splitlines())
-                if len(p) == 6 and p[0].isdigit()]
+                if len(p) == 8 and p[0].isdigit()]
         os.unlink(self.path)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        power = [x for x in (num(r[6]) for r in rows) if x is not None]
         return {"sm_mhz": statistics.median(int(r[0]) for r in rows), "sm_max_mhz": int(rows[0][1]),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows),
+                # board power over the same window (the steady state is power-limited when it sits at the limit)
+                "power_w": statistics.median(power) if power else None, "power_limit_w": num(rows[0][7])}
 
 
 def grid(cfg):
