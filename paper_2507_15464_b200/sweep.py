@@ -271,21 +271,21 @@ def error_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, rx_rule:
         sh_c = np.zeros((C, A))
         clo = np.zeros(C, np.int32)
         chi = np.zeros(C, np.int32)
-        start = 0
+        # np.nonzero walks row-major: the cells of column t are the contiguous run t_sel == t
+        bounds = np.searchsorted(t_sel, np.arange(Tb + 1))
         for t in range(Tb):
-            m = r_sel[t_sel == t]
-            if m.size == 0:
+            a, b = int(bounds[t]), int(bounds[t + 1])
+            if a == b:
                 continue
             n = len(idx[t])
-            d = d_fix[t][m]  # (k, n)
-            sl = slice(start, start + m.size)
-            rows_c[sl, :n] = t * n_el + idx[t] + half
-            sh_c[sl, :n] = d * fs
+            d = d_fix[t][r_sel[a:b]]  # (k, n)
+            rows_c[a:b, :n] = t * n_el + idx[t] + half
+            sh_c[a:b, :n] = d * fs
             span = np.ceil(-d.min(axis=1) * fs).astype(np.int64) + 2
-            clo[sl] = np.maximum(int(cols.wlo[t]) - span, 0)
-            chi[sl] = min(int(cols.whi[t]) + 2, int(cols.n_len[t]))
-            start += m.size
-        _das._count(int(sum(len(idx[t]) for t in t_sel)))
+            clo[a:b] = np.maximum(int(cols.wlo[t]) - span, 0)
+            chi[a:b] = min(int(cols.whi[t]) + 2, int(cols.n_len[t]))
+        lens = np.fromiter((len(i) for i in idx), np.int64, count=Tb)
+        _das._count(int(lens[t_sel].sum()))
         sums = _das._delayed_sums_dev(cols.flat, rows_c, sh_c, lo=clo, hi=chi)
         th_d = _f64(th[t_sel, r_sel], dev)
         cc_d = _i32(t_sel, dev)
