@@ -89,11 +89,13 @@ class DasPlan:
 
     def window(self) -> int:
         """Largest per-tile sample window of the plan (tidas_das_window, the
-        same logic K2 runs), measured once: K2 stages windows in the narrowest
-        TMA box that holds it."""
+        same logic K2 runs), measured once (plans are treated as immutable; a
+        stale value only costs speed — wider tiles take K2's global-gather
+        path): K2 stages windows in the narrowest TMA box that holds it."""
         if self._window is None:
             d = _lib.DasDesc()
             d.n_frames, d.n_angles, d.n_el, d.n_samples = 0, self.n_angles, self.n_el, self.n_samples
+            d.out_mode, d.prec = OUT_MODES[self.out], self.prec_code
             d.nx, d.nz = self.nx, self.nz
             d.pitch, d.c, d.fs, d.t0 = self.pitch, self.c, self.fs, self.t0
             if self.aperture[0] == "hann":
