@@ -326,6 +326,8 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
   const double zm = pix ? p.zg[iz] : 1.0;
   PixelGeo<R> geo;
   geo.init(p, x, zm);
+  float geo_a = 0.0f;  // FP32 Hann half-width in samples; per transmit, -1 marks an inactive pixel
+  if constexpr (sizeof(R) == 4) geo_a = geo.a;
 
   // receive aperture of this pixel and its most negative shift
   int n_lo, n_hi, ap_h, m_min;
@@ -388,7 +390,9 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
     const int w_lo = rw[0], w_hi = rw[1];
     if (w_hi < w_lo || c_lo > c_hi) continue;  // CTA-uniform
     const int W = w_hi - w_lo + 1;
-    const bool staged = W <= WCAP;
+    // staging needs 16-byte aligned rows (bulk / tensor copies): complex64 rows
+    // of odd length alternate 8-byte alignment, so those plans gather from global
+    const bool staged = W <= WCAP && (sizeof(C) == 16 || (p.N & 1) == 0);
     // element e of a staged window is sample (s0 + e) mod N of the channel row
     // (s0 even: every bulk copy is 16-byte aligned); per frame one or two
     // (wrap-around) bulk copies
@@ -468,7 +472,10 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
       float dnf = 0.0f;
       if constexpr (sizeof(R) == 4) {
         dnf = (float)(c_lo - geo.nref);
-        if (AP == TIDAS_AP_HANN && !active_px) geo.a = -1.0f;  // no tap passes |dx| < a
+        // no tap passes |dx| < a for a pixel off the trace in THIS transmit (set per
+        // transmit: a pixel can be on the trace for one steering angle and off it
+        // for another)
+        if (AP == TIDAS_AP_HANN) geo.a = active_px ? geo_a : -1.0f;
       }
       // channels outside every lane's aperture skip the tap math (warp-uniform)
       const int wn_lo = __reduce_min_sync(0xffffffffu, active_px ? n_lo : INT_MAX);
@@ -629,7 +636,8 @@ static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t
   auto kern = das_image_kernel<R, AP, OUT, DAS_NBUF, MINB, ONE_TX, WCAP>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
-  if constexpr (S::TMAP) {
+  // odd rows cannot be staged (16-byte copies; the kernel gathers from global)
+  if constexpr (S::TMAP) if ((p.N & 1) == 0) {
     static_assert(sizeof(C) == 8 && WCAP + 2 <= 256, "tensor path: complex64, box <= 256");
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
