@@ -37,6 +37,11 @@ enum tidas_aperture {
   TIDAS_AP_REF_BOXCAR = 0, /* array-centred boxcar, per-depth half count (geometry.py:188-199) */
   TIDAS_AP_HANN = 1        /* pixel-centred Hann, half-width z / (2 F#) (north star) */
 };
+/* FP32 receive-shift arithmetic (K2) */
+enum tidas_geometry {
+  TIDAS_GEO_FAST = 0,   /* FP32 shifts: ~1e-5 of a sample at |shift| ~ 100s of samples */
+  TIDAS_GEO_REFINED = 1 /* + one float64 Newton step: fraction to FP32 resolution (~7% K2 time) */
+};
 /* pixel value */
 enum tidas_out {
   TIDAS_OUT_ENVELOPE = 0, /* (1-f)|C(k0)| + f|C(k0+1)| per transmit, summed (das.py:165-193) */
@@ -102,6 +107,7 @@ typedef struct {
   int32_t window;     /* largest per-tile sample window of the plan (tidas_das_window);
                          0 = unknown: the widest FP32 staging box (256 samples) is used.
                          A too-small value is still exact (wider tiles gather from global). */
+  int32_t geometry;   /* enum tidas_geometry (PREC_F32; PREC_F64 is float64 throughout) */
 } tidas_das_desc_t;
 
 /*

@@ -19,6 +19,7 @@ F64, F32, I16 = 0, 1, 2
 PREC_F32, PREC_F64 = 0, 1
 AP_REF_BOXCAR, AP_HANN = 0, 1
 OUT_ENVELOPE, OUT_COHERENT, OUT_IQ = 0, 1, 2
+GEO_FAST, GEO_REFINED = 0, 1
 ROWCONV_PATHS = {"auto": 0, "tensor": 1, "simt": 2}
 
 DTYPE_CODE = {torch.float64: F64, torch.float32: F32, torch.int16: I16}
@@ -30,7 +31,7 @@ class DasDesc(C.Structure):
         ("n_samples", C.c_int32), ("nx", C.c_int32), ("nz", C.c_int32),
         ("pitch", C.c_double), ("c", C.c_double), ("fs", C.c_double), ("t0", C.c_double),
         ("aperture", C.c_int32), ("f_number", C.c_double), ("out_mode", C.c_int32),
-        ("prec", C.c_int32), ("window", C.c_int32),
+        ("prec", C.c_int32), ("window", C.c_int32), ("geometry", C.c_int32),
     ]
 
 

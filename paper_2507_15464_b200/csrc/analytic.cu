@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(1024, 1) analytic_pow2_kernel(const In* __rest
   const bool has_b = !DELAY && (ra + 1 < n_rows);
   const In* src_a = rf + ra * stride;
   const In* src_b = rf + (ra + 1) * stride;
-  if (threadIdx.x < 2) { first_nz[threadIdx.x] = N; last_nz[threadIdx.x] = -1; }
+  // (a one-thread CTA — N = 16 at 16 samples per thread — initialises both channels)
+  for (int c = threadIdx.x; c < 2; c += NT) { first_nz[c] = N; last_nz[c] = -1; }
   int lo_a = N, hi_a = -1, lo_b = N, hi_b = -1;
   // N == blockDim.x * EPT: every thread owns EPT samples per row; all loads are
   // issued before the first use so their latencies overlap

@@ -42,6 +42,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -53,6 +54,8 @@ struct DasParams {
   int F, A, E, N, nx, nz;
   int window;  // largest per-CTA sample window of the plan (tidas_das_window), 0 = unknown
   double pitch, c, fs, t0, f_number;
+  double pitch_s;  // pitch in sample units (pitch fs / c)
+  int geometry;    // TIDAS_GEO_*: FP32 receive shifts as computed, or float64-refined
   const int32_t* ap_half;
   const double* t_star;
   const double* xg;
@@ -100,10 +103,21 @@ template <typename R> struct Tap {
 
 // Pixel geometry in the units each precision computes in.
 template <typename R> struct PixelGeo;
+template <bool PG> struct PixelGeoF;
 
-template <> struct PixelGeo<float> {
-  // sample units (metres * fs / c)
-  float z, z2, a, pia, dxref, pitch;
+// FP32: sample units (metres * fs / c). PG (the plan's TIDAS_GEO_REFINED): the
+// receive shift s = D_n fs carries a few FP32 roundings of its own magnitude
+// (|s| reaches hundreds of samples at wide apertures: ~1e-5 of a sample, which
+// full-band RF turns into ~1e-5 of the image); one Newton step on
+//   g(s) = s^2 - 2 z s - dx^2 = 0   (r = z - s, r^2 = z^2 + dx^2)
+// with the residual in float64, s* = s + g(s) / (2 r), gives the interpolation
+// fraction to FP32 resolution of [0, 1). The sample index keeps floor(s): when
+// s* crosses an integer the fraction leaves [0, 1) by at most a few 1e-5 and the
+// linear interpolation extends over the neighbouring interval (continuous in s).
+template <bool PG> struct PixelGeoF {
+  float z, z2, a, pia;
+  float dxref, pitch;  // !PG: x_nref - x and the pitch
+  double dx0, z2x;     // PG: x_nref - x and 2 z in float64
   int nref;
   __device__ void init(const DasParams& p, double x, double z_m) {
     const double k = p.fs / p.c;
@@ -111,20 +125,33 @@ template <> struct PixelGeo<float> {
     z2 = z * z;
     a = (float)(z_m / (2.0 * p.f_number) * k);
     pia = 3.14159265358979f / a;
-    pitch = (float)(p.pitch * k);
     const int half = p.E / 2;
     int nr = (int)rint(x / p.pitch - 0.5);
     nr = max(-half, min(half - 1, nr));
     nref = nr;
-    dxref = (float)((((double)nr + 0.5) * p.pitch - x) * k);
+    if constexpr (PG) {
+      dx0 = (((double)nr + 0.5) * p.pitch - x) * k;
+      z2x = 2.0 * z_m * k;
+    } else {
+      pitch = (float)(p.pitch * k);
+      dxref = (float)((((double)nr + 0.5) * p.pitch - x) * k);
+    }
   }
   // dn = n - nref as a float (the caller steps it by 1.0f per channel, exact)
   template <int AP>
-  __device__ __forceinline__ void tap(const DasParams&, float dn, int k0, bool in_ap, Tap<float>& t) const {
-    const float dx = fmaf(dn, pitch, dxref);  // x_n - x
+  __device__ __forceinline__ void tap(const DasParams& p, float dn, int k0, bool in_ap, Tap<float>& t) const {
+    float dx;
+    double dxd = 0.0;
+    if constexpr (PG) {
+      dxd = fma((double)dn, p.pitch_s, dx0);  // x_n - x
+      dx = (float)dxd;
+    } else {
+      dx = fmaf(dn, pitch, dxref);
+    }
     const float q = dx * dx;
     const float rr = q + z2;
-    const float r = rr * rsqrtf(rr);
+    const float rs = rsqrtf(rr);
+    const float r = rr * rs;
     const float s = -__fdividef(q, r + z);  // D_n fs, cancellation-free, |s| < 2^22
     // floor(s) on the FMA/ALU pipes instead of FRND + F2I (XU): round to the
     // nearest integer with the 1.5 * 2^23 magic constant, step down if above s
@@ -132,7 +159,11 @@ template <> struct PixelGeo<float> {
     int mi = __float_as_int(tb) - 0x4B400000;
     float m = tb - 12582912.0f;
     if (m > s) { m -= 1.0f; --mi; }
-    const float mu = s - m;
+    float mu = s - m;
+    if constexpr (PG) {
+      const double sd = (double)s;
+      mu = fmaf((float)fma(sd, sd - z2x, -dxd * dxd), 0.5f * rs, mu);
+    }
     float w;
     if (AP == TIDAS_AP_HANN) {  // |dx| < a also encodes the aperture and pixel activity
       w = (fabsf(dx) < a) ? fmaf(0.5f, __cosf(dx * pia), 0.5f) : 0.0f;
@@ -282,7 +313,7 @@ __device__ __forceinline__ bool pixel_arrival(const DasParams& p, bool pix, int 
 // WCAP_T: the staging box holds WCAP_T + 2 samples per (frame, channel); CTAs
 // whose window is wider gather from global memory instead (slow, exact). The
 // plan's measured window picks the narrowest compiled box that holds it.
-template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX, int WCAP_T>
+template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX, int WCAP_T, bool PG>
 __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasParams p,
                                                                        const cplx<R>* __restrict__ A,
                                                                        void* __restrict__ out_,
@@ -324,7 +355,7 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
 
   const double x = pix ? p.xg[ix] : 0.0;
   const double zm = pix ? p.zg[iz] : 1.0;
-  PixelGeo<R> geo;
+  std::conditional_t<sizeof(R) == 4, PixelGeoF<PG>, PixelGeo<double>> geo;
   geo.init(p, x, zm);
   float geo_a = 0.0f;  // FP32 Hann half-width in samples; per transmit, -1 marks an inactive pixel
   if constexpr (sizeof(R) == 4) geo_a = geo.a;
@@ -628,12 +659,13 @@ __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double
   out[i] = (x[ix] * sn + z[iz] * cs + origin) / c + z[iz] / c;
 }
 
-template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX, int WCAP = DasShape<R>::WCAP>
+template <typename R, int AP, int OUT, int DAS_NBUF, int MINB, bool ONE_TX, int WCAP = DasShape<R>::WCAP,
+          bool PG = false>
 static int launch_das(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   using C = cplx<R>;
   using S = DasShape<R>;
   constexpr int FB = S::FB, DG = S::DG, WZ = S::WZ, CPB = S::CPB, NW = DAS_NW;
-  auto kern = das_image_kernel<R, AP, OUT, DAS_NBUF, MINB, ONE_TX, WCAP>;
+  auto kern = das_image_kernel<R, AP, OUT, DAS_NBUF, MINB, ONE_TX, WCAP, PG>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   // odd rows cannot be staged (16-byte copies; the kernel gathers from global)
@@ -699,12 +731,21 @@ constexpr int DAS_WCAP_NARROW = 134;
 // compounding keeps c0 / c1 and the frame accumulators live across transmits and
 // runs 3 buffers at 2 CTAs / SM. The choice depends on the plan only, never on
 // the frame count.
-template <typename R, int AP, int OUT, int WCAP>
+template <typename R, int AP, int OUT, int WCAP, bool PG>
 static int dispatch_fb_box(const DasParams& p, const void* A, void* out, cudaStream_t st) {
   constexpr int NB = WCAP <= DAS_WCAP_NARROW ? 3 : 2;
-  if (OUT == TIDAS_OUT_ENVELOPE && p.A == 1) return launch_das<R, AP, OUT, NB, 3, true, WCAP>(p, A, out, st);
-  if (OUT != TIDAS_OUT_ENVELOPE) return launch_das<R, AP, OUT, NB, 3, false, WCAP>(p, A, out, st);
-  return launch_das<R, AP, OUT, 3, 2, false, WCAP>(p, A, out, st);
+  if constexpr (OUT != TIDAS_OUT_ENVELOPE) {
+    return launch_das<R, AP, OUT, NB, 3, false, WCAP, PG>(p, A, out, st);
+  } else {
+    if (p.A == 1) return launch_das<R, AP, OUT, NB, 3, true, WCAP, PG>(p, A, out, st);
+    return launch_das<R, AP, OUT, 3, 2, false, WCAP, PG>(p, A, out, st);
+  }
+}
+
+template <typename R, int AP, int OUT, bool PG>
+static int dispatch_fb_geo(const DasParams& p, const void* A, void* out, cudaStream_t st) {
+  if (p.window > 0 && p.window <= DAS_WCAP_NARROW) return dispatch_fb_box<R, AP, OUT, DAS_WCAP_NARROW, PG>(p, A, out, st);
+  return dispatch_fb_box<R, AP, OUT, DasShape<R>::WCAP, PG>(p, A, out, st);
 }
 
 
@@ -713,8 +754,8 @@ static int dispatch_fb(const DasParams& p, const void* A, void* out, cudaStream_
   if constexpr (sizeof(R) == 8) {
     return launch_das<R, AP, OUT, 4, 3, false>(p, A, out, st);
   } else {
-    if (p.window > 0 && p.window <= DAS_WCAP_NARROW) return dispatch_fb_box<R, AP, OUT, DAS_WCAP_NARROW>(p, A, out, st);
-    return dispatch_fb_box<R, AP, OUT, DasShape<R>::WCAP>(p, A, out, st);
+    if (p.geometry == TIDAS_GEO_REFINED) return dispatch_fb_geo<R, AP, OUT, true>(p, A, out, st);
+    return dispatch_fb_geo<R, AP, OUT, false>(p, A, out, st);
   }
 }
 
@@ -750,13 +791,17 @@ extern "C" int tidas_das_image(const tidas_das_desc_t* d, const void* analytic, 
   TIDAS_REQUIRE(d->fs > 0 && d->c > 0 && d->pitch > 0, "fs, c, pitch must be positive");
   TIDAS_REQUIRE(d->aperture != TIDAS_AP_REF_BOXCAR || ap_half, "REF_BOXCAR needs ap_half");
   TIDAS_REQUIRE(d->aperture != TIDAS_AP_HANN || d->f_number > 0, "f_number must be positive");
+  TIDAS_REQUIRE(d->geometry == TIDAS_GEO_FAST || d->geometry == TIDAS_GEO_REFINED, "unknown geometry %d",
+                d->geometry);
   if (d->n_frames == 0 || d->nx == 0 || d->nz == 0) return TIDAS_OK;
   DasParams p;
   p.F = d->n_frames; p.A = d->n_angles; p.E = d->n_el; p.N = d->n_samples;
   p.nx = d->nx; p.nz = d->nz;
   p.pitch = d->pitch; p.c = d->c; p.fs = d->fs; p.t0 = d->t0; p.f_number = d->f_number;
+  p.pitch_s = d->pitch * d->fs / d->c;
   p.ap_half = ap_half; p.t_star = t_star; p.xg = x; p.zg = z;
   p.window = d->window;
+  p.geometry = d->geometry;
   cudaStream_t st = as_stream(stream);
   if (d->prec == TIDAS_PREC_F32) return dispatch_ap<float>(d, p, analytic, out, st);
   if (d->prec == TIDAS_PREC_F64) return dispatch_ap<double>(d, p, analytic, out, st);
@@ -780,6 +825,7 @@ extern "C" int tidas_das_window(const tidas_das_desc_t* d, const double* t_star,
   memset(&p, 0, sizeof(p));
   p.A = d->n_angles; p.E = d->n_el; p.N = d->n_samples; p.nx = d->nx; p.nz = d->nz;
   p.pitch = d->pitch; p.c = d->c; p.fs = d->fs; p.t0 = d->t0; p.f_number = d->f_number;
+  p.pitch_s = d->pitch * d->fs / d->c;
   p.ap_half = ap_half; p.t_star = t_star; p.xg = x; p.zg = z;
   using S = DasShape<float>;
   constexpr int TXC = (32 / S::WZ) * (DAS_NW / S::DG);  // tile columns

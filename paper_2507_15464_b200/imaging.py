@@ -25,6 +25,7 @@ from . import _lib
 _COMPLEX = {_lib.PREC_F32: torch.complex64, _lib.PREC_F64: torch.complex128}
 _REAL = {_lib.PREC_F32: torch.float32, _lib.PREC_F64: torch.float64}
 OUT_MODES = {"envelope": _lib.OUT_ENVELOPE, "coherent": _lib.OUT_COHERENT, "iq": _lib.OUT_IQ}
+GEOMETRIES = {"fast": _lib.GEO_FAST, "refined": _lib.GEO_REFINED}
 
 
 @dataclass
@@ -34,7 +35,11 @@ class DasPlan:
     n_el, pitch [m], fs [Hz], c [m/s], n_samples: acquisition;
     x [nx], z [nz]: pixel grid [m]; t_star [A][nz][nx]: expected arrival per
     transmit (float64, seconds); aperture: ("hann", f_number) or
-    ("ref", ap_half[nz]); out: "envelope" | "coherent" | "iq"; prec: "f32" | "f64".
+    ("ref", ap_half[nz]); out: "envelope" | "coherent" | "iq"; prec: "f32" | "f64";
+    geometry (FP32 plans): "fast" — receive shifts in FP32, ~1e-5 of a sample
+    at shifts of hundreds of samples, which full-band RF turns into up to ~1e-5
+    relative image error — or "refined": one float64 Newton step per shift
+    (fraction to FP32 resolution, ~7% more K2 time at cfg2).
     """
 
     n_el: int
@@ -51,8 +56,13 @@ class DasPlan:
     t0: float = 0.0
     ap_half: Optional[torch.Tensor] = None
     chunk_bytes: int = 1 << 30
+    geometry: str = "fast"
     _desc: Optional[_lib.DasDesc] = field(default=None, repr=False)
     _window: Optional[int] = field(default=None, repr=False)
+
+    def __post_init__(self):
+        if self.geometry not in GEOMETRIES:
+            raise ValueError(f"geometry must be one of {sorted(GEOMETRIES)}, got {self.geometry!r}")
 
     @property
     def n_angles(self) -> int:
@@ -85,6 +95,7 @@ class DasPlan:
         d.out_mode = OUT_MODES[self.out]
         d.prec = self.prec_code
         d.window = self.window() if self.prec == "f32" else 0
+        d.geometry = GEOMETRIES[self.geometry]
         return d
 
     def window(self) -> int:
@@ -119,7 +130,7 @@ def _dev(a, dtype, device) -> torch.Tensor:
 def plane_wave_plan(*, n_el: int, pitch: float, fs: float, c: float, n_samples: int,
                     x: Sequence[float], z: Sequence[float], angles: Sequence[float] = (0.0,),
                     f_number: float = 1.5, out: str = "envelope", prec: str = "f32",
-                    device=None) -> DasPlan:
+                    geometry: str = "fast", device=None) -> DasPlan:
     """Plan for steered plane-wave transmits and the pixel-centred Hann F# aperture.
 
     The arrival table t*[a][iz][ix] is built on the device in float64
@@ -134,12 +145,12 @@ def plane_wave_plan(*, n_el: int, pitch: float, fs: float, c: float, n_samples: 
         _lib.ptr(xd), xd.numel(), _lib.ptr(zd), zd.numel(), _lib.ptr(ad), ad.numel(), n_el,
         float(pitch), float(c), _lib.ptr(ts), _lib.stream_handle()))
     return DasPlan(n_el=n_el, pitch=pitch, fs=fs, c=c, n_samples=n_samples, x=xd, z=zd,
-                   t_star=ts, aperture=("hann", float(f_number)), out=out, prec=prec)
+                   t_star=ts, aperture=("hann", float(f_number)), out=out, prec=prec, geometry=geometry)
 
 
 def table_plan(*, n_el: int, pitch: float, fs: float, c: float, n_samples: int, x, z,
                t_star: np.ndarray, aperture: tuple, out: str = "envelope", prec: str = "f64",
-               t0: float = 0.0, device=None) -> DasPlan:
+               t0: float = 0.0, geometry: str = "fast", device=None) -> DasPlan:
     """Plan with a host-computed arrival table (e.g. the reference's focused
     transmit, das.py:135-137) and either aperture ("ref", ap_half[nz]) or
     ("hann", f_number)."""
@@ -153,7 +164,7 @@ def table_plan(*, n_el: int, pitch: float, fs: float, c: float, n_samples: int, 
     return DasPlan(n_el=n_el, pitch=pitch, fs=fs, c=c, n_samples=n_samples,
                    x=_dev(x, torch.float64, device), z=_dev(z, torch.float64, device),
                    t_star=_dev(ts, torch.float64, device), aperture=aperture, out=out,
-                   prec=prec, t0=t0, ap_half=ap_half)
+                   prec=prec, t0=t0, ap_half=ap_half, geometry=geometry)
 
 
 def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=None,

@@ -48,6 +48,20 @@ def test_analytic_bluestein_any_length(n, rng):
     assert np.max(np.abs(got32 - ref)) / np.max(np.abs(ref)) < 5e-6
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_analytic_support_scan_sixteen_samples(prec):
+    # N = 16 in FP64 runs one thread per CTA (16 samples per thread): both
+    # channels' support slots must still be initialised (found by the K1 fuzz test)
+    x = np.zeros((4, 16))
+    x[0, 3] = 1.0
+    x[1, 0:2] = -1.0
+    x[3, 15] = 2.0
+    sup = torch.full((4, 2), 99, dtype=torch.int32, device=DEV)
+    got = tb.rf_analytic(torch.as_tensor(x).to(DEV), prec, support=sup).cpu().numpy()
+    assert sup.cpu().tolist() == [[3, 3], [0, 1], [-1, -1], [15, 15]]
+    assert np.max(np.abs(got - od.analytic_signal(x))) < (1e-13 if prec == "f64" else 1e-6)
+
+
 def test_analytic_support_scan():
     x = np.zeros((3, 64))
     x[0, 10:20] = 1.0
