@@ -279,6 +279,33 @@ int tidas_psf_errors_f64(const double* sums, int32_t n_samples, const double* th
                          const int32_t* crop_hi, const int32_t* n_len, const int32_t* win_lo,
                          const int32_t* win_hi, double* out, void* stream);
 
+/* Sweep cell geometry on the device. Column t: depth z[t], receive aperture
+ * [-half[t], half[t]) at x_n = (n + 0.5) pitch, window support width[t];
+ * dfix_n = (ref - hypot(x_n, ref)) / c, dtrue_n = (z_t - hypot(x_n, z_t)) / c.
+ * Theta mode, cell c = (good[c / n_refs], refs[c % n_refs]): d_fixed / d_true
+ * [cell][max_rows] = (d - off) fs, off = min over both profiles (0-padded), and
+ * nfft = next_pow2(max(2 width, width + ceil(max(d - off) fs) + 4)).
+ * Replaces: the per-cell numpy of estimate_theta (tidas.py:254-265) over a sweep
+ * (rx_delay_profile per reference depth, geometry.py:193-199). */
+int tidas_sweep_theta_geometry_f64(int32_t n_cells, int32_t n_refs, const int32_t* good, const double* z,
+                                   const int32_t* half, const int32_t* width, const double* refs,
+                                   double pitch, double c, double fs, int32_t max_rows, double* d_fixed,
+                                   double* d_true, int32_t* nfft, void* stream);
+
+/* Crop mode, cell c = (column cell_col[c], refs[cell_ref[c]]): K3 rows
+ * (t n_el + n + n_el / 2; padding taps: zero_row) and shifts (dfix fs; padding
+ * 0) [cell][max_rows], crop [max(win_lo_t - ceil(-min dfix fs) - 2, 0),
+ * min(win_hi_t + 2, n_len_t)); *bad (device int32, caller-zeroed) = 1 when a
+ * shift reaches n_samples (the reference's ValueError, das.py:87-88).
+ * Replaces: the cropped fixed-profile tidas_psf of run_error_sweep
+ * (tidas.py:336-349, experiments.py:320-328). */
+int tidas_sweep_crop_geometry_f64(int32_t n_cells, const int32_t* cell_col, const int32_t* cell_ref,
+                                  const int32_t* half, const double* refs, const int32_t* win_lo,
+                                  const int32_t* win_hi, const int32_t* n_len, int32_t n_el,
+                                  int32_t zero_row, int32_t n_samples, double pitch, double c, double fs,
+                                  int32_t max_rows, int32_t* rows, double* shifts, int32_t* crop_lo,
+                                  int32_t* crop_hi, int32_t* bad, void* stream);
+
 /* ------------------------------------------------------------------------
  * On-device metrics over strided batches of lines.
  * Line r = (o, i), o < n_outer, i < n_inner, starts at o*s_outer + i*s_inner

@@ -56,6 +56,10 @@ SIGNATURES = {
                                  C.c_int),
     "tidas_theta_cells_f64": ([_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _P], C.c_int),
     "tidas_psf_errors_f64": ([_P, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "tidas_sweep_theta_geometry_f64": ([_I32, _I32, _P, _P, _P, _P, _P, _D, _D, _D, _I32, _P, _P, _P, _P],
+                                       C.c_int),
+    "tidas_sweep_crop_geometry_f64": ([_I32, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _D, _D, _D, _I32,
+                                      _P, _P, _P, _P, _P, _P], C.c_int),
     "tidas_line_sq_errors": ([_P, _P, C.c_int, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P], C.c_int),
     "tidas_line_half_width": ([_P, C.c_int, _I64, _I64, _I64, _I64, _I64, _I64, _D, _P, _P, _P], C.c_int),
     "tidas_line_sidelobes": ([_P, C.c_int, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P], C.c_int),

@@ -198,6 +198,115 @@ __global__ void psf_errors_kernel(const double* __restrict__ sums, int N, const 
   }
 }
 
+
+// ---- sweep cell geometry on the device (tidas.py:254-265, experiments.py:
+// 320-349; round 1 built these O(cells x aperture) arrays in numpy, 70% of the
+// 600 x 600 sweep's time). Cell c of the theta mode is (column good[c / R],
+// reference depth refs[c % R]); of the crop mode (column cell_col[c], reference
+// refs[cell_ref[c]]). The column's receive aperture is [-h, h), h = half[t],
+// x_n = (n + 0.5) pitch, and
+//   dfix_n = (ref - hypot(x_n, ref)) / c,   dtrue_n = (z_t - hypot(x_n, z_t)) / c.
+// theta mode: d_fixed / d_true = (d - off) fs, off = min(min dfix, min dtrue),
+//   nfft = next_pow2(max(2 w_t, w_t + ceil(max(max dfix, max dtrue) - off) fs) + 4))
+// crop mode: rows = t n_el + n + n_el / 2, shifts = dfix fs (padding taps: the
+//   all-zero row, shift 0), crop = [max(win_lo_t - ceil(-min dfix fs) - 2, 0),
+//   min(win_hi_t + 2, n_len_t)); *bad = 1 when a shift reaches the trace length.
+// One warp per cell; the float64 operations are numpy's (no contraction).
+__device__ __forceinline__ double rx_delay(double z, double x, double c) {
+  return __ddiv_rn(__dsub_rn(z, hypot(x, z)), c);
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void sweep_theta_geometry_kernel(int n_cells, int R, const int32_t* __restrict__ good,
+                                            const double* __restrict__ z, const int32_t* __restrict__ half,
+                                            const int32_t* __restrict__ width, const double* __restrict__ refs,
+                                            double pitch, double c, double fs, int A,
+                                            double* __restrict__ d_fixed, double* __restrict__ d_true,
+                                            int32_t* __restrict__ nfft) {
+  const int cell = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (cell >= n_cells) return;
+  const int t = good[cell / R];
+  const double ref = refs[cell % R], zt = z[t];
+  const int h = half[t], n_ap = 2 * h;
+  double fmn = INFINITY, fmx = -INFINITY, tmn = INFINITY, tmx = -INFINITY;
+  for (int k = lane; k < n_ap; k += 32) {
+    const double x = __dmul_rn((double)(k - h) + 0.5, pitch);
+    const double df = rx_delay(ref, x, c), dt = rx_delay(zt, x, c);
+    fmn = fmin(fmn, df); fmx = fmax(fmx, df);
+    tmn = fmin(tmn, dt); tmx = fmax(tmx, dt);
+  }
+  fmn = warp_min(fmn); fmx = warp_max(fmx);
+  tmn = warp_min(tmn); tmx = warp_max(tmx);
+  const double off = fmin(fmn, tmn);
+  double* of = d_fixed + (int64_t)cell * A;
+  double* ot = d_true + (int64_t)cell * A;
+  for (int k = lane; k < A; k += 32) {
+    double vf = 0.0, vt = 0.0;
+    if (k < n_ap) {
+      const double x = __dmul_rn((double)(k - h) + 0.5, pitch);
+      vf = __dmul_rn(__dsub_rn(rx_delay(ref, x, c), off), fs);
+      vt = __dmul_rn(__dsub_rn(rx_delay(zt, x, c), off), fs);
+    }
+    of[k] = vf;
+    ot[k] = vt;
+  }
+  if (lane == 0) {
+    const long long w = width[t];
+    const long long span = (long long)ceil(__dmul_rn(fmax(__dsub_rn(fmx, off), __dsub_rn(tmx, off)), fs)) + 4;
+    const long long n = max(2 * w, w + span);
+    long long p = 1;
+    while (p < n) p <<= 1;
+    nfft[cell] = (int32_t)p;
+  }
+}
+
+__global__ void sweep_crop_geometry_kernel(int n_cells, const int32_t* __restrict__ cell_col,
+                                           const int32_t* __restrict__ cell_ref, const int32_t* __restrict__ half,
+                                           const double* __restrict__ refs, const int32_t* __restrict__ win_lo,
+                                           const int32_t* __restrict__ win_hi, const int32_t* __restrict__ n_len,
+                                           int n_el, int zero_row, int N, double pitch, double c, double fs, int A,
+                                           int32_t* __restrict__ rows, double* __restrict__ shifts,
+                                           int32_t* __restrict__ crop_lo, int32_t* __restrict__ crop_hi,
+                                           int32_t* __restrict__ bad) {
+  const int cell = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (cell >= n_cells) return;
+  const int t = cell_col[cell];
+  const double ref = refs[cell_ref[cell]];
+  const int h = half[t], n_ap = 2 * h;
+  double mn = INFINITY;
+  bool out_of_range = false;
+  for (int k = lane; k < A; k += 32) {
+    int row = zero_row;
+    double sh = 0.0;
+    if (k < n_ap) {
+      const double x = __dmul_rn((double)(k - h) + 0.5, pitch);
+      const double d = rx_delay(ref, x, c);
+      mn = fmin(mn, d);
+      sh = __dmul_rn(d, fs);
+      row = t * n_el + (k - h) + n_el / 2;
+      out_of_range |= fabs(sh) >= (double)N;
+    }
+    rows[(int64_t)cell * A + k] = row;
+    shifts[(int64_t)cell * A + k] = sh;
+  }
+  mn = warp_min(mn);
+  if (__any_sync(0xffffffffu, out_of_range) && lane == 0) atomicExch(bad, 1);
+  if (lane == 0) {
+    const long long span = (long long)ceil(__dmul_rn(-mn, fs)) + 2;
+    crop_lo[cell] = (int32_t)max((long long)win_lo[t] - span, 0LL);
+    crop_hi[cell] = min(win_hi[t] + 2, n_len[t]);
+  }
+}
+
 }  // namespace tidas
 
 extern "C" int tidas_window_frames_f64(double* frames, int32_t n_frames, int32_t n_rows, int32_t n_samples,
@@ -258,6 +367,40 @@ extern "C" int tidas_psf_errors_f64(const double* sums, int32_t n_samples, const
   if (n_cells == 0) return TIDAS_OK;
   psf_errors_kernel<<<n_cells, 256, 0, as_stream(stream)>>>(sums, n_samples, theta, refs, cell_col, crop_lo, crop_hi,
                                                             n_len, win_lo, win_hi, out);
+  TIDAS_LAUNCH_CHECK();
+  return TIDAS_OK;
+}
+
+extern "C" int tidas_sweep_theta_geometry_f64(int32_t n_cells, int32_t n_refs, const int32_t* good, const double* z,
+                                              const int32_t* half, const int32_t* width, const double* refs,
+                                              double pitch, double c, double fs, int32_t max_rows, double* d_fixed,
+                                              double* d_true, int32_t* nfft, void* stream) {
+  using namespace tidas;
+  TIDAS_REQUIRE(good && z && half && width && refs && d_fixed && d_true && nfft, "null pointer");
+  TIDAS_REQUIRE(n_cells >= 0 && n_refs >= 1 && max_rows >= 1 && pitch > 0 && c > 0 && fs > 0, "bad sizes");
+  if (n_cells == 0) return TIDAS_OK;
+  sweep_theta_geometry_kernel<<<(n_cells + 3) / 4, 128, 0, as_stream(stream)>>>(
+      n_cells, n_refs, good, z, half, width, refs, pitch, c, fs, max_rows, d_fixed, d_true, nfft);
+  TIDAS_LAUNCH_CHECK();
+  return TIDAS_OK;
+}
+
+extern "C" int tidas_sweep_crop_geometry_f64(int32_t n_cells, const int32_t* cell_col, const int32_t* cell_ref,
+                                             const int32_t* half, const double* refs, const int32_t* win_lo,
+                                             const int32_t* win_hi, const int32_t* n_len, int32_t n_el,
+                                             int32_t zero_row, int32_t n_samples, double pitch, double c, double fs,
+                                             int32_t max_rows, int32_t* rows, double* shifts, int32_t* crop_lo,
+                                             int32_t* crop_hi, int32_t* bad, void* stream) {
+  using namespace tidas;
+  TIDAS_REQUIRE(cell_col && cell_ref && half && refs && win_lo && win_hi && n_len && rows && shifts && crop_lo &&
+                    crop_hi && bad,
+                "null pointer");
+  TIDAS_REQUIRE(n_cells >= 0 && n_el >= 2 && n_samples >= 1 && max_rows >= 1 && pitch > 0 && c > 0 && fs > 0,
+                "bad sizes");
+  if (n_cells == 0) return TIDAS_OK;
+  sweep_crop_geometry_kernel<<<(n_cells + 3) / 4, 128, 0, as_stream(stream)>>>(
+      n_cells, cell_col, cell_ref, half, refs, win_lo, win_hi, n_len, n_el, zero_row, n_samples, pitch, c, fs,
+      max_rows, rows, shifts, crop_lo, crop_hi, bad);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
 }

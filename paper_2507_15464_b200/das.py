@@ -91,17 +91,22 @@ def _check_shifts(shifts: np.ndarray, n: int) -> None:
 def _delayed_sums_dev(traces_d: torch.Tensor, rows: np.ndarray, shifts: np.ndarray,
                       lo: Optional[np.ndarray] = None, hi: Optional[np.ndarray] = None,
                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """K3 over P profiles: rows/shifts [P][T] -> [P][N] float64 on the device."""
+    """K3 over P profiles: rows/shifts [P][T] -> [P][N] float64 on the device.
+    rows / shifts / lo / hi are host arrays, or device tensors (int32 / float64 /
+    int32 / int32) whose builder has checked the shifts (the sweep's crop geometry)."""
     L = _lib.lib()
     P, T = rows.shape
     n_rows, N = traces_d.shape
-    _check_shifts(shifts, N)
     if out is None:
         out = torch.zeros((P, N), dtype=torch.float64, device=traces_d.device)
-    r_d = _to_dev(rows.astype(np.int32), torch.int32)
-    s_d = _to_dev(shifts.astype(np.float64))
-    lo_d = _to_dev(lo.astype(np.int32), torch.int32) if lo is not None else None
-    hi_d = _to_dev(hi.astype(np.int32), torch.int32) if hi is not None else None
+    if isinstance(rows, torch.Tensor):
+        r_d, s_d, lo_d, hi_d = rows, shifts, lo, hi
+    else:
+        _check_shifts(shifts, N)
+        r_d = _to_dev(rows.astype(np.int32), torch.int32)
+        s_d = _to_dev(shifts.astype(np.float64))
+        lo_d = _to_dev(lo.astype(np.int32), torch.int32) if lo is not None else None
+        hi_d = _to_dev(hi.astype(np.int32), torch.int32) if hi is not None else None
     for p0 in range(0, P, 65535):
         p1 = min(P, p0 + 65535)
         _lib.check(L.tidas_delayed_sum_f64(

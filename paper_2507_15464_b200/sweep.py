@@ -25,8 +25,8 @@ import torch
 
 from . import _lib
 from . import das as _das
-from .geometry import (ApertureRule, DelayProfile, ProbeConfig, element_positions, rx_aperture,
-                       rx_delay_profile, tx_aperture)
+from .geometry import (ApertureRule, DelayProfile, ProbeConfig, aperture_half_counts, element_positions,
+                       tx_aperture)
 from .metrics import window_bounds
 from .simulate import RfFrame, _focused_arrivals, _synth_device, make_pulse
 
@@ -131,35 +131,15 @@ def _cell_geometry(cols, t: int, idx, d_fix: np.ndarray, d_true: np.ndarray):
     return df * fs, dt * fs, nfft
 
 
-def _theta_cells(cols, idx_of_col, d_fix_of_col, d_true_of_col, form: str) -> np.ndarray:
-    """theta [t][r] for every column t and fixed profile row r of d_fix_of_col[t]
-    (an (R, n_t) array of delays in seconds) against the column's true profile.
-    NaN where the reference raises (window outside the frame, no support, zero
-    denominator)."""
-    if form not in FORMS:
-        raise ValueError(f"unknown estimator form {form!r}")
+def _theta_from_geometry(cols, idx_of_col, cell_t: np.ndarray, nffts: np.ndarray, dfx_d: torch.Tensor,
+                         dtr_d: torch.Tensor, A: int, form: str) -> torch.Tensor:
+    """theta of C cells on the device: cell i of column cell_t[i] with FFT length
+    nffts[i] and rebased delays dfx_d / dtr_d [C][A] (samples)."""
     dev = _dev()
     L = _lib.lib()
-    T = len(idx_of_col)
-    R = d_fix_of_col[0].shape[0]
-    theta = np.full((T, R), np.nan)
-    good_cols = [t for t in range(T) if cols.ok[t] and cols.has_support[t]]
-    if not good_cols:
-        return theta
-    A = max(len(idx_of_col[t]) for t in good_cols)
-    C = len(good_cols) * R
-    dfx = np.zeros((C, A))
-    dtr = np.zeros((C, A))
-    nffts = np.zeros(C, np.int64)
-    cell_t = np.repeat(np.asarray(good_cols, np.int64), R)
-    for j, t in enumerate(good_cols):
-        n = len(idx_of_col[t])
-        df, dt, nf = _cell_geometry(cols, t, idx_of_col[t], d_fix_of_col[t], np.asarray(d_true_of_col[t], float))
-        dfx[j * R:(j + 1) * R, :n] = df
-        dtr[j * R:(j + 1) * R, :n] = dt
-        nffts[j * R:(j + 1) * R] = nf
+    C = len(cell_t)
     # spectra pairs: distinct (column, nfft)
-    keys, cell_pair = np.unique(cell_t * (1 << 32) + nffts, return_inverse=True)
+    keys, cell_pair = np.unique(cell_t.astype(np.int64) * (1 << 32) + nffts, return_inverse=True)
     pair_frame = (keys >> 32).astype(np.int32)
     pair_nfft = (keys & ((1 << 32) - 1)).astype(np.int32)
     P = len(keys)
@@ -184,28 +164,104 @@ def _theta_cells(cols, idx_of_col, d_fix_of_col, d_true_of_col, form: str) -> np
             A, _lib.ptr(keep[6][p0:]), kmax, _lib.ptr(S), _lib.stream_handle()))
     th_d = torch.empty(C, dtype=torch.float64, device=dev)
     st_d = torch.empty(C, dtype=torch.int32, device=dev)
-    cp_d, df_d, dt_d = _i32(cell_pair, dev), _f64(dfx, dev), _f64(dtr, dev)
+    cp_d = _i32(cell_pair, dev)
     _lib.check(L.tidas_theta_cells_f64(_lib.ptr(S), C, _lib.ptr(cp_d), _lib.ptr(keep[4]), _lib.ptr(keep[3]),
-                                       _lib.ptr(keep[6]), kmax, _lib.ptr(df_d), _lib.ptr(dt_d), A, FORMS[form],
+                                       _lib.ptr(keep[6]), kmax, _lib.ptr(dfx_d), _lib.ptr(dtr_d), A, FORMS[form],
                                        _lib.ptr(th_d), _lib.ptr(st_d), _lib.stream_handle()))
+    return th_d
+
+
+def _good_columns(cols) -> list:
+    return [t for t in range(len(cols.ok)) if cols.ok[t] and cols.has_support[t]]
+
+
+def _theta_cells(cols, idx_of_col, d_fix_of_col, d_true_of_col, form: str) -> np.ndarray:
+    """theta [t][r] for every column t and fixed profile row r of d_fix_of_col[t]
+    (an (R, n_t) array of delays in seconds) against the column's true profile,
+    host geometry (arbitrary profiles: estimate_theta). NaN where the reference
+    raises (window outside the frame, no support, zero denominator)."""
+    if form not in FORMS:
+        raise ValueError(f"unknown estimator form {form!r}")
+    dev = _dev()
+    T = len(idx_of_col)
+    R = d_fix_of_col[0].shape[0]
+    theta = np.full((T, R), np.nan)
+    good_cols = _good_columns(cols)
+    if not good_cols:
+        return theta
+    A = max(len(idx_of_col[t]) for t in good_cols)
+    C = len(good_cols) * R
+    dfx = np.zeros((C, A))
+    dtr = np.zeros((C, A))
+    nffts = np.zeros(C, np.int64)
+    cell_t = np.repeat(np.asarray(good_cols, np.int64), R)
+    for j, t in enumerate(good_cols):
+        n = len(idx_of_col[t])
+        df, dt, nf = _cell_geometry(cols, t, idx_of_col[t], d_fix_of_col[t], np.asarray(d_true_of_col[t], float))
+        dfx[j * R:(j + 1) * R, :n] = df
+        dtr[j * R:(j + 1) * R, :n] = dt
+        nffts[j * R:(j + 1) * R] = nf
+    th_d = _theta_from_geometry(cols, idx_of_col, cell_t, nffts, _f64(dfx, dev), _f64(dtr, dev), A, form)
     theta[np.asarray(good_cols)] = th_d.cpu().numpy().reshape(len(good_cols), R)
     return theta
 
 
-def _profiles(targets, refs, config, rx_rule):
-    """Per column: aperture (element indices), true delays (n_t,), fixed delays
-    (R, n_t) — rx_aperture / rx_delay_profile (geometry.py:169-199), vectorised
-    over the reference depths: D_n = (z - hypot(x_n, z)) / c."""
-    refs = np.asarray(refs, float)[:, None]
-    c = config.sound_speed
-    idx_of_col, d_true, d_fix = [], [], []
-    for z in targets:
-        ap = np.asarray(rx_aperture(float(z), rx_rule, config), int)
-        xs = element_positions(ap, config)[None, :]
-        idx_of_col.append(ap)
-        d_true.append(rx_delay_profile(float(z), ap, config).delays)
-        d_fix.append((refs - np.hypot(xs, refs)) / c)
-    return idx_of_col, d_true, d_fix
+def _theta_cells_sweep(cols, halves: np.ndarray, refs: np.ndarray, config: ProbeConfig, form: str) -> np.ndarray:
+    """theta [t][r] of a sweep batch: column t's aperture [-halves[t], halves[t]),
+    fixed profiles at every reference depth; the cell geometry (delays, FFT
+    lengths) is built on the device (tidas_sweep_theta_geometry_f64)."""
+    if form not in FORMS:
+        raise ValueError(f"unknown estimator form {form!r}")
+    dev = _dev()
+    L = _lib.lib()
+    T, R = len(halves), len(refs)
+    theta = np.full((T, R), np.nan)
+    good_cols = _good_columns(cols)
+    if not good_cols:
+        return theta
+    A = int(2 * halves[good_cols].max())
+    C = len(good_cols) * R
+    width = (cols.s_hi - cols.s_lo).astype(np.int32)
+    good_d, z_d, h_d, w_d, refs_d = (_i32(good_cols, dev), _f64(cols.targets, dev), _i32(halves, dev),
+                                     _i32(width, dev), _f64(refs, dev))
+    dfx_d = torch.empty((C, A), dtype=torch.float64, device=dev)
+    dtr_d = torch.empty((C, A), dtype=torch.float64, device=dev)
+    nfft_d = torch.empty(C, dtype=torch.int32, device=dev)
+    _lib.check(L.tidas_sweep_theta_geometry_f64(C, R, _lib.ptr(good_d), _lib.ptr(z_d), _lib.ptr(h_d), _lib.ptr(w_d),
+                                                _lib.ptr(refs_d), float(config.pitch), float(config.sound_speed),
+                                                float(config.sampling_frequency), A, _lib.ptr(dfx_d),
+                                                _lib.ptr(dtr_d), _lib.ptr(nfft_d), _lib.stream_handle()))
+    idx_of_col = [np.arange(-int(h), int(h)) for h in halves]
+    cell_t = np.repeat(np.asarray(good_cols, np.int64), R)
+    th_d = _theta_from_geometry(cols, idx_of_col, cell_t, nfft_d.cpu().numpy().astype(np.int64), dfx_d, dtr_d,
+                                A, form)
+    theta[np.asarray(good_cols)] = th_d.cpu().numpy().reshape(len(good_cols), R)
+    return theta
+
+
+def _sweep_profiles(cols, halves: np.ndarray, col_d: torch.Tensor, ref_idx_d: torch.Tensor, depths_d: torch.Tensor,
+                    config: ProbeConfig, A: int):
+    """K3 rows / shifts [C][A] (device) of receive profiles at depths_d[ref_idx_d[c]]
+    over column col_d[c]'s aperture, and the cells' crops around the column
+    windows (tidas_sweep_crop_geometry_f64). The true-profile PSFs (the column's
+    own depth) and the cropped fixed-profile sums share this one device
+    expression, so a cell whose reference is its own depth cancels exactly, as
+    in the reference's numpy."""
+    dev = _dev()
+    C = int(col_d.numel())
+    h_d = _i32(halves, dev)
+    n_d, wlo_d, whi_d = _i32(cols.n_len, dev), _i32(cols.wlo, dev), _i32(cols.whi, dev)
+    rows = torch.empty((C, A), dtype=torch.int32, device=dev)
+    sh = torch.empty((C, A), dtype=torch.float64, device=dev)
+    clo = torch.empty(C, dtype=torch.int32, device=dev)
+    chi = torch.empty(C, dtype=torch.int32, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().tidas_sweep_crop_geometry_f64(
+        C, _lib.ptr(col_d), _lib.ptr(ref_idx_d), _lib.ptr(h_d), _lib.ptr(depths_d), _lib.ptr(wlo_d), _lib.ptr(whi_d),
+        _lib.ptr(n_d), cols.n_el, cols.zero_row, cols.N, float(config.pitch), float(config.sound_speed),
+        float(config.sampling_frequency), A, _lib.ptr(rows), _lib.ptr(sh), _lib.ptr(clo), _lib.ptr(chi),
+        _lib.ptr(bad), _lib.stream_handle()))
+    return rows, sh, clo, chi, bad, (h_d, n_d, wlo_d, whi_d)
 
 
 def theta_matrix_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, rx_rule: ApertureRule, *,
@@ -222,8 +278,8 @@ def theta_matrix_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, r
     for b0 in range(0, len(targets), _COL_BATCH):
         tb = targets[b0:b0 + _COL_BATCH]
         cols = _Columns(tb, config, tx_rule, tx_focus_depth, window_half_width, spreading)
-        idx, d_true, d_fix = _profiles(tb, refs, config, rx_rule)
-        values[:, b0:b0 + len(tb)] = _theta_cells(cols, idx, d_fix, d_true, form).T
+        halves = aperture_half_counts(tb, rx_rule, config).astype(np.int64)
+        values[:, b0:b0 + len(tb)] = _theta_cells_sweep(cols, halves, refs, config, form).T
         del cols
     return ThetaMatrix(reference_depths=refs, target_depths=targets, values=values)
 
@@ -243,58 +299,37 @@ def error_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, rx_rule:
     refs = targets if reference_depths is None else np.asarray(reference_depths, dtype=float)
     R, T = len(refs), len(targets)
     th_m, loc_m, glo_m = (np.full((R, T), np.nan) for _ in range(3))
-    fs = config.sampling_frequency
-    n_el, half = config.element_count, config.element_count // 2
+    refs_d = _f64(refs, dev)
     for b0 in range(0, T, _COL_BATCH):
         tb = targets[b0:b0 + _COL_BATCH]
-        Tb = len(tb)
         cols = _Columns(tb, config, tx_rule, tx_focus_depth, window_half_width, spreading)
-        idx, d_true, d_fix = _profiles(tb, refs, config, rx_rule)
-        A = max(len(i) for i in idx)
+        halves = aperture_half_counts(tb, rx_rule, config).astype(np.int64)
+        A = int(2 * halves.max())
         # true-profile PSF per column (das_psf of the windowed frame), K3
-        rows_t = np.full((Tb, A), cols.zero_row, np.int64)
-        sh_t = np.zeros((Tb, A))
-        for t in range(Tb):
-            n = len(idx[t])
-            rows_t[t, :n] = t * n_el + idx[t] + half
-            sh_t[t, :n] = np.asarray(d_true[t]) * fs
-        _das._count(int(sum(len(i) for i in idx)))
-        refs_d = _das._delayed_sums_dev(cols.flat, rows_t, sh_t)
-        th = _theta_cells(cols, idx, d_fix, d_true, form)  # [t][r]
-        th_m[:, b0:b0 + Tb] = th.T
+        cols_d = torch.arange(len(tb), dtype=torch.int32, device=dev)
+        z_d = _f64(tb, dev)
+        rows_t, sh_t, _, _, bad_t, _ = _sweep_profiles(cols, halves, cols_d, cols_d, z_d, config, A)
+        _das._count(int(2 * halves.sum()))
+        psf_d = _das._delayed_sums_dev(cols.flat, rows_t, sh_t)
+        th = _theta_cells_sweep(cols, halves, refs, config, form)  # [t][r]
+        th_m[:, b0:b0 + len(tb)] = th.T
         t_sel, r_sel = np.nonzero(np.isfinite(th))
         C = t_sel.size
         if C == 0:
             continue
         # fixed-profile sums on each cell's crop [lo - span, hi + 2) (tidas.py:336-349), K3
-        rows_c = np.full((C, A), cols.zero_row, np.int64)
-        sh_c = np.zeros((C, A))
-        clo = np.zeros(C, np.int32)
-        chi = np.zeros(C, np.int32)
-        # np.nonzero walks row-major: the cells of column t are the contiguous run t_sel == t
-        bounds = np.searchsorted(t_sel, np.arange(Tb + 1))
-        for t in range(Tb):
-            a, b = int(bounds[t]), int(bounds[t + 1])
-            if a == b:
-                continue
-            n = len(idx[t])
-            d = d_fix[t][r_sel[a:b]]  # (k, n)
-            rows_c[a:b, :n] = t * n_el + idx[t] + half
-            sh_c[a:b, :n] = d * fs
-            span = np.ceil(-d.min(axis=1) * fs).astype(np.int64) + 2
-            clo[a:b] = np.maximum(int(cols.wlo[t]) - span, 0)
-            chi[a:b] = min(int(cols.whi[t]) + 2, int(cols.n_len[t]))
-        lens = np.fromiter((len(i) for i in idx), np.int64, count=Tb)
-        _das._count(int(lens[t_sel].sum()))
-        sums = _das._delayed_sums_dev(cols.flat, rows_c, sh_c, lo=clo, hi=chi)
+        cc_d, cr_d = _i32(t_sel, dev), _i32(r_sel, dev)
+        rows_c, sh_c, clo_d, chi_d, bad, (_, n_d, wlo_d, whi_d) = _sweep_profiles(
+            cols, halves, cc_d, cr_d, refs_d, config, A)
+        _das._count(int((2 * halves)[t_sel].sum()))
+        sums = _das._delayed_sums_dev(cols.flat, rows_c, sh_c, lo=clo_d, hi=chi_d)
         th_d = _f64(th[t_sel, r_sel], dev)
-        cc_d = _i32(t_sel, dev)
-        clo_d, chi_d = _i32(clo, dev), _i32(chi, dev)
-        n_d, wlo_d, whi_d = _i32(cols.n_len, dev), _i32(cols.wlo, dev), _i32(cols.whi, dev)
         out = torch.empty((C, 4), dtype=torch.float64, device=dev)
-        _lib.check(L.tidas_psf_errors_f64(_lib.ptr(sums), cols.N, _lib.ptr(th_d), _lib.ptr(refs_d), C,
+        _lib.check(L.tidas_psf_errors_f64(_lib.ptr(sums), cols.N, _lib.ptr(th_d), _lib.ptr(psf_d), C,
                                           _lib.ptr(cc_d), _lib.ptr(clo_d), _lib.ptr(chi_d), _lib.ptr(n_d),
                                           _lib.ptr(wlo_d), _lib.ptr(whi_d), _lib.ptr(out), _lib.stream_handle()))
+        if int(bad.item()) or int(bad_t.item()):
+            raise ValueError(f"a fixed-profile delay shift exceeds the trace support {cols.N}")
         e = out.cpu().numpy()
         with np.errstate(divide="ignore", invalid="ignore"):
             loc = np.where(e[:, 1] > 0.0, e[:, 0] / np.where(e[:, 1] > 0.0, e[:, 1], 1.0), np.nan)
@@ -303,7 +338,7 @@ def error_sweep(depth_grid, config: ProbeConfig, tx_rule: ApertureRule, rx_rule:
         glo = np.where(np.isfinite(loc), glo, np.nan)
         loc_m[r_sel, b0 + t_sel] = loc
         glo_m[r_sel, b0 + t_sel] = glo
-        del cols, sums, refs_d
+        del cols, sums, psf_d
     return th_m, loc_m, glo_m
 
 

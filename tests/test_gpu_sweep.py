@@ -96,3 +96,58 @@ def test_estimate_theta_errors(ref_vectors):
     zero = tb.RfFrame(np.zeros_like(win), REF_PROBE["fs"], 0.0, 25e-3, np.arange(-4, 4))
     with pytest.raises(ZeroDivisionError):
         tb.estimate_theta(zero, true, true)
+
+
+def test_device_cell_geometry_matches_the_host_restatement(ref_vectors):
+    """tidas_sweep_theta_geometry_f64 / tidas_sweep_crop_geometry_f64 against the
+    numpy cell geometry (tidas.py:254-265, 336-349): FFT lengths, crops and rows
+    exactly, delays to a few ulp (CUDA's hypot against glibc's)."""
+    import torch
+    from paper_2507_15464_b200 import _lib
+    from paper_2507_15464_b200 import sweep as sw
+    depths = np.linspace(0.005, 0.042, 40)
+    refs = depths[::3]
+    cols = sw._Columns(depths, PROBE, tb.Kossoff(0.6), 25e-3, float(ref_vectors["eps"]), True)
+    from paper_2507_15464_b200.geometry import aperture_half_counts
+    halves = aperture_half_counts(depths, tb.FNumber(1.0), PROBE).astype(np.int64)
+    good = sw._good_columns(cols)
+    R, A, dev = len(refs), int(2 * halves[good].max()), torch.device("cuda")
+    C = len(good) * R
+    dfx = torch.empty((C, A), dtype=torch.float64, device=dev)
+    dtr = torch.empty((C, A), dtype=torch.float64, device=dev)
+    nf = torch.empty(C, dtype=torch.int32, device=dev)
+    keep = [sw._i32(good, dev), sw._f64(depths, dev), sw._i32(halves, dev),
+            sw._i32(cols.s_hi - cols.s_lo, dev), sw._f64(refs, dev)]
+    _lib.check(_lib.lib().tidas_sweep_theta_geometry_f64(
+        C, R, *[_lib.ptr(k) for k in keep], PROBE.pitch, PROBE.sound_speed, PROBE.sampling_frequency, A,
+        _lib.ptr(dfx), _lib.ptr(dtr), _lib.ptr(nf), _lib.stream_handle()))
+    dfx, dtr, nf = dfx.cpu().numpy(), dtr.cpu().numpy(), nf.cpu().numpy()
+    c = PROBE.sound_speed
+    for j, t in enumerate(good):
+        idx = np.arange(-halves[t], halves[t])
+        xs = tb.element_positions(idx, PROBE)
+        d_fix = (refs[:, None] - np.hypot(xs[None, :], refs[:, None])) / c
+        d_true = (depths[t] - np.hypot(xs, depths[t])) / c
+        df, dt, nfft = sw._cell_geometry(cols, t, idx, d_fix, d_true)
+        n = len(idx)
+        sl = slice(j * R, (j + 1) * R)
+        assert np.array_equal(nf[sl], nfft)
+        np.testing.assert_allclose(dfx[sl, :n], df, rtol=0, atol=1e-9)
+        np.testing.assert_allclose(dtr[sl, :n], dt, rtol=0, atol=1e-9)
+        assert not dfx[sl, n:].any() and not dtr[sl, n:].any()
+    # crop mode: every (good column, reference) cell
+    t_sel = np.repeat(np.asarray(good), R)
+    r_sel = np.tile(np.arange(R), len(good))
+    rows, sh, clo, chi, bad, _ = sw._sweep_profiles(cols, halves, sw._i32(t_sel, dev), sw._i32(r_sel, dev),
+                                                    sw._f64(refs, dev), PROBE, A)
+    rows, sh, clo, chi = (v.cpu().numpy() for v in (rows, sh, clo, chi))
+    assert int(bad.item()) == 0
+    fs = PROBE.sampling_frequency
+    for i, (t, r) in enumerate(zip(t_sel, r_sel)):
+        idx = np.arange(-halves[t], halves[t])
+        d = (refs[r] - np.hypot(tb.element_positions(idx, PROBE), refs[r])) / c
+        span = int(np.ceil(-d.min() * fs)) + 2
+        assert clo[i] == max(int(cols.wlo[t]) - span, 0) and chi[i] == min(int(cols.whi[t]) + 2, int(cols.n_len[t]))
+        assert np.array_equal(rows[i, :len(idx)], t * PROBE.element_count + idx + PROBE.element_count // 2)
+        assert (rows[i, len(idx):] == cols.zero_row).all() and not sh[i, len(idx):].any()
+        np.testing.assert_allclose(sh[i, :len(idx)], d * fs, rtol=0, atol=1e-9)
