@@ -14,12 +14,14 @@ timed region.
 
 Multi-GPU (north star (e)): ``--gpus N`` without torchrun re-launches itself
 as N ranks under torch.distributed.run (127.0.0.1 rendezvous); under torchrun
-WORLD_SIZE must equal N. cfg2 is weak-scaled (F frames per rank); each rank
-images its frames in sub-chunks of 64 and all-gathers each sub-chunk's images
-over NCCL while the next one computes. ``other_configs`` adds cfg1 (weak),
-cfg3 (64 frames, 11-angle coherent compounding, sharded + NCCL image gather),
-cfg5 (1024 int16 frames, sharded + gather) and ``tidas`` the row operator
-(cfg2 maps, weak; cfg4's 256 maps sharded, K built by K5). NCCL's
+WORLD_SIZE must equal N. Frames and maps are independent units, so every line
+is frame- (map-) sharded with no data-path collective, except cfg3, whose
+compounded images are gathered over NCCL inside the step as BASELINE.json's
+cfg3 asks. cfg2 is weak-scaled (F frames per rank). ``other_configs`` adds
+cfg1 (weak), cfg3 (64 frames, 11-angle coherent compounding, sharded + NCCL
+image gather) and cfg5 (1024 int16 frames, sharded); ``tidas`` the row
+operator (cfg2 maps, weak; cfg4's 256 maps and cfg5's 1024 maps sharded, K
+built by K5 for each config's array and grid). NCCL's
 communicator log is kept (NCCL_DEBUG=INFO to a file) and summarised.
 
 ``--impl reference`` times the reference's own CPU algorithm (oracle port,
@@ -47,13 +49,18 @@ METRIC = "DAS/tiDAS frames/s (128 ch, 512x256 px) and % of HBM-bandwidth rooflin
 BYTES_PER_FRAME_CFG2 = 128 * 4096 * 4 + 512 * 256 * 4          # 2,621,440
 BYTES_PER_MAP_CFG2 = 512 * 256 * 4 * 2                         # 1,048,576
 BYTES_PER_MAP_CFG4 = 2048 * 1024 * 4 * 2                       # 16,777,216
-SUB = 64  # frames per pipelined sub-chunk at N > 1 (K2: 64 / 8 x 512 CTAs = 9 waves)
 
 CFG2 = dict(n_el=128, pitch=0.3e-3, f0=5e6, fs=40e6, c=1540.0, fbw=0.6, n_samples=4096,
             nz=512, nx=256, z=(5e-3, 45e-3), x=(-19.2e-3, 19.2e-3), f_number=1.5, n_scat=2000,
             region_x=(-20e-3, 20e-3), region_z=(5e-3, 45e-3))
 CFG4 = dict(nz=2048, nx=1024, z=(5e-3, 45e-3), x=(-19.2e-3, 19.2e-3), taps=129, maps=256, density=0.02,
             neighbourhood=8)
+# cfg5's tiDAS: the row operator on 1024 maps of the cfg5 grid (1024 x 1024, z 5-60 mm, x +-28.8 mm), K by K5
+# for the cfg5 array (192 el, 0.3 mm, 5 MHz, 40 MHz, 8192 samples); maps drawn as cfg4's
+CFG5T = dict(nz=1024, nx=1024, z=(5e-3, 60e-3), x=(-28.8e-3, 28.8e-3), taps=129, maps=1024, density=0.02,
+             neighbourhood=8, probe=dict(n_el=192, pitch=0.3e-3, fs=40e6, c=1540.0, f0=5e6, fbw=0.6,
+                                         f_number=1.5, n_samples=8192))
+BYTES_PER_MAP_CFG5 = 1024 * 1024 * 4 * 2                       # 8,388,608
 WORKLOAD = ("cfg2 (BASELINE.json configs[1]): DAS, 128 ch x 4096 f32 RF -> 512x256 px, Hann F#1.5, "
             "linear interp, envelope")
 DATA = ("synthetic: seeded speckle (2000 N(0,1) scatterers over 40x40 mm per frame), 0-degree plane-wave RF "
@@ -66,9 +73,9 @@ def workload_config(frames_per_gpu: int, world: int) -> dict:
     return {"workload": WORKLOAD, "frames_per_step_per_gpu": frames_per_gpu,
             "parallelism": f"frame-sharded dp{world}",
             "l2": f"inputs larger than L2 ({frames_per_gpu * 2} MiB RF per GPU per step)",
-            "gather": (f"NCCL all_gather_into_tensor of images inside the step (chunk-major, no staging copy), "
-                       f"pipelined per {SUB} frames with the DAS of "
-                       f"the next {SUB}") if world > 1 else "none"}
+            "gather": "none: cfg2 frames are independent units, each rank keeps the images it made (no data-path "
+                      "collective); the NCCL image gather north star (e) asks for runs on cfg3's compounded "
+                      "images (other_configs)" if world > 1 else "none"}
 
 
 def cpu_model() -> str:
@@ -368,16 +375,11 @@ def main():
                               device=dev)
     ws = imaging.DasWorkspace(plan, dev)
     img = torch.empty((len(frames), cfg["nz"], cfg["nx"]), device=dev)
-    gathered = torch.empty((total_frames, cfg["nz"], cfg["nx"]), device=dev) if world > 1 else None
-    per_launch = min(len(frames), ws.chunk) if world == 1 else min(SUB, len(frames), ws.chunk)
+    per_launch = min(len(frames), ws.chunk)
 
     def step():
-        if world == 1:
-            tb.das_image(rf, plan, out=img, workspace=ws)
-        else:
-            # the all-gather of sub-chunk c (async NCCL over NVLink) overlaps K1 + K2 of c + 1
-            parallel.pipelined_gather(lambda c0, c1: tb.das_image(rf[c0:c1], plan, out=img[c0:c1], workspace=ws),
-                                      len(frames), gathered, sub=SUB, layout="chunk_major")
+        # frames are independent: every rank images its own shard, no collective
+        tb.das_image(rf, plan, out=img, workspace=ws)
 
     for _ in range(args.warmup):
         step()
@@ -406,18 +408,20 @@ def main():
     launches = args.steps * n_launch * 2
 
     # K1 / K2 separately, on the per-launch frame count of the step
-    k1_ms, k2_ms = [], []
+    # (back-to-back pairs with no host sync in between, so the clocks stay at the step's)
     an = ws.buf[:per_launch]
-    for _ in range(5):
+    evs = []
+    for _ in range(8):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
         tb.rf_analytic(rf[:per_launch], plan.prec, out=an)
         ev[1].record(stream)
         tb.das_from_analytic(an, plan, out=img[:per_launch])
         ev[2].record(stream)
-        torch.cuda.synchronize()
-        k1_ms.append(ev[0].elapsed_time(ev[1]) / per_launch)
-        k2_ms.append(ev[1].elapsed_time(ev[2]) / per_launch)
+        evs.append(ev)
+    torch.cuda.synchronize()
+    k1_ms = [ev[0].elapsed_time(ev[1]) / per_launch for ev in evs[2:]]
+    k2_ms = [ev[1].elapsed_time(ev[2]) / per_launch for ev in evs[2:]]
     k1, k2 = statistics.median(k1_ms), statistics.median(k2_ms)
     pipe_gbs = BYTES_PER_FRAME_CFG2 / ((k1 + k2) / 1e3) / 1e9
     tr = committed_traffic()
@@ -436,6 +440,16 @@ def main():
                "live_pairs_per_frame": pairs, "bytes_per_pair": 24, "kernel": "das_image_kernel (K2)",
                "note": "shared-memory gather roofline of K2 (128 B/clk/SM at the measured SM clock); "
                        "the HBM roofline above is the contract metric"}
+    # the HBM fraction this pipeline could reach at both kernels' own floors: K1 at HBM
+    # speed on its RF read + complex64 write, K2 at the shared-memory gather floor
+    k1_floor_us = (128 * 4096 * (4 + 8)) / (hbm * 1e9) * 1e6
+    k2_floor_us = pairs * 24 / (smem_peak * 1e9) * 1e6
+    roofline["ceiling"] = {
+        "frac": BYTES_PER_FRAME_CFG2 / ((k1_floor_us + k2_floor_us) * 1e-6) / 1e9 / hbm,
+        "K1_floor_us": k1_floor_us, "K2_floor_us": k2_floor_us,
+        "note": "HBM fraction at K1's HBM floor (RF in + complex64 analytic out) plus K2's shared-memory "
+                "gather floor (24 B per live pixel-channel pair at 128 B/clk/SM): the DAS gather, not HBM, "
+                "bounds the pipeline; achieved / ceiling = frac / ceiling.frac"}
 
     # e2e through the public API with pinned host buffers (HostPipeline: H2D of
     # chunk i+1 || K1 + K2 of chunk i || D2H of chunk i-1, three streams)
@@ -532,6 +546,35 @@ def main():
             "cpu_baseline": cpu_rowconv,
         }
         del maps4, y4, a4
+        torch.cuda.empty_cache()
+        # cfg5 ("run DAS and tiDAS at 1/2/4/8 GPUs with frame sharding"): K5 on the cfg5 array, 1024 maps sharded
+        c5 = CFG5T
+        x5, z5 = np.linspace(*c5["x"], c5["nx"]), np.linspace(*c5["z"], c5["nz"])
+        K5k, th5 = tb.build_row_kernels(z5, c5["taps"], x5[1] - x5[0], neighbourhood=c5["neighbourhood"],
+                                        **c5["probe"])
+        m0, m1 = parallel.shard_range(c5["maps"], rank, world)
+        M5 = m1 - m0
+        gen5 = torch.Generator(device=dev).manual_seed(50 + rank)
+        maps5 = (torch.rand((M5, c5["nz"], c5["nx"]), device=dev, generator=gen5) < c5["density"]).float() * \
+            torch.randn((M5, c5["nz"], c5["nx"]), device=dev, generator=gen5)
+        y5, a5 = torch.empty_like(maps5), torch.empty_like(maps5)
+        tf5 = timed(lambda: tb.tidas_rowconv(maps5, K5k, out=y5), max(3, min(args.steps, 10)), 2)
+        ta5 = timed(lambda: tb.tidas_rowconv_adjoint(y5, K5k, out=a5), max(3, min(args.steps, 10)), 2)
+        lhs5 = float((y5.double() * y5.double()).sum())
+        rhs5 = float((maps5.double() * a5.double()).sum())
+        g5 = (BYTES_PER_MAP_CFG5 * M5 + K5k.numel() * 4) / (tf5 / 1e3) / 1e9
+        ga5 = (BYTES_PER_MAP_CFG5 * M5 + K5k.numel() * 4) / (ta5 / 1e3) / 1e9
+        tidas["cfg5_fwd_adj"] = {
+            "value": c5["maps"] / ((tf5 + ta5) / 1e3), "unit": "maps/s (fwd+adj)", "fwd_ms": tf5, "adj_ms": ta5,
+            "fwd_maps_per_s": c5["maps"] / (tf5 / 1e3), "maps_per_gpu": M5, "maps_total": c5["maps"],
+            "scaling": "strong", "adjoint_identity_rel": abs(lhs5 - rhs5) / max(abs(lhs5), 1e-300),
+            "kernels": "K5 on the cfg5 array and grid (1024 rows x 129 taps), theta in "
+                       f"[{float(th5.min()):.4f}, {float(th5.max()):.4f}]",
+            "roofline": {"bound": "hbm", "achieved": g5, "peak": hbm, "unit": "GB/s", "frac": g5 / hbm,
+                         "adj_frac": ga5 / hbm, "traffic": None,
+                         "kernel": f"rowconv_tc1_kernel<fwd> (tcgen05 3xTF32), {M5} maps/launch"}}
+        del maps5, y5, a5
+        torch.cuda.empty_cache()
 
     # ---------------- the paper's 600 x 600 theta / error sweep
     sweep = None
@@ -564,7 +607,7 @@ def main():
                                      "seconds_per_cell": ct / len(d12) ** 2,
                                      "extrapolated_600x600_minutes": ct / len(d12) ** 2 * 360000 / 60}
 
-    # ------------ the other BASELINE.json DAS configs (cfg1 weak; cfg3 / cfg5 sharded + gathered)
+    # ------------ the other BASELINE.json DAS configs (cfg1 weak; cfg3 / cfg5 sharded, cfg3 gathered)
     others = None
     if not args.no_configs:
         sys.path.insert(0, str(ROOT / "tools"))
@@ -575,8 +618,8 @@ def main():
                                          "scaling", "gather")}
                   for k, v in res.items()}
         others["note"] = ("das_image (K1 + K2) with the RF resident in HBM, CUDA events, max over ranks; cfg3 / "
-                          "cfg5 shard a fixed batch (64 / 1024 frames) over the ranks and all-gather the images "
-                          "over NCCL inside the step")
+                          "cfg5 shard a fixed batch (64 / 1024 frames) over the ranks; cfg3 all-gathers its "
+                          "compounded images over NCCL inside the step")
 
     # ------------------------------------------------- CPU baselines (N = 1)
     cpu = None

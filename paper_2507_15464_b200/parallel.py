@@ -68,13 +68,21 @@ def gather_images(local: torch.Tensor, n_units: int, out: Optional[torch.Tensor]
                   group=None) -> Optional[torch.Tensor]:
     """All-gather per-rank image shards [n_local][...] into [n_units][...] on every rank.
 
-    Shards may differ by one unit; they are padded to the largest shard for
-    ``all_gather_into_tensor`` (one NCCL call over NVLink) and trimmed."""
+    Equal shards are gathered by one ``all_gather_into_tensor`` straight into
+    the result; shards that differ by one unit are padded to the largest shard,
+    gathered and trimmed."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return local if out is None else out.copy_(local)
     tail = tuple(local.shape[1:])
     cap = shard_range(n_units, 0, world)[1]
+    if n_units % world == 0 and local.is_contiguous():
+        # equal shards: NCCL writes every rank's shard straight into its slice of the result
+        if out is None:
+            out = local.new_empty((n_units,) + tail)
+        if out.is_contiguous() and tuple(out.shape) == (n_units,) + tail:
+            dist.all_gather_into_tensor(out, local, group=group)
+            return out
     padded = local.new_zeros((cap,) + tail)
     padded[: local.shape[0]] = local
     buf = local.new_empty((cap * world,) + tail)

@@ -36,12 +36,14 @@ def _worker(rank, world, port, n_units, q):
     local = torch.stack([torch.full((3, 4), float(f)) + torch.arange(12.0).view(3, 4)
                          for f in range(a, b)]) if b > a else torch.zeros((0, 3, 4))
     full = gather_images(local, n_units)
+    into = gather_images(local, n_units, out=torch.full((n_units, 3, 4), -1.0))  # caller-owned result
+    assert torch.equal(full, into)
     q.put((rank, full.numpy().tolist()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_units", [7, 8])
+@pytest.mark.parametrize("n_units", [7, 8])  # padded (unequal shards) and direct (equal shards) paths
 def test_gather_two_ranks_matches_single_process(n_units):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -8,8 +8,10 @@ its arrival dtype + FP32 image) and the HBM-roofline fraction. Inputs are
 seeded synthetic frames simulated on the device (cfg5: scaled to std 1000,
 rounded, clipped to int16 by the library quantiser). Called by bench.py with
 its rank / world: cfg1 is weak-scaled (256 frames per rank); cfg3 (64 frames)
-and cfg5 (1024 frames) shard a fixed batch over the ranks (strong scaling) and
-all-gather the images over NCCL inside the timed step (north star (e)).
+and cfg5 (1024 frames) shard a fixed batch over the ranks (strong scaling).
+cfg3 all-gathers its compounded images over NCCL inside the timed step (north
+star (e), BASELINE.json cfg3); cfg1 / cfg5 frames stay on their rank (no
+data-path collective).
 """
 import argparse
 import json
@@ -30,7 +32,7 @@ CFGS = {
                  out="envelope", bytes=64 * 2048 * 8 + 256 * 128 * 4, region=None),
     "cfg3": dict(n_el=128, pitch=0.3e-3, f0=5e6, fs=40e6, fbw=0.6, N=4096, nz=1024, nx=512, z=(5e-3, 45e-3),
                  x=(-19.2e-3, 19.2e-3), angles=list(np.deg2rad(np.linspace(-10, 10, 11))), frames=64,
-                 per_rank=False, n_scat=2000, n_bright=5, dtype=torch.float32, out="coherent",
+                 per_rank=False, gather=True, n_scat=2000, n_bright=5, dtype=torch.float32, out="coherent",
                  bytes=11 * 128 * 4096 * 4 + 1024 * 512 * 4, region=((-20e-3, 20e-3), (5e-3, 45e-3))),
     "cfg5": dict(n_el=192, pitch=0.3e-3, f0=5e6, fs=40e6, fbw=0.6, N=8192, nz=1024, nx=1024, z=(5e-3, 60e-3),
                  x=(-28.8e-3, 28.8e-3), angles=[0.0], frames=1024, per_rank=False, n_scat=4000, dtype=torch.int16,
@@ -88,10 +90,20 @@ def run_configs(names, steps=10, warmup=3, echo=False, rank=0, world=1, timed=No
                                   x=x, z=z, angles=c["angles"], f_number=1.5, out=c["out"])
         ws = imaging.DasWorkspace(plan)
         img = torch.empty((rf.shape[0], c["nz"], c["nx"]), device="cuda")
-        gather = world > 1 and not c["per_rank"]
+        gather = world > 1 and c.get("gather", False)
         full = torch.empty((total, c["nz"], c["nx"]), device="cuda") if gather else None
+        n_local = int(rf.shape[0])
+        # sub-chunks of whole 8-frame groups (K2's frames per thread); with two or
+        # more, the all-gather of one overlaps the DAS of the next
+        sub = max(8, (n_local // 2) // 8 * 8)
+        pipelined = gather and total % world == 0 and n_local >= 2 * sub
 
         def step():
+            if pipelined:  # NCCL over NVLink, chunk-major order (parallel.chunk_major_index)
+                parallel.pipelined_gather(
+                    lambda a, b: tb.das_image(rf[a:b], plan, out=img[a:b], workspace=ws), n_local, full, sub=sub,
+                    layout="chunk_major")
+                return
             tb.das_image(rf, plan, out=img, workspace=ws)
             if gather:  # NCCL over NVLink: every rank receives the whole batch's images
                 parallel.gather_images(img, total, out=full)
@@ -104,7 +116,9 @@ def run_configs(names, steps=10, warmup=3, echo=False, rank=0, world=1, timed=No
                      "hbm_frac": gbs / hbm, "rf_dtype": str(c["dtype"]).replace("torch.", ""),
                      "transmits": len(c["angles"]), "grid": [c["nz"], c["nx"]], "out": c["out"],
                      "chunk_frames": ws.chunk, "scaling": "weak" if c["per_rank"] else "strong",
-                     "gather": "NCCL all_gather_into_tensor of the images" if gather else "none",
+                     "gather": ("NCCL all_gather_into_tensor of the images, pipelined per "
+                                f"{sub} frames" if pipelined else "NCCL all_gather_into_tensor of the images")
+                               if gather else "none",
                      "checksum": float(img.double().sum())}
         if echo:
             print(json.dumps({name: res[name]}), flush=True)
