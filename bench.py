@@ -615,7 +615,7 @@ def main():
         res = bench_configs.run_configs(["cfg1", "cfg3", "cfg5"], rank=rank, world=world, timed=timed, hbm=hbm)
         others = {k: {q: v[q] for q in ("frames_per_s", "ms_per_step", "frames_total", "frames_per_rank",
                                          "hbm_frac", "bytes_per_frame", "rf_dtype", "transmits", "grid", "out",
-                                         "scaling", "gather")}
+                                         "scaling", "gather", "nccl_gather_frames_per_s")}
                   for k, v in res.items()}
         others["note"] = ("das_image (K1 + K2) with the RF resident in HBM, CUDA events, max over ranks; cfg3 / "
                           "cfg5 shard a fixed batch (64 / 1024 frames) over the ranks; cfg3 all-gathers its "

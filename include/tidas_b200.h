@@ -136,6 +136,24 @@ int tidas_das_image(const tidas_das_desc_t* desc, const void* analytic,
                     const int32_t* ap_half, void* out, void* stream);
 
 /*
+ * K2 with the image gather fused into its epilogue (north star (e), ABI 4):
+ * every pixel value is stored to `out` and, at the same element offset, to each
+ * of the n_peers (<= TIDAS_MAX_PEERS) device buffers in the host array
+ * peer_out — typically the peer-mapped symmetric-memory image buffers of the
+ * other GPUs of the node, offset to where this launch's first frame belongs,
+ * so the stores travel over NVLink while the next tiles compute. Completion
+ * and visibility on the peers is the caller's (a system-scope barrier after
+ * the launch on the same stream). n_peers = 0 is tidas_das_image.
+ * Replaces: the reference's process-pool result gathering
+ * (experiments.py:195-199), which has no device counterpart.
+ */
+#define TIDAS_MAX_PEERS 7
+int tidas_das_image_peers(const tidas_das_desc_t* desc, const void* analytic,
+                          const double* t_star, const double* x, const double* z,
+                          const int32_t* ap_half, void* out, void* const* peer_out,
+                          int32_t n_peers, void* stream);
+
+/*
  * K3 — delayed sum (das.py:140-149, float64, bit-identical to the reference):
  *   out[p][k] = sum_{j in order} lerp-shift(traces[rows[p][j]], shift[p][j])[k]
  * for n_profiles independent profiles of length n_taps (rows are absolute trace

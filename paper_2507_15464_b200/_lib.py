@@ -44,6 +44,7 @@ SIGNATURES = {
     "tidas_spectral_shift_f64": ([_P, _I64, _I32, _D, _P, _P], C.c_int),
     "tidas_plane_wave_arrivals": ([_P, _I32, _P, _I32, _P, _I32, _I32, _D, _D, _P, _P], C.c_int),
     "tidas_das_image": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "tidas_das_image_peers": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "tidas_das_window": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P], C.c_int),
     "tidas_delayed_sum_f64": ([_P, _I32, _I32, _P, _P, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "tidas_window_envelope_f64": ([_P, _I32, _P, _P, _P, _P, _P, _I32, _P, _P], C.c_int),

@@ -60,6 +60,11 @@ struct DasParams {
   const double* t_star;
   const double* xg;
   const double* zg;
+  // extra image destinations, same layout as out (buffers of other GPUs mapped
+  // into this address space: the image gather of north star (e) done by K2's
+  // own stores over NVLink instead of a separate NCCL collective)
+  int n_peer;
+  void* peer[TIDAS_MAX_PEERS];
 };
 
 // ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier
@@ -604,9 +609,18 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
     const int f = f0 + b;
     if (f >= p.F) break;
     const int64_t o = ((int64_t)f * p.nz + iz) * p.nx + ix;
-    if (OUT == TIDAS_OUT_ENVELOPE) reinterpret_cast<R*>(out_)[o] = acc_env[b];
-    else if (OUT == TIDAS_OUT_COHERENT) reinterpret_cast<R*>(out_)[o] = cabs_(acc_iq[b]);
-    else reinterpret_cast<C*>(out_)[o] = acc_iq[b];
+    if constexpr (OUT == TIDAS_OUT_IQ) {
+      reinterpret_cast<C*>(out_)[o] = acc_iq[b];
+#pragma unroll
+      for (int q = 0; q < TIDAS_MAX_PEERS; ++q)
+        if (q < p.n_peer) reinterpret_cast<C*>(p.peer[q])[o] = acc_iq[b];
+    } else {
+      const R v = OUT == TIDAS_OUT_ENVELOPE ? acc_env[b] : cabs_(acc_iq[b]);
+      reinterpret_cast<R*>(out_)[o] = v;
+#pragma unroll
+      for (int q = 0; q < TIDAS_MAX_PEERS; ++q)  // static indices: the pointers stay in the parameter bank
+        if (q < p.n_peer) reinterpret_cast<R*>(p.peer[q])[o] = v;
+    }
   }
 }
 
@@ -783,8 +797,17 @@ static int dispatch_ap(const tidas_das_desc_t* d, const DasParams& p, const void
 extern "C" int tidas_das_image(const tidas_das_desc_t* d, const void* analytic, const double* t_star,
                                const double* x, const double* z, const int32_t* ap_half, void* out,
                                void* stream) {
+  return tidas_das_image_peers(d, analytic, t_star, x, z, ap_half, out, nullptr, 0, stream);
+}
+
+extern "C" int tidas_das_image_peers(const tidas_das_desc_t* d, const void* analytic, const double* t_star,
+                                     const double* x, const double* z, const int32_t* ap_half, void* out,
+                                     void* const* peer_out, int32_t n_peers, void* stream) {
   using namespace tidas;
   TIDAS_REQUIRE(d && analytic && t_star && x && z && out, "null pointer");
+  TIDAS_REQUIRE(n_peers >= 0 && n_peers <= TIDAS_MAX_PEERS, "n_peers must be in [0, %d]", TIDAS_MAX_PEERS);
+  TIDAS_REQUIRE(n_peers == 0 || peer_out, "null peer_out");
+  for (int q = 0; q < n_peers; ++q) TIDAS_REQUIRE(peer_out[q], "null peer_out[%d]", q);
   TIDAS_REQUIRE(d->n_el >= 2 && d->n_el % 2 == 0, "n_el must be even and >= 2");
   TIDAS_REQUIRE(d->n_samples >= 4, "n_samples must be >= 4");
   TIDAS_REQUIRE(d->n_frames >= 0 && d->n_angles >= 1 && d->nx >= 0 && d->nz >= 0, "bad sizes");
@@ -802,6 +825,8 @@ extern "C" int tidas_das_image(const tidas_das_desc_t* d, const void* analytic, 
   p.ap_half = ap_half; p.t_star = t_star; p.xg = x; p.zg = z;
   p.window = d->window;
   p.geometry = d->geometry;
+  p.n_peer = n_peers;
+  for (int q = 0; q < TIDAS_MAX_PEERS; ++q) p.peer[q] = q < n_peers ? peer_out[q] : nullptr;
   cudaStream_t st = as_stream(stream);
   if (d->prec == TIDAS_PREC_F32) return dispatch_ap<float>(d, p, analytic, out, st);
   if (d->prec == TIDAS_PREC_F64) return dispatch_ap<double>(d, p, analytic, out, st);

@@ -201,8 +201,18 @@ def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=Non
     return out
 
 
-def das_from_analytic(analytic: torch.Tensor, plan: DasPlan, out=None, stream=None) -> torch.Tensor:
-    """K2 on a precomputed analytic batch [F][A][E][N] -> image [F][nz][nx]."""
+MAX_PEERS = 7  # TIDAS_MAX_PEERS
+
+
+def das_from_analytic(analytic: torch.Tensor, plan: DasPlan, out=None, stream=None,
+                      peers: Optional[Sequence[int]] = None) -> torch.Tensor:
+    """K2 on a precomputed analytic batch [F][A][E][N] -> image [F][nz][nx].
+
+    ``peers``: device addresses of up to 7 more buffers laid out like ``out``
+    (e.g. other GPUs' symmetric-memory image buffers, already offset to this
+    batch's first frame); K2's epilogue stores every pixel there too
+    (tidas_das_image_peers). The caller owns their size and the barrier that
+    makes the stores visible."""
     L = _lib.lib()
     F = int(analytic.shape[0])
     if analytic.dtype != _COMPLEX[plan.prec_code]:
@@ -219,9 +229,21 @@ def das_from_analytic(analytic: torch.Tensor, plan: DasPlan, out=None, stream=No
         out = torch.empty((F, plan.nz, plan.nx), dtype=dt, device=analytic.device)
     _check_image_out(out, F, plan, dt, analytic.device)
     d = plan.desc(F)
-    _lib.check(L.tidas_das_image(C.byref(d), _lib.ptr(analytic), _lib.ptr(plan.t_star),
-                                 _lib.ptr(plan.x), _lib.ptr(plan.z), _lib.ptr(plan.ap_half),
-                                 _lib.ptr(out), _lib.stream_handle(stream)))
+    peers = [int(q) for q in (peers or ())]
+    if len(peers) > MAX_PEERS:
+        raise ValueError(f"at most {MAX_PEERS} peer image buffers, got {len(peers)}")
+    if any(q == 0 for q in peers):
+        raise ValueError("null peer image buffer")
+    if not peers:
+        _lib.check(L.tidas_das_image(C.byref(d), _lib.ptr(analytic), _lib.ptr(plan.t_star),
+                                     _lib.ptr(plan.x), _lib.ptr(plan.z), _lib.ptr(plan.ap_half),
+                                     _lib.ptr(out), _lib.stream_handle(stream)))
+        return out
+    table = (C.c_void_p * len(peers))(*peers)
+    _lib.check(L.tidas_das_image_peers(C.byref(d), _lib.ptr(analytic), _lib.ptr(plan.t_star),
+                                       _lib.ptr(plan.x), _lib.ptr(plan.z), _lib.ptr(plan.ap_half),
+                                       _lib.ptr(out), C.cast(table, C.c_void_p), len(peers),
+                                       _lib.stream_handle(stream)))
     return out
 
 
@@ -249,12 +271,15 @@ class DasWorkspace:
 
 
 def das_image(rf: torch.Tensor, plan: DasPlan, *, scale: float = 1.0, out=None,
-              workspace: Optional[DasWorkspace] = None, stream=None) -> torch.Tensor:
+              workspace: Optional[DasWorkspace] = None, stream=None,
+              peers: Optional[Sequence[int]] = None) -> torch.Tensor:
     """Fused DAS of a frame batch.
 
-    rf  : CUDA tensor [F][A][E][N] (or [F][E][N] for one transmit), f64/f32/int16,
-          sample-contiguous rows ("channel-contiguous").
-    out : optional [F][nz][nx] result buffer.
+    rf    : CUDA tensor [F][A][E][N] (or [F][E][N] for one transmit), f64/f32/int16,
+            sample-contiguous rows ("channel-contiguous").
+    out   : optional [F][nz][nx] result buffer.
+    peers : optional device addresses of up to 7 more [F][nz][nx] buffers that
+            receive the same images from K2's epilogue (das_from_analytic).
     """
     if rf.dim() == 3:
         rf = rf.unsqueeze(1)
@@ -278,7 +303,8 @@ def das_image(rf: torch.Tensor, plan: DasPlan, *, scale: float = 1.0, out=None,
         f1 = min(F, f0 + ws.chunk)
         an = ws.buf[: f1 - f0]
         rf_analytic(rf[f0:f1], plan.prec, scale=scale, out=an, stream=stream)
-        das_from_analytic(an, plan, out=out[f0:f1], stream=stream)
+        das_from_analytic(an, plan, out=out[f0:f1], stream=stream,
+                          peers=[q + f0 * out[0].numel() * out.element_size() for q in peers] if peers else None)
     return out
 
 

@@ -143,3 +143,62 @@ def chunk_major_index(f: int, n_local: int, world: int, sub: int) -> int:
     c0 = (i // sub) * sub
     c1 = min(n_local, c0 + sub)
     return world * c0 + r * (c1 - c0) + (i - c0)
+
+
+def peer_destinations(buffer_ptrs: Sequence[int], rank: int, first_unit: int, unit_bytes: int) -> list:
+    """Addresses, in every OTHER rank's copy of a symmetric [n_units][...]
+    buffer, of this rank's first unit: where K2's epilogue stores its images."""
+    off = int(first_unit) * int(unit_bytes)
+    return [int(p) + off for r, p in enumerate(buffer_ptrs) if r != rank]
+
+
+class PeerImageGather:
+    """Image gather fused into K2 (north star (e) over NVLink, no NCCL kernel).
+
+    Every rank holds the whole batch's images in one symmetric-memory buffer
+    [n_units][...] (torch symmetric memory: the same allocation mapped into
+    every GPU of the node). Rank r images its shard straight into its own slice
+    and, from the same epilogue, into the slice of every peer's copy
+    (``das_image(..., peers=self.peers)``): the gather traffic leaves the SMs as
+    the tiles finish instead of after the last one. ``begin`` / ``end`` are
+    device-side barriers over the group on the current stream: nobody
+    overwrites a peer's buffer before that peer is done with the previous
+    step, and after ``end`` every rank's copy holds every image (the barrier's
+    system-scope release / acquire orders the kernel's peer stores)."""
+
+    def __init__(self, n_units: int, unit_shape: Sequence[int], dtype, device, group=None):
+        import torch.distributed._symmetric_memory as symm
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if world - 1 > 7:
+            raise ValueError("at most 8 ranks (7 peers per K2 launch)")
+        self.buf = symm.empty((n_units, *unit_shape), dtype=dtype, device=device)
+        self.handle = symm.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
+        self.a, self.b = shard_range(n_units, rank, world)
+        unit_bytes = self.buf[0].numel() * self.buf.element_size()
+        self.peers = peer_destinations(self.handle.buffer_ptrs, rank, self.a, unit_bytes)
+
+    def local(self) -> torch.Tensor:
+        """This rank's slice of its own copy: the ``out`` of its K2 launches."""
+        return self.buf[self.a:self.b]
+
+    def begin(self) -> None:
+        self.handle.barrier(channel=0)
+
+    def end(self) -> None:
+        self.handle.barrier(channel=1)
+
+
+def try_peer_gather(n_units: int, unit_shape: Sequence[int], dtype, device, group=None):
+    """A PeerImageGather if every rank could set one up (agreed over the group,
+    so no rank goes on alone), else None — the caller then gathers over NCCL."""
+    ok, pg, err = 1, None, None
+    try:
+        pg = PeerImageGather(n_units, unit_shape, dtype, device, group)
+    except Exception as e:  # no symmetric-memory support on this node / build
+        ok, err = 0, f"{type(e).__name__}: {e}"
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        t = torch.tensor([ok], device=device, dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        ok = int(t.item())
+    return (pg if ok else None), err

@@ -135,3 +135,10 @@ def test_relaunch_spawns_ranks_like_bench():
     lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert lines == [{"world": 2, "ok": True}]
 
+
+
+def test_peer_destinations_skip_self_and_offset():
+    from paper_2507_15464_b200.parallel import peer_destinations
+    ptrs = [1000, 5000, 9000, 13000]
+    assert peer_destinations(ptrs, 1, 3, 16) == [1048, 9048, 13048]
+    assert peer_destinations(ptrs[:1], 0, 0, 16) == []

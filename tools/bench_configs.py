@@ -109,6 +109,26 @@ def run_configs(names, steps=10, warmup=3, echo=False, rank=0, world=1, timed=No
                 parallel.gather_images(img, total, out=full)
 
         ms = timed(step, steps, warmup)
+        ms_nccl, peer_err = None, None
+        if gather:
+            # the same gather fused into K2: the epilogue stores every pixel into each
+            # peer's symmetric-memory copy over NVLink, one device barrier per step
+            pg, peer_err = parallel.try_peer_gather(total, (c["nz"], c["nx"]), torch.float32, img.device)
+            if pg is not None:
+                def step_peer():
+                    pg.begin()
+                    tb.das_image(rf, plan, out=pg.local(), workspace=ws, peers=pg.peers)
+                    pg.end()
+
+                ms_nccl, ms = ms, timed(step_peer, steps, warmup)
+                if pipelined:
+                    order = [parallel.chunk_major_index(f, n_local, world, sub) for f in range(total)]
+                    ref = full[torch.tensor(order, device=full.device)]
+                else:
+                    ref = full
+                if not (torch.equal(pg.local(), img) and torch.equal(pg.buf, ref)):
+                    raise RuntimeError("peer-gathered images differ from the NCCL all-gather")
+                del pg
         fps = total / (ms / 1e3)
         gbs = c["bytes"] * fps / world / 1e9
         res[name] = {"frames_total": total, "frames_per_rank": int(rf.shape[0]), "ms_per_step": ms,
@@ -116,9 +136,14 @@ def run_configs(names, steps=10, warmup=3, echo=False, rank=0, world=1, timed=No
                      "hbm_frac": gbs / hbm, "rf_dtype": str(c["dtype"]).replace("torch.", ""),
                      "transmits": len(c["angles"]), "grid": [c["nz"], c["nx"]], "out": c["out"],
                      "chunk_frames": ws.chunk, "scaling": "weak" if c["per_rank"] else "strong",
-                     "gather": ("NCCL all_gather_into_tensor of the images, pipelined per "
-                                f"{sub} frames" if pipelined else "NCCL all_gather_into_tensor of the images")
+                     "gather": ("K2 epilogue stores into every peer's symmetric-memory image buffer over "
+                                "NVLink (tidas_das_image_peers) + device barrier; NCCL all-gather timed beside it"
+                                if ms_nccl is not None else
+                                ("NCCL all_gather_into_tensor of the images, pipelined per "
+                                 f"{sub} frames" if pipelined else "NCCL all_gather_into_tensor of the images")
+                                + (f" (peer stores unavailable: {peer_err})" if peer_err else ""))
                                if gather else "none",
+                     "nccl_gather_frames_per_s": total / (ms_nccl / 1e3) if ms_nccl else None,
                      "checksum": float(img.double().sum())}
         if echo:
             print(json.dumps({name: res[name]}), flush=True)
