@@ -72,6 +72,17 @@ int tidas_rf_analytic(const void* rf, int rf_dtype, int64_t rf_row_stride, doubl
                       int32_t* support, void* stream);
 
 /*
+ * The same transform, storing only output samples lo .. hi of every row (the
+ * others are left untouched; lo <= hi, clipped to [0, n_samples)). The DAS
+ * path passes its plan's tap range (tidas_das_window_range): K2 never reads
+ * outside it, and at cfg2 / cfg5 it is ~52% / ~39% of the row — the analytic
+ * intermediate's DRAM writes shrink by as much. ABI 5.
+ */
+int tidas_rf_analytic_range(const void* rf, int rf_dtype, int64_t rf_row_stride, double scale,
+                            void* out, int out_prec, int64_t n_rows, int32_t n_samples,
+                            int32_t lo, int32_t hi, int32_t* support, void* stream);
+
+/*
  * Spectral fractional delay (das.py:108-111, method="spectral"): complex
  * IFFT(FFT(x) * exp(-2 pi i f shift / fs)) per row, f on numpy's fftfreq grid;
  * the caller keeps the real part. x: [n_rows][n_samples] double, out: double2.
@@ -118,6 +129,16 @@ typedef struct {
  */
 int tidas_das_window(const tidas_das_desc_t* desc, const double* t_star, const double* x,
                      const double* z, const int32_t* ap_half, int32_t* max_window, void* stream);
+
+/*
+ * tidas_das_window plus, in range[0..1] (device int32[2], may be NULL), the
+ * union of those tile windows over the plan: every sample index a live tap of
+ * K2 can read (range[0] > range[1] when no pixel is active; indices outside
+ * [0, n_samples) mean the taps wrap around the row). ABI 5.
+ */
+int tidas_das_window_range(const tidas_das_desc_t* desc, const double* t_star, const double* x,
+                           const double* z, const int32_t* ap_half, int32_t* max_window,
+                           int32_t* range, void* stream);
 
 /*
  *   analytic : [F][A][n_el][N] complex (from tidas_rf_analytic, same prec)

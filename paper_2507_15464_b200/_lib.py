@@ -41,11 +41,13 @@ SIGNATURES = {
     "tidas_abi_version": ([], C.c_int),
     "tidas_init": ([C.c_int], C.c_int),
     "tidas_rf_analytic": ([_P, C.c_int, _I64, _D, _P, C.c_int, _I64, _I32, _P, _P], C.c_int),
+    "tidas_rf_analytic_range": ([_P, C.c_int, _I64, _D, _P, C.c_int, _I64, _I32, _I32, _I32, _P, _P], C.c_int),
     "tidas_spectral_shift_f64": ([_P, _I64, _I32, _D, _P, _P], C.c_int),
     "tidas_plane_wave_arrivals": ([_P, _I32, _P, _I32, _P, _I32, _I32, _D, _D, _P, _P], C.c_int),
     "tidas_das_image": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "tidas_das_image_peers": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P, _P, _I32, _P], C.c_int),
     "tidas_das_window": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P], C.c_int),
+    "tidas_das_window_range": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "tidas_delayed_sum_f64": ([_P, _I32, _I32, _P, _P, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "tidas_window_envelope_f64": ([_P, _I32, _P, _P, _P, _P, _P, _I32, _P, _P], C.c_int),
     "tidas_window_dots_f64": ([_P, _P, _I32, _P, _P, _I32, _P, _P], C.c_int),

@@ -11,6 +11,7 @@
 // (fft.cuh); other lengths use Bluestein's chirp-z on a power-of-two grid
 // (bluestein_* below), which keeps the exact length-N periodic semantics.
 #include <math.h>
+#include <climits>
 
 #include <algorithm>
 
@@ -252,22 +253,27 @@ __device__ __forceinline__ float2 conj_scaled(float2 a, float s) { return make_f
 
 // Output rows: complex (input real part, Hilbert part), the real parts re-read
 // (L2) in batches of 8 slots so that 16 loads are in flight before the stores.
+// Only samples lo .. hi are stored (the range the consumer reads, e.g. the DAS
+// plan's tap range: tidas_rf_analytic_range); the transform itself is global.
 template <typename In, bool SCALED, typename IDX>
 __device__ __forceinline__ void store_analytic_pair(const In* src_a, const In* src_b, bool has_b, float scale,
                                                     const float2 (&v)[32], cplx<float>* dst_a, cplx<float>* dst_b,
-                                                    IDX idx) {
+                                                    IDX idx, int lo, int hi) {
+  const unsigned span = (unsigned)(hi - lo);
 #pragma unroll
   for (int j0 = 0; j0 < 32; j0 += 8) {
     float ra[8], rb[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int n = idx(j0 + q);
-      ra[q] = (float)load_as_double(src_a + n);
-      rb[q] = has_b ? (float)load_as_double(src_b + n) : 0.0f;
+      const bool keep = (unsigned)(n - lo) <= span;
+      ra[q] = keep ? (float)load_as_double(src_a + n) : 0.0f;
+      rb[q] = keep && has_b ? (float)load_as_double(src_b + n) : 0.0f;
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int n = idx(j0 + q);
+      if ((unsigned)(n - lo) > span) continue;
       float2 a; a.x = scaled<SCALED>(ra[q], scale); a.y = v[j0 + q].x;
       dst_a[n] = a;
       if (has_b) { float2 b; b.x = scaled<SCALED>(rb[q], scale); b.y = v[j0 + q].y; dst_b[n] = b; }
@@ -343,7 +349,7 @@ template <bool INV> __device__ __forceinline__ void dft64_pair_dif(float2 (&w)[3
 template <typename In, bool SCALED, bool SUPPORT, bool BULK>
 __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                            cplx<float>* __restrict__ out, int64_t n_rows,
-                                                           int32_t* __restrict__ support) {
+                                                           int32_t* __restrict__ support, int s_lo, int s_hi) {
   constexpr int N = 4096, LP = 65;
   constexpr int SH = TW_LOG - 12;
   __shared__ float2 S[64 * LP];
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   dft64_pair_dif<true>(w, v, h);  // slot j: x[t + 64 (2 sig32(j) + h)]
   cplx<float>* dst_a = out + ra * (int64_t)N;
   store_analytic_pair<In, SCALED>(row_a, row_b, has_b, scale, v, dst_a, dst_a + N,
-                                  [&](int j) { return t + 64 * (2 * sig32(j) + hi); });
+                                  [&](int j) { return t + 64 * (2 * sig32(j) + hi); }, s_lo, s_hi);
   if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -604,7 +610,7 @@ template <bool INV> __device__ __forceinline__ void dft128_quad_dif(float2 (&y)[
 template <typename In, bool SCALED, bool SUPPORT>
 __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                                 cplx<float>* __restrict__ out, int64_t n_rows,
-                                                                int32_t* __restrict__ support) {
+                                                                int32_t* __restrict__ support, int s_lo, int s_hi) {
   constexpr int N = 8192;
   constexpr int LP1 = 65, LP2 = 129;  // [128][65] and [64][129] transposes: conflict-free columns
   constexpr int SH = TW_LOG - 13;
@@ -734,7 +740,7 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   dft128_quad_dif<true>(y, v, q0, q1);  // slot j: x[n1 + 64 (q0 + 2 q1 + 4 sig32(j))]
   cplx<float>* dst_a = out + ra * (int64_t)N;
   store_analytic_pair<In, SCALED>(src_a, src_b, has_b, scale, v, dst_a, dst_a + N,
-                                  [&](int j) { return n1 + 64 * (mq + 4 * sig32(j)); });
+                                  [&](int j) { return n1 + 64 * (mq + 4 * sig32(j)); }, s_lo, s_hi);
   if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -758,7 +764,7 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
 template <typename In, bool SCALED, bool SUPPORT>
 __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                             cplx<float>* __restrict__ out, int64_t n_rows,
-                                                            int32_t* __restrict__ support) {
+                                                            int32_t* __restrict__ support, int s_lo, int s_hi) {
   constexpr int N = 2048, LP1 = 33, LP2 = 65;  // [64][33] and [32][65] transposes
   constexpr int SH = TW_LOG - 11;
   __shared__ float2 S[64 * LP1 > 32 * LP2 ? 64 * LP1 : 32 * LP2];
@@ -874,7 +880,7 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   dft64_pair_dif<true>(w, v, h);  // slot j: x[n1 + 32 (2 sig32(j) + h)]
   cplx<float>* dst_a = out + ra * (int64_t)N;
   store_analytic_pair<In, SCALED>(src_a, src_b, has_b, scale, v, dst_a, dst_a + N,
-                                  [&](int j) { return n1 + 32 * (2 * sig32(j) + hi); });
+                                  [&](int j) { return n1 + 32 * (2 * sig32(j) + hi); }, s_lo, s_hi);
   if (SUPPORT) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1067,7 +1073,11 @@ static K pick4(K plain, K support_only, K scaled_only, K both, double scale, con
 
 template <typename R, typename In>
 static int launch_analytic(const In* rf, int64_t stride, double scale, void* out, int64_t n_rows,
-                           int32_t N, int32_t* support, double shift, cudaStream_t st) {
+                           int32_t N, int32_t* support, double shift, cudaStream_t st, int lo = 0,
+                           int hi = INT_MAX) {
+  // the register four-step kernels store only samples lo .. hi; the others store every sample
+  lo = lo < 0 ? 0 : lo;
+  hi = hi > N - 1 ? N - 1 : hi;
   using C = cplx<R>;
   int dev = 0;
   TIDAS_CUDA_CHECK(cudaGetDevice(&dev));
@@ -1092,7 +1102,7 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         auto k2 = pick4(analytic_r2048_kernel<In, false, false>, analytic_r2048_kernel<In, false, true>,
                         analytic_r2048_kernel<In, true, false>, analytic_r2048_kernel<In, true, true>, scale, support);
         TIDAS_CUDA_CHECK(launch_pdl(k2, dim3((unsigned)((n_rows + 1) / 2)), dim3(64), 0, st,
-                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
+                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi));
         return TIDAS_OK;
       }
       if (!delay && logN == 13) {
@@ -1101,7 +1111,7 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         const size_t smem8 = sizeof(float2) * 128 * 65;
         TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8));
         TIDAS_CUDA_CHECK(launch_pdl(kr, dim3((unsigned)((n_rows + 1) / 2)), dim3(256), smem8, st, rf, stride,
-                                    (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
+                                    (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi));
         return TIDAS_OK;
       }
       if (!delay && logN == 12) {
@@ -1117,7 +1127,7 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         const size_t dyn = bulk ? 2 * 4096 * sizeof(In) : 0;
         if (bulk) TIDAS_CUDA_CHECK(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         TIDAS_CUDA_CHECK(launch_pdl(k4, dim3((unsigned)((n_rows + 1) / 2)), dim3(128), dyn, st,
-                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support));
+                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi));
         return TIDAS_OK;
       }
     }
@@ -1152,14 +1162,17 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
 template <typename R>
 static int dispatch_analytic(const void* rf, int dtype, int64_t stride, double scale, void* out,
                              int64_t n_rows, int32_t N, int32_t* support, double shift,
-                             cudaStream_t st) {
+                             cudaStream_t st, int lo = 0, int hi = INT_MAX) {
   switch (dtype) {
     case TIDAS_F64:
-      return launch_analytic<R>(static_cast<const double*>(rf), stride, scale, out, n_rows, N, support, shift, st);
+      return launch_analytic<R>(static_cast<const double*>(rf), stride, scale, out, n_rows, N, support, shift, st,
+                                lo, hi);
     case TIDAS_F32:
-      return launch_analytic<R>(static_cast<const float*>(rf), stride, scale, out, n_rows, N, support, shift, st);
+      return launch_analytic<R>(static_cast<const float*>(rf), stride, scale, out, n_rows, N, support, shift, st,
+                                lo, hi);
     case TIDAS_I16:
-      return launch_analytic<R>(static_cast<const int16_t*>(rf), stride, scale, out, n_rows, N, support, shift, st);
+      return launch_analytic<R>(static_cast<const int16_t*>(rf), stride, scale, out, n_rows, N, support, shift, st,
+                                lo, hi);
   }
   set_error("unknown rf dtype %d", dtype);
   return TIDAS_EINVAL;
@@ -1172,7 +1185,15 @@ extern "C" int tidas_init(int device) { return tidas::ensure_init(device); }
 extern "C" int tidas_rf_analytic(const void* rf, int rf_dtype, int64_t rf_row_stride, double scale,
                                  void* out, int out_prec, int64_t n_rows, int32_t n_samples,
                                  int32_t* support, void* stream) {
+  return tidas_rf_analytic_range(rf, rf_dtype, rf_row_stride, scale, out, out_prec, n_rows, n_samples, 0,
+                                 n_samples - 1, support, stream);
+}
+
+extern "C" int tidas_rf_analytic_range(const void* rf, int rf_dtype, int64_t rf_row_stride, double scale,
+                                       void* out, int out_prec, int64_t n_rows, int32_t n_samples,
+                                       int32_t lo, int32_t hi, int32_t* support, void* stream) {
   using namespace tidas;
+  TIDAS_REQUIRE(lo <= hi, "empty sample range [%d, %d]", lo, hi);
   TIDAS_REQUIRE(n_rows >= 0 && n_rows < (int64_t(1) << 31), "n_rows out of range");
   if (n_rows == 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
   TIDAS_REQUIRE(rf && out, "null pointer");
@@ -1181,9 +1202,11 @@ extern "C" int tidas_rf_analytic(const void* rf, int rf_dtype, int64_t rf_row_st
   if (n_rows == 0) return TIDAS_OK;
   const double hilbert = nan("");
   if (out_prec == TIDAS_PREC_F32)
-    return dispatch_analytic<float>(rf, rf_dtype, rf_row_stride, scale, out, n_rows, n_samples, support, hilbert, as_stream(stream));
+    return dispatch_analytic<float>(rf, rf_dtype, rf_row_stride, scale, out, n_rows, n_samples, support, hilbert,
+                                    as_stream(stream), lo, hi);
   if (out_prec == TIDAS_PREC_F64)
-    return dispatch_analytic<double>(rf, rf_dtype, rf_row_stride, scale, out, n_rows, n_samples, support, hilbert, as_stream(stream));
+    return dispatch_analytic<double>(rf, rf_dtype, rf_row_stride, scale, out, n_rows, n_samples, support, hilbert,
+                                     as_stream(stream), lo, hi);
   set_error("unknown precision %d", out_prec);
   return TIDAS_EINVAL;
 }

@@ -609,26 +609,37 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
     const int f = f0 + b;
     if (f >= p.F) break;
     const int64_t o = ((int64_t)f * p.nz + iz) * p.nx + ix;
-    if constexpr (OUT == TIDAS_OUT_IQ) {
-      reinterpret_cast<C*>(out_)[o] = acc_iq[b];
+    if (OUT == TIDAS_OUT_ENVELOPE) reinterpret_cast<R*>(out_)[o] = acc_env[b];
+    else if (OUT == TIDAS_OUT_COHERENT) reinterpret_cast<R*>(out_)[o] = cabs_(acc_iq[b]);
+    else reinterpret_cast<C*>(out_)[o] = acc_iq[b];
+  }
+#ifndef TIDAS_DAS_NO_PEERS
+  // the same values into every peer destination (one rolled loop: the common
+  // n_peer = 0 case costs one uniform branch)
+#pragma unroll 1
+  for (int q = 0; q < p.n_peer; ++q) {
+    unsigned char* dst = reinterpret_cast<unsigned char*>(p.peer[q]);
 #pragma unroll
-      for (int q = 0; q < TIDAS_MAX_PEERS; ++q)
-        if (q < p.n_peer) reinterpret_cast<C*>(p.peer[q])[o] = acc_iq[b];
-    } else {
-      const R v = OUT == TIDAS_OUT_ENVELOPE ? acc_env[b] : cabs_(acc_iq[b]);
-      reinterpret_cast<R*>(out_)[o] = v;
-#pragma unroll
-      for (int q = 0; q < TIDAS_MAX_PEERS; ++q)  // static indices: the pointers stay in the parameter bank
-        if (q < p.n_peer) reinterpret_cast<R*>(p.peer[q])[o] = v;
+    for (int b = 0; b < FB; ++b) {
+      const int f = f0 + b;
+      if (f >= p.F) break;
+      const int64_t o = ((int64_t)f * p.nz + iz) * p.nx + ix;
+      if (OUT == TIDAS_OUT_ENVELOPE) reinterpret_cast<R*>(dst)[o] = acc_env[b];
+      else if (OUT == TIDAS_OUT_COHERENT) reinterpret_cast<R*>(dst)[o] = cabs_(acc_iq[b]);
+      else reinterpret_cast<C*>(dst)[o] = acc_iq[b];
     }
   }
+#endif
 }
 
 // The plan's largest per-CTA sample window over all transmits, for the FP32
 // tile shape (WZ x DG depths x 32 / WZ columns): K2's own window logic
 // (pixel_aperture, pixel_arrival), one CTA per pixel tile, max into *out.
+// With `range` (int32[2], may be NULL) it also gathers the union of those
+// windows, [min lo, max hi]: every sample a live tap of K2 can read.
 template <int AP>
-__global__ void __launch_bounds__(256) das_window_kernel(DasParams p, int32_t* __restrict__ out) {
+__global__ void __launch_bounds__(256) das_window_kernel(DasParams p, int32_t* __restrict__ out,
+                                                         int32_t* __restrict__ range) {
   using S = DasShape<float>;
   constexpr int WZ = S::WZ, WX = 32 / WZ;
   __shared__ int lo_s, hi_s;
@@ -641,7 +652,7 @@ __global__ void __launch_bounds__(256) das_window_kernel(DasParams p, int32_t* _
   const double zm = pix ? p.zg[iz] : 1.0;
   int n_lo, n_hi, ap_h, m_min;
   pixel_aperture<AP>(p, pix, iz, x, zm, n_lo, n_hi, ap_h, m_min);
-  int wmax = 0;
+  int wmax = 0, ulo = INT_MAX, uhi = INT_MIN;
   for (int a = 0; a < p.A; ++a) {
     int k0;
     float fr;
@@ -652,10 +663,17 @@ __global__ void __launch_bounds__(256) das_window_kernel(DasParams p, int32_t* _
     const int wh = __reduce_max_sync(0xffffffffu, active ? k0 - m_min + 1 : INT_MIN);
     if (lane == 0) { atomicMin(&lo_s, wl); atomicMax(&hi_s, wh); }
     __syncthreads();
-    if (hi_s >= lo_s) wmax = max(wmax, hi_s - lo_s + 1);
+    if (hi_s >= lo_s) {
+      wmax = max(wmax, hi_s - lo_s + 1);
+      ulo = min(ulo, lo_s);
+      uhi = max(uhi, hi_s);
+    }
     __syncthreads();
   }
-  if (threadIdx.x == 0 && threadIdx.y == 0 && wmax > 0) atomicMax(out, wmax);
+  if (threadIdx.x == 0 && threadIdx.y == 0 && wmax > 0) {
+    atomicMax(out, wmax);
+    if (range) { atomicMin(range, ulo); atomicMax(range + 1, uhi); }
+  }
 }
 
 __global__ void plane_wave_arrivals_kernel(const double* x, int nx, const double* z, int nz,
@@ -836,6 +854,12 @@ extern "C" int tidas_das_image_peers(const tidas_das_desc_t* d, const void* anal
 
 extern "C" int tidas_das_window(const tidas_das_desc_t* d, const double* t_star, const double* x,
                                 const double* z, const int32_t* ap_half, int32_t* max_window, void* stream) {
+  return tidas_das_window_range(d, t_star, x, z, ap_half, max_window, nullptr, stream);
+}
+
+extern "C" int tidas_das_window_range(const tidas_das_desc_t* d, const double* t_star, const double* x,
+                                      const double* z, const int32_t* ap_half, int32_t* max_window,
+                                      int32_t* range, void* stream) {
   using namespace tidas;
   TIDAS_REQUIRE(d && t_star && x && z && max_window, "null pointer");
   TIDAS_REQUIRE(d->n_el >= 2 && d->n_el % 2 == 0, "n_el must be even and >= 2");
@@ -845,6 +869,10 @@ extern "C" int tidas_das_window(const tidas_das_desc_t* d, const double* t_star,
                 d->aperture);
   cudaStream_t st = as_stream(stream);
   TIDAS_CUDA_CHECK(cudaMemsetAsync(max_window, 0, sizeof(int32_t), st));
+  if (range) {  // empty-range sentinels 0x7f7f7f7f / 0x80808080 (min / max identities here)
+    TIDAS_CUDA_CHECK(cudaMemsetAsync(range, 0x7f, sizeof(int32_t), st));
+    TIDAS_CUDA_CHECK(cudaMemsetAsync(range + 1, 0x80, sizeof(int32_t), st));
+  }
   if (d->nx == 0 || d->nz == 0) return TIDAS_OK;
   DasParams p;
   memset(&p, 0, sizeof(p));
@@ -856,8 +884,8 @@ extern "C" int tidas_das_window(const tidas_das_desc_t* d, const double* t_star,
   constexpr int TXC = (32 / S::WZ) * (DAS_NW / S::DG);  // tile columns
   const dim3 grid((d->nz + S::WZ * S::DG - 1) / (S::WZ * S::DG), (d->nx + TXC - 1) / TXC);
   TIDAS_REQUIRE(grid.y <= 65535, "pixel grid too large");
-  if (d->aperture == TIDAS_AP_HANN) das_window_kernel<TIDAS_AP_HANN><<<grid, dim3(32, 8), 0, st>>>(p, max_window);
-  else das_window_kernel<TIDAS_AP_REF_BOXCAR><<<grid, dim3(32, 8), 0, st>>>(p, max_window);
+  if (d->aperture == TIDAS_AP_HANN) das_window_kernel<TIDAS_AP_HANN><<<grid, dim3(32, 8), 0, st>>>(p, max_window, range);
+  else das_window_kernel<TIDAS_AP_REF_BOXCAR><<<grid, dim3(32, 8), 0, st>>>(p, max_window, range);
   TIDAS_LAUNCH_CHECK();
   return TIDAS_OK;
 }

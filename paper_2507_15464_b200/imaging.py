@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -59,6 +59,7 @@ class DasPlan:
     geometry: str = "fast"
     _desc: Optional[_lib.DasDesc] = field(default=None, repr=False)
     _window: Optional[int] = field(default=None, repr=False)
+    _range: Optional[Tuple[int, int]] = field(default=None, repr=False)
 
     def __post_init__(self):
         if self.geometry not in GEOMETRIES:
@@ -113,14 +114,31 @@ class DasPlan:
                 d.aperture, d.f_number = _lib.AP_HANN, float(self.aperture[1])
             else:
                 d.aperture, d.f_number = _lib.AP_REF_BOXCAR, 1.0
-            w = torch.zeros(1, dtype=torch.int32, device=self.x.device)
+            w = torch.zeros(3, dtype=torch.int32, device=self.x.device)
             with torch.cuda.device(self.x.device):
-                _lib.check(_lib.lib().tidas_das_window(
+                _lib.check(_lib.lib().tidas_das_window_range(
                     C.byref(d), _lib.ptr(self.t_star), _lib.ptr(self.x), _lib.ptr(self.z),
                     _lib.ptr(self.ap_half) if self.ap_half is not None else None, _lib.ptr(w),
-                    _lib.stream_handle()))
-                self._window = int(w.item())
+                    _lib.ptr(w[1:]), _lib.stream_handle()))
+                self._window, lo, hi = (int(v) for v in w.tolist())
+            N = self.n_samples
+            if lo > hi:            # no active pixel: K2 reads nothing
+                self._range = (0, 0)
+            elif lo < 0 or hi > N - 1:  # taps wrap around the row
+                self._range = (0, N - 1)
+            else:                  # + 2 samples of slack each side (free: K1 computes every sample)
+                self._range = (max(0, lo - 2), min(N - 1, hi + 2))
         return self._window
+
+    def sample_range(self) -> Tuple[int, int]:
+        """Samples (lo, hi) of each analytic row K2 can read for this plan: the
+        union of its tile windows (tidas_das_window_range), for FP32 plans; the
+        whole row for FP64 (drop-in) plans. ``das_image`` has K1 store only
+        these (tidas_rf_analytic_range)."""
+        if self.prec != "f32":
+            return (0, self.n_samples - 1)
+        self.window()
+        return self._range
 
 
 def _dev(a, dtype, device) -> torch.Tensor:
@@ -168,11 +186,15 @@ def table_plan(*, n_el: int, pitch: float, fs: float, c: float, n_samples: int, 
 
 
 def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=None,
-                support: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                support: Optional[torch.Tensor] = None, stream=None,
+                sample_range: Optional[Tuple[int, int]] = None) -> torch.Tensor:
     """K1: periodic analytic signal of every row of rf [..., N] (f64/f32/int16).
 
     Returns complex64 (prec "f32") or complex128 (prec "f64") of the same shape.
     ``support`` (int32 [rows, 2]) receives first / last nonzero sample per row.
+    ``sample_range`` (lo, hi): store only output samples lo .. hi of each row
+    (tidas_rf_analytic_range; the rest of ``out`` is left as it was) — what
+    ``das_image`` passes from its plan (``DasPlan.sample_range``).
     """
     L = _lib.lib()
     if not rf.is_cuda:
@@ -195,9 +217,17 @@ def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=Non
     if support is not None and (support.dtype != torch.int32 or support.numel() != 2 * rows
                                 or not support.is_contiguous() or support.device != rf.device):
         raise ValueError(f"support must be a contiguous int32 tensor of {rows} x 2 on {rf.device}")
-    _lib.check(L.tidas_rf_analytic(_lib.ptr(rf), _lib.DTYPE_CODE[rf.dtype], n, float(scale),
-                                   _lib.ptr(out), pc, rows, n, _lib.ptr(support),
-                                   _lib.stream_handle(stream)))
+    if sample_range is None:
+        _lib.check(L.tidas_rf_analytic(_lib.ptr(rf), _lib.DTYPE_CODE[rf.dtype], n, float(scale),
+                                       _lib.ptr(out), pc, rows, n, _lib.ptr(support),
+                                       _lib.stream_handle(stream)))
+        return out
+    lo, hi = (int(v) for v in sample_range)
+    if lo > hi:
+        raise ValueError(f"empty sample range {sample_range}")
+    _lib.check(L.tidas_rf_analytic_range(_lib.ptr(rf), _lib.DTYPE_CODE[rf.dtype], n, float(scale),
+                                         _lib.ptr(out), pc, rows, n, lo, hi, _lib.ptr(support),
+                                         _lib.stream_handle(stream)))
     return out
 
 
@@ -302,7 +332,7 @@ def das_image(rf: torch.Tensor, plan: DasPlan, *, scale: float = 1.0, out=None,
     for f0 in range(0, F, ws.chunk):
         f1 = min(F, f0 + ws.chunk)
         an = ws.buf[: f1 - f0]
-        rf_analytic(rf[f0:f1], plan.prec, scale=scale, out=an, stream=stream)
+        rf_analytic(rf[f0:f1], plan.prec, scale=scale, out=an, stream=stream, sample_range=plan.sample_range())
         das_from_analytic(an, plan, out=out[f0:f1], stream=stream,
                           peers=[q + f0 * out[0].numel() * out.element_size() for q in peers] if peers else None)
     return out
