@@ -333,13 +333,15 @@ def main():
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     stream = torch.cuda.current_stream()
 
+    dist_on = world > 1 or parallel.rehearsal()  # rehearsal: one rank, every collective issued
+
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(v):
-        if world > 1:
+        if dist_on:
             t = torch.tensor([v], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return float(t.item())
@@ -414,7 +416,7 @@ def main():
     for _ in range(8):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
-        tb.rf_analytic(rf[:per_launch], plan.prec, out=an)
+        tb.rf_analytic(rf[:per_launch], plan.prec, out=an, sample_range=plan.sample_range())  # as das_image
         ev[1].record(stream)
         tb.das_from_analytic(an, plan, out=img[:per_launch])
         ev[2].record(stream)
@@ -442,14 +444,34 @@ def main():
                        "the HBM roofline above is the contract metric"}
     # the HBM fraction this pipeline could reach at both kernels' own floors: K1 at HBM
     # speed on its RF read + complex64 write, K2 at the shared-memory gather floor
-    k1_floor_us = (128 * 4096 * (4 + 8)) / (hbm * 1e9) * 1e6
+    r_lo, r_hi = plan.sample_range()  # K1 stores only the samples K2's taps can read
+    k1_floor_us = 128 * (4096 * 4 + (r_hi - r_lo + 1) * 8) / (hbm * 1e9) * 1e6
     k2_floor_us = pairs * 24 / (smem_peak * 1e9) * 1e6
     roofline["ceiling"] = {
         "frac": BYTES_PER_FRAME_CFG2 / ((k1_floor_us + k2_floor_us) * 1e-6) / 1e9 / hbm,
         "K1_floor_us": k1_floor_us, "K2_floor_us": k2_floor_us,
-        "note": "HBM fraction at K1's HBM floor (RF in + complex64 analytic out) plus K2's shared-memory "
+        "note": "HBM fraction at K1's HBM floor (RF in + the stored complex64 sample range out) plus K2's shared-memory "
                 "gather floor (24 B per live pixel-channel pair at 128 B/clk/SM): the DAS gather, not HBM, "
                 "bounds the pipeline; achieved / ceiling = frac / ceiling.frac"}
+
+    # the same step at an L2-sized chunk: the analytic intermediate of 24 frames
+    # (~53 MB) stays in L2 between K1 and K2 and is overwritten there by the next
+    # chunk, at the price of shorter launches (more last-wave tails)
+    plan_l2 = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
+                                 n_samples=cfg["n_samples"], x=x, z=z, angles=[0.0], f_number=cfg["f_number"],
+                                 device=dev)
+    plan_l2.chunk_bytes = 24 * cfg["n_el"] * cfg["n_samples"] * 8
+    ws_l2 = imaging.DasWorkspace(plan_l2, dev)
+    ms_l2 = timed(lambda: tb.das_image(rf, plan_l2, out=img, workspace=ws_l2), max(3, args.steps // 2), 2)
+    tr_l2 = (tr or {}).get("l2_chunk")
+    roofline["l2_resident_chunk"] = {
+        "chunk_frames": ws_l2.chunk, "frames_per_s": total_frames / (ms_l2 / 1e3),
+        "dram_bytes_per_frame": tr_l2.get("dram_bytes_per_frame") if tr_l2 else None,
+        "x_algorithmic": tr_l2.get("x_algorithmic") if tr_l2 else None,
+        "traffic_source": tr_l2.get("source") if tr_l2 else None,
+        "note": "DasPlan.chunk_bytes sized for L2: DRAM traffic near the algorithmic bytes, lower throughput; "
+                "the default chunk (headline) is the faster one"}
+    del ws_l2, plan_l2
 
     # e2e through the public API with pinned host buffers (HostPipeline: H2D of
     # chunk i+1 || K1 + K2 of chunk i || D2H of chunk i-1, three streams)
@@ -661,10 +683,12 @@ def main():
             "gpu_launches": launches, "gpu_launches_e2e": launches_e2e, "clocks": clocks,
             "tidas": tidas, "theta_error_sweep": sweep, "other_configs": others,
             "tidas_line_cpu_baseline": line_cpu,
-            "nccl": nccl_summary() if world > 1 else None,
+            "nccl": nccl_summary() if dist_on else None,
         }
+        if parallel.rehearsal():
+            line["rehearsal"] = "TIDAS_DIST_REHEARSAL: one rank issuing the multi-rank step's collectives; not a scaling number"
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
     return 0

@@ -384,12 +384,18 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
       const unsigned bytes = (unsigned)(N * sizeof(In));
       asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(bar), "r"(has_b ? 2 * bytes : bytes)
                    : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                   ::"r"((unsigned)__cvta_generic_to_shared(rows)), "l"(src_a), "r"(bytes), "r"(bar) : "memory");
+      // the RF rows are read once: evict-first in L2, so the stream does not push
+      // out the analytic rows K2 is about to read (and the next chunk overwrites)
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+          ::"r"((unsigned)__cvta_generic_to_shared(rows)), "l"(src_a), "r"(bytes), "r"(bar), "l"(pol) : "memory");
       if (has_b)
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                     ::"r"((unsigned)__cvta_generic_to_shared(rows + N)), "l"(src_b), "r"(bytes), "r"(bar)
-                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+            ::"r"((unsigned)__cvta_generic_to_shared(rows + N)), "l"(src_b), "r"(bytes), "r"(bar), "l"(pol)
+            : "memory");
     }
     __syncthreads();  // the barrier is initialised before anyone waits on it
     asm volatile(

@@ -609,9 +609,11 @@ __global__ void __launch_bounds__(32 * DAS_NW + 32, MINB) das_image_kernel(DasPa
     const int f = f0 + b;
     if (f >= p.F) break;
     const int64_t o = ((int64_t)f * p.nz + iz) * p.nx + ix;
-    if (OUT == TIDAS_OUT_ENVELOPE) reinterpret_cast<R*>(out_)[o] = acc_env[b];
-    else if (OUT == TIDAS_OUT_COHERENT) reinterpret_cast<R*>(out_)[o] = cabs_(acc_iq[b]);
-    else reinterpret_cast<C*>(out_)[o] = acc_iq[b];
+    // streaming stores: the image is written once and not read back here, so it
+    // should not displace the analytic rows in L2
+    if (OUT == TIDAS_OUT_ENVELOPE) __stcs(reinterpret_cast<R*>(out_) + o, acc_env[b]);
+    else if (OUT == TIDAS_OUT_COHERENT) __stcs(reinterpret_cast<R*>(out_) + o, cabs_(acc_iq[b]));
+    else __stcs(reinterpret_cast<C*>(out_) + o, acc_iq[b]);
   }
 #ifndef TIDAS_DAS_NO_PEERS
   // the same values into every peer destination (one rolled loop: the common

@@ -53,10 +53,27 @@ def needs_relaunch(requested: int) -> bool:
     return requested > 1 and "WORLD_SIZE" not in os.environ
 
 
+def rehearsal() -> bool:
+    """TIDAS_DIST_REHEARSAL=1: a single process still creates the process group
+    and issues every collective of the multi-rank step (NCCL all-gathers of one
+    rank, the symmetric-memory barriers) — a one-GPU dry run of the code the
+    ranks of a node execute. Timings from it say nothing about NVLink."""
+    return os.environ.get("TIDAS_DIST_REHEARSAL", "") not in ("", "0")
+
+
+def collectives_on(group=None) -> bool:
+    """True when gathers must go through the process group (more than one rank, or a rehearsal)."""
+    return dist.is_initialized() and (dist.get_world_size(group) > 1 or rehearsal())
+
+
 def init(backend: Optional[str] = None) -> Tuple[int, int]:
     """Initialise the process group when launched by torchrun; returns (rank, world)."""
     rank, world, local = env_rank_world()
-    if world > 1 and not dist.is_initialized():
+    if world == 1 and rehearsal():
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", str(free_port())), ("RANK", "0"),
+                     ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0")):
+            os.environ.setdefault(k, v)
+    if (world > 1 or rehearsal()) and not dist.is_initialized():
         backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
@@ -72,7 +89,7 @@ def gather_images(local: torch.Tensor, n_units: int, out: Optional[torch.Tensor]
     the result; shards that differ by one unit are padded to the largest shard,
     gathered and trimmed."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    if world == 1:
+    if not collectives_on(group):
         return local if out is None else out.copy_(local)
     tail = tuple(local.shape[1:])
     cap = shard_range(n_units, 0, world)[1]
@@ -121,7 +138,7 @@ def pipelined_gather(compute, n_local: int, out: torch.Tensor, sub: int, group=N
     for c0 in range(0, n_local, sub):
         c1 = min(n_local, c0 + sub)
         part = compute(c0, c1)
-        if world == 1:
+        if not collectives_on(group):
             if part.data_ptr() != out[c0:c1].data_ptr():
                 out[c0:c1].copy_(part)
             continue

@@ -44,7 +44,7 @@ def main() -> int:
     oks = [None] * world
     dist.all_gather_object(oks, ok)
     if rank == 0:
-        print(json.dumps({"world": world, "ok": all(oks)}), flush=True)
+        print(json.dumps({"world": world, "ok": all(oks), "collectives": parallel.collectives_on()}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
     return 0

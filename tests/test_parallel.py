@@ -133,8 +133,23 @@ def test_relaunch_spawns_ranks_like_bench():
     r = subprocess.run([sys.executable, str(script), "2"], capture_output=True, text=True, timeout=240, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
-    assert lines == [{"world": 2, "ok": True}]
+    assert lines == [{"world": 2, "ok": True, "collectives": True}]
 
+
+def test_rehearsal_one_rank_issues_the_collectives():
+    """TIDAS_DIST_REHEARSAL=1: one process creates the group and runs the same
+    gathers through it (what the one-GPU dry run of the multi-rank bench does)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    script = Path(__file__).resolve().parent / "spawn_worker.py"
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    env["TIDAS_DIST_REHEARSAL"] = "1"
+    r = subprocess.run([sys.executable, str(script), "1"], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert lines == [{"world": 1, "ok": True, "collectives": True}]
 
 
 def test_peer_destinations_skip_self_and_offset():

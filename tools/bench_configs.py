@@ -90,7 +90,7 @@ def run_configs(names, steps=10, warmup=3, echo=False, rank=0, world=1, timed=No
                                   x=x, z=z, angles=c["angles"], f_number=1.5, out=c["out"])
         ws = imaging.DasWorkspace(plan)
         img = torch.empty((rf.shape[0], c["nz"], c["nx"]), device="cuda")
-        gather = world > 1 and c.get("gather", False)
+        gather = (world > 1 or parallel.rehearsal()) and c.get("gather", False)
         full = torch.empty((total, c["nz"], c["nx"]), device="cuda") if gather else None
         n_local = int(rf.shape[0])
         # sub-chunks of whole 8-frame groups (K2's frames per thread); with two or

@@ -1,7 +1,7 @@
 """cfg2 DAS (K1 + K2) over 256 frames at different chunk sizes (frames per
 K1 / K2 launch): small chunks keep the analytic intermediate L2-resident
 (less DRAM traffic), large chunks shorten the kernels' last-wave tails.
-python tools/das_chunk_sweep.py [--sustain] [chunk ...]
+python tools/das_chunk_sweep.py [--sustain] [--lib=variant.so] [chunk ...]
 --sustain: 1.5 s of load before a 1 s timed window (the bench's power-capped
 steady state) and the median SM clock over the window (NVML)."""
 import json
@@ -11,6 +11,11 @@ from pathlib import Path
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2507_15464_b200 import _lib  # noqa: E402
+
+_libs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--lib=")]
+if _libs:  # a variant library (tools/build_variant.sh)
+    _lib.load(Path(_libs[0]))
 import bench  # noqa: E402
 import paper_2507_15464_b200 as tb  # noqa: E402
 from paper_2507_15464_b200 import imaging  # noqa: E402
@@ -23,7 +28,7 @@ rf = tb.synthesize_batch(sx, sz, a, angles=[0.0], dtype=torch.float32,
                          **{k: cfg[k] for k in ("n_el", "pitch", "fs", "c", "f0", "fbw", "n_samples")})
 img = torch.empty((F, cfg["nz"], cfg["nx"]), device="cuda")
 sustain = "--sustain" in sys.argv
-chunks = [int(c) for c in sys.argv[1:] if c != "--sustain"] or [8, 16, 24, 32, 64, 128, 256]
+chunks = [int(c) for c in sys.argv[1:] if not c.startswith("--")] or [8, 16, 24, 32, 64, 128, 256]
 
 
 def sm_clock_sampler():

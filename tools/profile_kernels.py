@@ -42,7 +42,7 @@ pk = dict(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"], f0=cfg
           f_number=cfg["f_number"], n_samples=cfg["n_samples"])
 torch.cuda.synchronize()
 for _ in range(args.iters):
-    tb.rf_analytic(rf, "f32", out=an)
+    tb.rf_analytic(rf, "f32", out=an, sample_range=plan.sample_range())  # as das_image calls it
     tb.das_from_analytic(an, plan, out=img)
     tb.tidas_rowconv(maps, K, out=y)
     tb.build_row_kernels(z4, 129, dx4, neighbourhood=8, **pk)  # K5 at cfg4

@@ -31,5 +31,11 @@ out_d = {"das_pipeline_bytes_per_frame": res["K1"] + res["K2"], "K1_bytes_per_fr
 if "RC" in res:
     out_d.update(rowconv_cfg4_bytes_per_launch=res["RC"], rowconv_cfg4_algorithmic_bytes_per_launch=256 * 2048 * 1024 * 8,
                  rowconv_source=f"{rep}: rowconv_tc1_kernel<fwd>, 256 cfg4 maps")
+try:  # keep the L2-sized-chunk record (tools/chunk_dram_summary.py) across refreshes
+    old = json.load(open(out))
+    if "l2_chunk" in old:
+        out_d["l2_chunk"] = old["l2_chunk"]
+except (OSError, ValueError):
+    pass
 open(out, "w").write(json.dumps(out_d, indent=1) + "\n")
 print(out_d)
