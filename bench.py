@@ -290,8 +290,11 @@ def nccl_summary():
     if not path:
         return None
     p = Path(path.replace("%h", platform.node()).replace("%p", str(os.getpid())))
-    if not p.exists():
-        return {"log": str(p), "found": False}
+    if not p.exists():  # NCCL expands %h itself: look for this process's file under any host name
+        hits = sorted(p.parent.glob(Path(path).name.replace("%h", "*").replace("%p", str(os.getpid()))))
+        if not hits:
+            return {"log": str(p), "found": False, "NCCL_DEBUG": os.environ.get("NCCL_DEBUG")}
+        p = hits[0]
     text = p.read_text(errors="replace")
     return {"log": str(p), "found": True, "nvls": "NVLS" in text and "NVLS multicast support is not available" not in text,
             "p2p": "via P2P" in text, "lines": text.count("\n")}

@@ -77,7 +77,10 @@ def init(backend: Optional[str] = None) -> Tuple[int, int]:
         backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
-        dist.init_process_group(backend=backend)
+            # device_id: the communicator is bound to this rank's GPU and created eagerly
+            dist.init_process_group(backend=backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend=backend)
     return rank, world
 
 
