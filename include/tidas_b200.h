@@ -83,6 +83,21 @@ int tidas_rf_analytic_range(const void* rf, int rf_dtype, int64_t rf_row_stride,
                             int32_t lo, int32_t hi, int32_t* support, void* stream);
 
 /*
+ * tidas_rf_analytic_range with flags (ABI 6).
+ * TIDAS_K1_RF_READY: the caller vouches that the kernel launched just before
+ * this call on `stream` does not write `rf` (e.g. the DAS of the previous
+ * chunk, which only reads `out` and writes images). The FP32 register kernels
+ * (n_samples = 2048 / 4096 / 8192) then load the rows and run both transforms
+ * during that kernel's last wave (programmatic dependent launch) and wait for
+ * it only before storing to `out`; other kernels ignore the flag. Without it
+ * every global access waits for the preceding kernel.
+ */
+enum tidas_k1_flags { TIDAS_K1_RF_READY = 1 };
+int tidas_rf_analytic_ex(const void* rf, int rf_dtype, int64_t rf_row_stride, double scale,
+                         void* out, int out_prec, int64_t n_rows, int32_t n_samples,
+                         int32_t lo, int32_t hi, int32_t* support, int32_t flags, void* stream);
+
+/*
  * Spectral fractional delay (das.py:108-111, method="spectral"): complex
  * IFFT(FFT(x) * exp(-2 pi i f shift / fs)) per row, f on numpy's fftfreq grid;
  * the caller keeps the real part. x: [n_rows][n_samples] double, out: double2.

@@ -20,6 +20,7 @@ PREC_F32, PREC_F64 = 0, 1
 AP_REF_BOXCAR, AP_HANN = 0, 1
 OUT_ENVELOPE, OUT_COHERENT, OUT_IQ = 0, 1, 2
 GEO_FAST, GEO_REFINED = 0, 1
+K1_RF_READY = 1  # tidas_k1_flags
 ROWCONV_PATHS = {"auto": 0, "tensor": 1, "simt": 2}
 
 DTYPE_CODE = {torch.float64: F64, torch.float32: F32, torch.int16: I16}
@@ -42,6 +43,7 @@ SIGNATURES = {
     "tidas_init": ([C.c_int], C.c_int),
     "tidas_rf_analytic": ([_P, C.c_int, _I64, _D, _P, C.c_int, _I64, _I32, _P, _P], C.c_int),
     "tidas_rf_analytic_range": ([_P, C.c_int, _I64, _D, _P, C.c_int, _I64, _I32, _I32, _I32, _P, _P], C.c_int),
+    "tidas_rf_analytic_ex": ([_P, C.c_int, _I64, _D, _P, C.c_int, _I64, _I32, _I32, _I32, _P, _I32, _P], C.c_int),
     "tidas_spectral_shift_f64": ([_P, _I64, _I32, _D, _P, _P], C.c_int),
     "tidas_plane_wave_arrivals": ([_P, _I32, _P, _I32, _P, _I32, _I32, _D, _D, _P, _P], C.c_int),
     "tidas_das_image": ([C.POINTER(DasDesc), _P, _P, _P, _P, _P, _P, _P], C.c_int),

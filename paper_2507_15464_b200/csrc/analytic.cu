@@ -349,7 +349,7 @@ template <bool INV> __device__ __forceinline__ void dft64_pair_dif(float2 (&w)[3
 template <typename In, bool SCALED, bool SUPPORT, bool BULK>
 __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                            cplx<float>* __restrict__ out, int64_t n_rows,
-                                                           int32_t* __restrict__ support, int s_lo, int s_hi) {
+                                                           int32_t* __restrict__ support, int s_lo, int s_hi, int early) {
   constexpr int N = 4096, LP = 65;
   constexpr int SH = TW_LOG - 12;
   __shared__ float2 S[64 * LP];
@@ -374,8 +374,11 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
     asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&rows_bar)));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  // `early` (TIDAS_K1_RF_READY): the caller vouches that the kernel just ahead
+  // in the stream does not write the RF, so the loads and both transforms run
+  // during that kernel's last wave and only the stores wait for it
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (!early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const In* row_a = src_a;
   const In* row_b = src_b;
   if constexpr (BULK) {
@@ -498,6 +501,7 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   }
   dft64_pair_dif<true>(w, v, h);  // slot j: x[t + 64 (2 sig32(j) + h)]
   cplx<float>* dst_a = out + ra * (int64_t)N;
+  if (early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the output rows may still be read
   store_analytic_pair<In, SCALED>(row_a, row_b, has_b, scale, v, dst_a, dst_a + N,
                                   [&](int j) { return t + 64 * (2 * sig32(j) + hi); }, s_lo, s_hi);
   if (SUPPORT) {
@@ -616,7 +620,7 @@ template <bool INV> __device__ __forceinline__ void dft128_quad_dif(float2 (&y)[
 template <typename In, bool SCALED, bool SUPPORT>
 __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                                 cplx<float>* __restrict__ out, int64_t n_rows,
-                                                                int32_t* __restrict__ support, int s_lo, int s_hi) {
+                                                                int32_t* __restrict__ support, int s_lo, int s_hi, int early) {
   constexpr int N = 8192;
   constexpr int LP1 = 65, LP2 = 129;  // [128][65] and [64][129] transposes: conflict-free columns
   constexpr int SH = TW_LOG - 13;
@@ -639,8 +643,11 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
   // start its prologue during this kernel's last wave; wait for the previous
   // kernel (which may have written the input or still read the output rows)
   // before touching global data
+  // `early` (TIDAS_K1_RF_READY): the caller vouches that the kernel just ahead
+  // in the stream does not write the RF, so the loads and both transforms run
+  // during that kernel's last wave and only the stores wait for it
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (!early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   float2 v[32], y[32];
   const int mq = q0i + 2 * q1i;
   // W8192^n1, W8192^(8 n1) (forward, quad roles); W8192^k2, W8192^(8 k2) (inverse, pair roles)
@@ -745,6 +752,7 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
     }
   dft128_quad_dif<true>(y, v, q0, q1);  // slot j: x[n1 + 64 (q0 + 2 q1 + 4 sig32(j))]
   cplx<float>* dst_a = out + ra * (int64_t)N;
+  if (early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the output rows may still be read
   store_analytic_pair<In, SCALED>(src_a, src_b, has_b, scale, v, dst_a, dst_a + N,
                                   [&](int j) { return n1 + 64 * (mq + 4 * sig32(j)); }, s_lo, s_hi);
   if (SUPPORT) {
@@ -770,7 +778,7 @@ __global__ void __launch_bounds__(256, 2) analytic_r8192_kernel(const In* __rest
 template <typename In, bool SCALED, bool SUPPORT>
 __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                             cplx<float>* __restrict__ out, int64_t n_rows,
-                                                            int32_t* __restrict__ support, int s_lo, int s_hi) {
+                                                            int32_t* __restrict__ support, int s_lo, int s_hi, int early) {
   constexpr int N = 2048, LP1 = 33, LP2 = 65;  // [64][33] and [32][65] transposes
   constexpr int SH = TW_LOG - 11;
   __shared__ float2 S[64 * LP1 > 32 * LP2 ? 64 * LP1 : 32 * LP2];
@@ -789,8 +797,11 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   // start its prologue during this kernel's last wave; wait for the previous
   // kernel (which may have written the input or still read the output rows)
   // before touching global data
+  // `early` (TIDAS_K1_RF_READY): the caller vouches that the kernel just ahead
+  // in the stream does not write the RF, so the loads and both transforms run
+  // during that kernel's last wave and only the stores wait for it
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (!early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   float2 v[32], w[32];
   // W2048^n1, W2048^(8 n1) (forward, pair roles); W2048^k2, W2048^(8 k2) (inverse, row roles)
   const float2 T1 = g_tw32[n1 << SH], T8 = g_tw32[((8 * n1) & 2047) << SH];
@@ -885,6 +896,7 @@ __global__ void __launch_bounds__(64) analytic_r2048_kernel(const In* __restrict
   }
   dft64_pair_dif<true>(w, v, h);  // slot j: x[n1 + 32 (2 sig32(j) + h)]
   cplx<float>* dst_a = out + ra * (int64_t)N;
+  if (early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the output rows may still be read
   store_analytic_pair<In, SCALED>(src_a, src_b, has_b, scale, v, dst_a, dst_a + N,
                                   [&](int j) { return n1 + 32 * (2 * sig32(j) + hi); }, s_lo, s_hi);
   if (SUPPORT) {
@@ -1080,7 +1092,7 @@ static K pick4(K plain, K support_only, K scaled_only, K both, double scale, con
 template <typename R, typename In>
 static int launch_analytic(const In* rf, int64_t stride, double scale, void* out, int64_t n_rows,
                            int32_t N, int32_t* support, double shift, cudaStream_t st, int lo = 0,
-                           int hi = INT_MAX) {
+                           int hi = INT_MAX, int early = 0) {
   // the register four-step kernels store only samples lo .. hi; the others store every sample
   lo = lo < 0 ? 0 : lo;
   hi = hi > N - 1 ? N - 1 : hi;
@@ -1108,7 +1120,7 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         auto k2 = pick4(analytic_r2048_kernel<In, false, false>, analytic_r2048_kernel<In, false, true>,
                         analytic_r2048_kernel<In, true, false>, analytic_r2048_kernel<In, true, true>, scale, support);
         TIDAS_CUDA_CHECK(launch_pdl(k2, dim3((unsigned)((n_rows + 1) / 2)), dim3(64), 0, st,
-                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi));
+                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi, early));
         return TIDAS_OK;
       }
       if (!delay && logN == 13) {
@@ -1117,7 +1129,7 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         const size_t smem8 = sizeof(float2) * 128 * 65;
         TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8));
         TIDAS_CUDA_CHECK(launch_pdl(kr, dim3((unsigned)((n_rows + 1) / 2)), dim3(256), smem8, st, rf, stride,
-                                    (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi));
+                                    (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi, early));
         return TIDAS_OK;
       }
       if (!delay && logN == 12) {
@@ -1133,7 +1145,7 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         const size_t dyn = bulk ? 2 * 4096 * sizeof(In) : 0;
         if (bulk) TIDAS_CUDA_CHECK(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         TIDAS_CUDA_CHECK(launch_pdl(k4, dim3((unsigned)((n_rows + 1) / 2)), dim3(128), dyn, st,
-                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi));
+                                    rf, stride, (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, support, lo, hi, early));
         return TIDAS_OK;
       }
     }
@@ -1168,17 +1180,17 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
 template <typename R>
 static int dispatch_analytic(const void* rf, int dtype, int64_t stride, double scale, void* out,
                              int64_t n_rows, int32_t N, int32_t* support, double shift,
-                             cudaStream_t st, int lo = 0, int hi = INT_MAX) {
+                             cudaStream_t st, int lo = 0, int hi = INT_MAX, int early = 0) {
   switch (dtype) {
     case TIDAS_F64:
       return launch_analytic<R>(static_cast<const double*>(rf), stride, scale, out, n_rows, N, support, shift, st,
-                                lo, hi);
+                                lo, hi, early);
     case TIDAS_F32:
       return launch_analytic<R>(static_cast<const float*>(rf), stride, scale, out, n_rows, N, support, shift, st,
-                                lo, hi);
+                                lo, hi, early);
     case TIDAS_I16:
       return launch_analytic<R>(static_cast<const int16_t*>(rf), stride, scale, out, n_rows, N, support, shift, st,
-                                lo, hi);
+                                lo, hi, early);
   }
   set_error("unknown rf dtype %d", dtype);
   return TIDAS_EINVAL;
@@ -1198,7 +1210,16 @@ extern "C" int tidas_rf_analytic(const void* rf, int rf_dtype, int64_t rf_row_st
 extern "C" int tidas_rf_analytic_range(const void* rf, int rf_dtype, int64_t rf_row_stride, double scale,
                                        void* out, int out_prec, int64_t n_rows, int32_t n_samples,
                                        int32_t lo, int32_t hi, int32_t* support, void* stream) {
+  return tidas_rf_analytic_ex(rf, rf_dtype, rf_row_stride, scale, out, out_prec, n_rows, n_samples, lo, hi,
+                              support, 0, stream);
+}
+
+extern "C" int tidas_rf_analytic_ex(const void* rf, int rf_dtype, int64_t rf_row_stride, double scale,
+                                    void* out, int out_prec, int64_t n_rows, int32_t n_samples,
+                                    int32_t lo, int32_t hi, int32_t* support, int32_t flags, void* stream) {
   using namespace tidas;
+  TIDAS_REQUIRE((flags & ~TIDAS_K1_RF_READY) == 0, "unknown flags 0x%x", flags);
+  const int early = (flags & TIDAS_K1_RF_READY) != 0;
   TIDAS_REQUIRE(lo <= hi, "empty sample range [%d, %d]", lo, hi);
   TIDAS_REQUIRE(n_rows >= 0 && n_rows < (int64_t(1) << 31), "n_rows out of range");
   if (n_rows == 0) return TIDAS_OK;  // empty batch (null data pointers allowed)
@@ -1209,7 +1230,7 @@ extern "C" int tidas_rf_analytic_range(const void* rf, int rf_dtype, int64_t rf_
   const double hilbert = nan("");
   if (out_prec == TIDAS_PREC_F32)
     return dispatch_analytic<float>(rf, rf_dtype, rf_row_stride, scale, out, n_rows, n_samples, support, hilbert,
-                                    as_stream(stream), lo, hi);
+                                    as_stream(stream), lo, hi, early);
   if (out_prec == TIDAS_PREC_F64)
     return dispatch_analytic<double>(rf, rf_dtype, rf_row_stride, scale, out, n_rows, n_samples, support, hilbert,
                                      as_stream(stream), lo, hi);

@@ -19,5 +19,5 @@ void set_error(const char* fmt, ...) {
 
 extern "C" const char* tidas_last_error(void) { return tidas::g_err; }
 
-extern "C" int tidas_abi_version(void) { return 5; }  // 2: tidas_das_desc_t.window, tidas_das_window; 3: .geometry; 4: tidas_das_image_peers;
-// 5: tidas_rf_analytic_range, tidas_das_window_range
+extern "C" int tidas_abi_version(void) { return 6; }  // 2: tidas_das_desc_t.window, tidas_das_window; 3: .geometry; 4: tidas_das_image_peers;
+// 5: tidas_rf_analytic_range, tidas_das_window_range; 6: tidas_rf_analytic_ex (TIDAS_K1_RF_READY)

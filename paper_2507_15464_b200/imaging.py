@@ -187,7 +187,7 @@ def table_plan(*, n_el: int, pitch: float, fs: float, c: float, n_samples: int, 
 
 def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=None,
                 support: Optional[torch.Tensor] = None, stream=None,
-                sample_range: Optional[Tuple[int, int]] = None) -> torch.Tensor:
+                sample_range: Optional[Tuple[int, int]] = None, rf_ready: bool = False) -> torch.Tensor:
     """K1: periodic analytic signal of every row of rf [..., N] (f64/f32/int16).
 
     Returns complex64 (prec "f32") or complex128 (prec "f64") of the same shape.
@@ -195,13 +195,17 @@ def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=Non
     ``sample_range`` (lo, hi): store only output samples lo .. hi of each row
     (tidas_rf_analytic_range; the rest of ``out`` is left as it was) — what
     ``das_image`` passes from its plan (``DasPlan.sample_range``).
+    ``rf_ready`` (TIDAS_K1_RF_READY): the caller vouches that the kernel just
+    ahead on the stream does not write ``rf``; K1 then loads and transforms
+    during that kernel's last wave and waits for it only before its stores.
     """
     L = _lib.lib()
     if not rf.is_cuda:
         raise ValueError("rf must be a CUDA tensor")
     if rf.dtype not in _lib.DTYPE_CODE:
         raise ValueError(f"unsupported rf dtype {rf.dtype}")
-    rf = rf.contiguous()
+    if not rf.is_contiguous():
+        rf, rf_ready = rf.contiguous(), False  # the copy kernel just ahead writes K1's input
     n = int(rf.shape[-1])
     rows = rf.numel() // n if n else 0
     if prec not in ("f32", "f64"):
@@ -217,17 +221,17 @@ def rf_analytic(rf: torch.Tensor, prec: str = "f32", scale: float = 1.0, out=Non
     if support is not None and (support.dtype != torch.int32 or support.numel() != 2 * rows
                                 or not support.is_contiguous() or support.device != rf.device):
         raise ValueError(f"support must be a contiguous int32 tensor of {rows} x 2 on {rf.device}")
-    if sample_range is None:
+    if sample_range is None and not rf_ready:
         _lib.check(L.tidas_rf_analytic(_lib.ptr(rf), _lib.DTYPE_CODE[rf.dtype], n, float(scale),
                                        _lib.ptr(out), pc, rows, n, _lib.ptr(support),
                                        _lib.stream_handle(stream)))
         return out
-    lo, hi = (int(v) for v in sample_range)
+    lo, hi = (int(v) for v in sample_range) if sample_range is not None else (0, max(n - 1, 0))
     if lo > hi:
         raise ValueError(f"empty sample range {sample_range}")
-    _lib.check(L.tidas_rf_analytic_range(_lib.ptr(rf), _lib.DTYPE_CODE[rf.dtype], n, float(scale),
-                                         _lib.ptr(out), pc, rows, n, lo, hi, _lib.ptr(support),
-                                         _lib.stream_handle(stream)))
+    _lib.check(L.tidas_rf_analytic_ex(_lib.ptr(rf), _lib.DTYPE_CODE[rf.dtype], n, float(scale),
+                                      _lib.ptr(out), pc, rows, n, lo, hi, _lib.ptr(support),
+                                      _lib.K1_RF_READY if rf_ready else 0, _lib.stream_handle(stream)))
     return out
 
 
@@ -332,7 +336,10 @@ def das_image(rf: torch.Tensor, plan: DasPlan, *, scale: float = 1.0, out=None,
     for f0 in range(0, F, ws.chunk):
         f1 = min(F, f0 + ws.chunk)
         an = ws.buf[: f1 - f0]
-        rf_analytic(rf[f0:f1], plan.prec, scale=scale, out=an, stream=stream, sample_range=plan.sample_range())
+        # from the second chunk on, the kernel ahead on the stream is this loop's own K2:
+        # it reads `an` and writes images, never the RF
+        rf_analytic(rf[f0:f1], plan.prec, scale=scale, out=an, stream=stream, sample_range=plan.sample_range(),
+                    rf_ready=f0 > 0)
         das_from_analytic(an, plan, out=out[f0:f1], stream=stream,
                           peers=[q + f0 * out[0].numel() * out.element_size() for q in peers] if peers else None)
     return out

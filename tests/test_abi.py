@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_text_without_gpu():
     lib = _lib.load()
-    assert lib.tidas_abi_version() == 5
+    assert lib.tidas_abi_version() == 6
     # argument validation happens before any CUDA call
     rc = lib.tidas_rowconv_fwd_f32(None, None, None, 1, 1, 4, 3, None)
     assert rc == _lib.EINVAL

@@ -98,3 +98,46 @@ def test_das_image_never_reads_outside_the_stored_range(case):
         assert (lo, hi) == (0, cfg["n_samples"] - 1)
     else:
         assert hi - lo + 1 < cfg["n_samples"]
+
+
+# ------------------------------------------------ TIDAS_K1_RF_READY (ABI 6)
+@pytest.mark.parametrize("N,dtype,rows", [(2048, torch.float64, 7), (4096, torch.float32, 2048),
+                                          (4096, torch.int16, 9), (8192, torch.int16, 1024), (1000, torch.float32, 3)])
+def test_rf_ready_flag_same_values_behind_a_busy_kernel(N, dtype, rows):
+    """K1 with rf_ready behind a long kernel that is still READING K1's output
+    buffer (the situation in das_image's chunk loop): the early loads and
+    transforms must not disturb that kernel, and the stores must come out
+    bitwise equal to the unflagged call."""
+    g = torch.Generator(device=DEV).manual_seed(N + rows)
+    rf = torch.randn((rows, N), device=DEV, generator=g) * 300
+    rf = rf.to(dtype) if dtype != torch.int16 else rf.round().to(torch.int16)
+    plain = tb.rf_analytic(rf, "f32")
+    prev = torch.view_as_complex(torch.randn((rows, N, 2), device=DEV, generator=g)).contiguous()
+    out = prev.clone()
+    acc = torch.zeros((), device=DEV, dtype=torch.float64)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        # a reader of `out` just ahead on the stream, then K1 storing into `out`
+        acc += torch.view_as_real(out).double().sum()
+        tb.rf_analytic(rf, "f32", out=out, sample_range=(0, N - 1), rf_ready=True)
+        assert torch.equal(out, plain)
+        out.copy_(prev)
+    # the reader saw `prev` every time (the stores waited for it)
+    assert float(acc) == pytest.approx(3 * float(torch.view_as_real(prev).double().sum()), rel=1e-12)
+
+
+def test_das_image_multi_chunk_equals_single_chunk_bitwise():
+    """das_image over several chunks (K1 of chunk c + 1 flagged rf_ready behind
+    K2 of chunk c) against one chunk holding every frame."""
+    cfg = CFG2
+    nz, nx, F = 96, 64, 40
+    plan = _plan(cfg, nz, nx)
+    g = torch.Generator(device=DEV).manual_seed(5)
+    rf = torch.randn((F, 1, cfg["n_el"], cfg["n_samples"]), device=DEV, generator=g)
+    one = tb.das_image(rf, plan)
+    small = _plan(cfg, nz, nx)
+    small.chunk_bytes = 8 * cfg["n_el"] * cfg["n_samples"] * 8
+    ws = imaging.DasWorkspace(small)
+    assert ws.chunk == 8
+    for _ in range(3):
+        assert torch.equal(tb.das_image(rf, small, workspace=ws), one)

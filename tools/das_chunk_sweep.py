@@ -45,6 +45,7 @@ def sm_clock_sampler():
     th = threading.Thread(target=run, daemon=True)
     th.start()
     return samples, stop, th
+ref_img = None
 for ch in chunks:
     plan = tb.plane_wave_plan(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"],
                               n_samples=cfg["n_samples"], x=x, z=z, f_number=cfg["f_number"])
@@ -54,6 +55,9 @@ for ch in chunks:
     for _ in range(3):
         tb.das_image(rf, plan, out=img, workspace=ws)
     torch.cuda.synchronize()
+    if ref_img is None:
+        ref_img = img.clone()
+    same = bool(torch.equal(img, ref_img))  # images are bitwise independent of the chunk size
     n_it, clk = 10, None
     if sustain:
         import statistics
@@ -75,5 +79,6 @@ for ch in chunks:
         th.join()
         clk = statistics.median(samples) if samples else None
     us = e0.elapsed_time(e1) / n_it / F * 1e3
-    print(json.dumps({"chunk_frames": ch, "us_per_frame": us, "frames_per_s": 1e6 / us, "sm_mhz": clk}), flush=True)
+    print(json.dumps({"chunk_frames": ch, "us_per_frame": us, "frames_per_s": 1e6 / us, "sm_mhz": clk,
+                      "bitwise_equal_to_first": same}), flush=True)
     del ws
