@@ -115,6 +115,26 @@ def gather_images(local: torch.Tensor, n_units: int, out: Optional[torch.Tensor]
     return res if out is None else out.copy_(res)
 
 
+def compound_angle_shards(iq_local: torch.Tensor, group=None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Angle sharding (north star (e)): every rank images ITS steering angles
+    of the same frames with an ``out="iq"`` plan (the complex sum over its
+    transmits, ``das_image(rf[:, a0:a1], plan_over(angles[a0:a1]))`` with
+    ``a0, a1 = shard_range(n_angles, rank, world)``); the coherently compounded
+    image is the magnitude of the sum over ranks. One all-reduce (SUM) of the
+    IQ images — float pairs through ``view_as_real`` — then ``abs``. Equal to
+    the one-plan ``out="coherent"`` image up to the order of the FP32 adds.
+
+    ``iq_local`` [F][nz][nx] complex; returns the real image [F][nz][nx] on
+    every rank (in ``out`` when given). One rank: just the magnitude."""
+    if not iq_local.is_complex():
+        raise ValueError("iq_local must be a complex IQ image (plan out='iq')")
+    total = iq_local
+    if collectives_on(group):
+        total = iq_local.clone() if iq_local.is_contiguous() else iq_local.contiguous()
+        dist.all_reduce(torch.view_as_real(total), op=dist.ReduceOp.SUM, group=group)
+    return torch.abs(total, out=out) if out is not None else torch.abs(total)
+
+
 def pipelined_gather(compute, n_local: int, out: torch.Tensor, sub: int, group=None,
                      layout: str = "rank_major") -> torch.Tensor:
     """Compute the local units in sub-chunks and all-gather each one as soon as

@@ -157,3 +157,48 @@ def test_peer_destinations_skip_self_and_offset():
     ptrs = [1000, 5000, 9000, 13000]
     assert peer_destinations(ptrs, 1, 3, 16) == [1048, 9048, 13048]
     assert peer_destinations(ptrs[:1], 0, 0, 16) == []
+
+
+def _angle_worker(rank, world, port, n_angles, q):
+    from paper_2507_15464_b200.parallel import compound_angle_shards, shard_range
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.Generator().manual_seed(11)
+    per_angle = torch.view_as_complex(torch.randn((n_angles, 2, 5, 4, 2), generator=g, dtype=torch.float64))
+    a0, a1 = shard_range(n_angles, rank, world)
+    iq_local = per_angle[a0:a1].sum(0)               # what an out="iq" plan over this rank's angles returns
+    img = compound_angle_shards(iq_local)
+    out = torch.empty((2, 5, 4), dtype=torch.float64)
+    compound_angle_shards(iq_local, out=out)
+    assert torch.equal(img, out)
+    q.put((rank, img.numpy().tolist(), per_angle.sum(0).abs().numpy().tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_angles", [11, 4])  # cfg3's 11 angles: shards of 6 + 5
+def test_angle_sharded_compounding_two_ranks(n_angles):
+    """Each rank sums its own steering angles' IQ; the all-reduced magnitude is
+    the coherently compounded image of all angles on every rank."""
+    import numpy as np
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_angle_worker, args=(r, 2, port, n_angles, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, img, want in res:
+        np.testing.assert_allclose(np.array(img), np.array(want), rtol=1e-13, atol=0)
+    assert res[0][1] == res[1][1]                    # identical on both ranks
+
+
+def test_compound_angle_shards_one_process_is_the_magnitude():
+    from paper_2507_15464_b200.parallel import compound_angle_shards
+    iq = torch.view_as_complex(torch.randn((3, 4, 5, 2)))
+    assert torch.equal(compound_angle_shards(iq), iq.abs())
+    with pytest.raises(ValueError):
+        compound_angle_shards(iq.real)
