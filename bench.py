@@ -277,9 +277,13 @@ def run_reference(args):
 
 
 def nccl_env():
-    """Keep NCCL's communicator log (read at communicator creation)."""
+    """Keep NCCL's communicator log (read at communicator creation). An
+    NCCL_DEBUG already in the environment (the launcher's own choice of level
+    and destination) is left exactly as it is."""
+    if "NCCL_DEBUG" in os.environ:
+        return
     log_dir = ROOT / "gpurun_out" if (ROOT / "gpurun_out").is_dir() else Path(tempfile.gettempdir())
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ["NCCL_DEBUG"] = "INFO"
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH,NVLS")
     os.environ.setdefault("NCCL_DEBUG_FILE", str(log_dir / "nccl_bench.%h.%p.log"))
 
@@ -287,8 +291,8 @@ def nccl_env():
 def nccl_summary():
     """Transport facts from this process's NCCL log (P2P / NVLink / NVLS)."""
     path = os.environ.get("NCCL_DEBUG_FILE", "")
-    if not path:
-        return None
+    if not path:  # the environment's own NCCL_DEBUG setting: its output goes to stderr
+        return {"log": None, "NCCL_DEBUG": os.environ.get("NCCL_DEBUG")}
     p = Path(path.replace("%h", platform.node()).replace("%p", str(os.getpid())))
     if not p.exists():  # NCCL expands %h itself: look for this process's file under any host name
         hits = sorted(p.parent.glob(Path(path).name.replace("%h", "*").replace("%p", str(os.getpid()))))
