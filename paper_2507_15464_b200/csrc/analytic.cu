@@ -516,6 +516,155 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
   }
 }
 
+// ------------------------ N = 4096 as 16 x 16 x 16, 256 threads: 16 values per thread
+//
+// n = n0 + 16 n1 + 256 n2, k = k0 + 16 k1 + 256 k2:
+//   A[n0, n1, k0] = DFT16_n2(x) W256^(n1 k0)
+//   B[n0, k1, k0] = DFT16_n1(A) W4096^(n0 (k0 + 16 k1))
+//   X[k0 + 16 k1 + 256 k2] = DFT16_n0(B)
+// Thread t = 16 n1 + n0 owns x[t + 256 n2]; after the three passes thread
+// t = 16 k1 + k0 owns X[t + 256 k2]. The inverse is the SAME routine with
+// conjugate twiddles applied to that layout (k2 plays n2), and it ends with
+// thread t owning x[t + 256 n2] again — no shuffles, no lane selects, no bit
+// reversal; two shared-memory transposes per transform ([256][17] float2,
+// conflict-free both ways). A third of analytic_r32_kernel's instructions is
+// lane-pair plumbing and its 59 KB body overflows the 32 KB instruction cache
+// (no_instructions 22% of its stall samples); this kernel issues ~35% fewer
+// warp instructions per channel pair from a body that fits, at 24 instead of
+// 16 warps per SM. Rows arrive by bulk copies (16-byte aligned f32 / int16).
+constexpr int T16_LP = 17;
+constexpr int T16_ELEMS = 256 * T16_LP;
+
+// v[slot(r)] *= base * w^r, r = 0..15 (r = 0: base only when BASE); dft16 leaves
+// X[r] in slot dft16_slot(r). Powers by products of depth <= 3 past w / base.
+template <bool BASE> __device__ __forceinline__ void t16_twiddle(float2 base, float2 w, float2 (&v)[16]) {
+  const float2 w2 = cmul(w, w), w3 = cmul(w2, w), w4 = cmul(w2, w2), w8 = cmul(w4, w4);
+  float2 b0 = base, b4 = BASE ? cmul(base, w4) : w4, b8 = BASE ? cmul(base, w8) : w8;
+  const float2 b12 = cmul(b8, w4);
+  if (BASE) v[dft16_slot(0)] = cmul(v[dft16_slot(0)], b0);
+  v[dft16_slot(1)] = cmul(v[dft16_slot(1)], BASE ? cmul(b0, w) : w);
+  v[dft16_slot(2)] = cmul(v[dft16_slot(2)], BASE ? cmul(b0, w2) : w2);
+  v[dft16_slot(3)] = cmul(v[dft16_slot(3)], BASE ? cmul(b0, w3) : w3);
+  v[dft16_slot(4)] = cmul(v[dft16_slot(4)], b4);
+  v[dft16_slot(5)] = cmul(v[dft16_slot(5)], cmul(b4, w));
+  v[dft16_slot(6)] = cmul(v[dft16_slot(6)], cmul(b4, w2));
+  v[dft16_slot(7)] = cmul(v[dft16_slot(7)], cmul(b4, w3));
+  v[dft16_slot(8)] = cmul(v[dft16_slot(8)], b8);
+  v[dft16_slot(9)] = cmul(v[dft16_slot(9)], cmul(b8, w));
+  v[dft16_slot(10)] = cmul(v[dft16_slot(10)], cmul(b8, w2));
+  v[dft16_slot(11)] = cmul(v[dft16_slot(11)], cmul(b8, w3));
+  v[dft16_slot(12)] = cmul(v[dft16_slot(12)], b12);
+  v[dft16_slot(13)] = cmul(v[dft16_slot(13)], cmul(b12, w));
+  v[dft16_slot(14)] = cmul(v[dft16_slot(14)], cmul(b12, w2));
+  v[dft16_slot(15)] = cmul(v[dft16_slot(15)], cmul(b12, w3));
+}
+
+// one 4096-point transform on the thread layout above; T1 = W256^(t >> 4),
+// Ta = W4096^((t & 15) (t >> 4)), Tb = W256^(t & 15) (forward sign; conjugated here for INV)
+template <bool INV>
+__device__ __forceinline__ void t16_fft4096(float2 (&v)[16], float2* S, int t, float2 T1, float2 Ta, float2 Tb) {
+  const int lo = t & 15, hi = t >> 4;
+  if (INV) { T1.y = -T1.y; Ta.y = -Ta.y; Tb.y = -Tb.y; }
+  dft16<INV, float>(v);                    // over n2 -> k0 in slot dft16_slot(k0)
+  t16_twiddle<false>(T1, T1, v);           // W256^(n1 k0)
+  __syncthreads();                         // the previous transform's readers are done with S
+#pragma unroll
+  for (int r = 0; r < 16; ++r) S[(16 * r + lo) * T16_LP + hi] = v[dft16_slot(r)];   // [k0][n0][n1]
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = S[t * T16_LP + r];                            // thread (k0, n0): over n1
+  dft16<INV, float>(v);                    // over n1 -> k1
+  t16_twiddle<true>(Ta, Tb, v);            // W4096^(n0 k0) W256^(n0 k1)
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) S[(16 * r + hi) * T16_LP + lo] = v[dft16_slot(r)];   // [k1][k0][n0]
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = S[t * T16_LP + r];                            // thread (k1, k0): over n0
+  dft16<INV, float>(v);                    // over n0 -> k2 in slot dft16_slot(k2)
+}
+
+template <typename In, bool SCALED>
+__global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restrict__ rf, int64_t stride, float scale,
+                                                            cplx<float>* __restrict__ out, int64_t n_rows,
+                                                            int s_lo, int s_hi, int early) {
+  constexpr int N = 4096;
+  constexpr int SH = TW_LOG - 12;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* S = reinterpret_cast<float2*>(smem_raw);                       // [256][17]
+  In* rows = reinterpret_cast<In*>(smem_raw + sizeof(float2) * T16_ELEMS);  // [2][N]
+  __shared__ __align__(8) uint64_t rows_bar;
+  const int t = threadIdx.x;
+  const int64_t ra = 2 * (int64_t)blockIdx.x;
+  const bool has_b = ra + 1 < n_rows;
+  const In* src_a = rf + ra * stride;
+  const In* src_b = rf + (ra + 1) * stride;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&rows_bar);
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // programmatic dependent launch as in analytic_r32_kernel: `early` moves the
+  // wait for the kernel ahead from here to just before the stores
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (!early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (t == 0) {
+    const unsigned bytes = (unsigned)(N * sizeof(In));
+    uint64_t pol;  // RF rows are read once: evict-first in L2
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(bar), "r"(has_b ? 2 * bytes : bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+        ::"r"((unsigned)__cvta_generic_to_shared(rows)), "l"(src_a), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+    if (has_b)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+          ::"r"((unsigned)__cvta_generic_to_shared(rows + N)), "l"(src_b), "r"(bytes), "r"(bar), "l"(pol)
+          : "memory");
+  }
+  // per-thread table twiddles, loaded while the rows are in flight
+  const int lo = t & 15, hi = t >> 4;
+  const float2 T1 = g_tw32[(16 * hi) << SH], Ta = g_tw32[(lo * hi) << SH], Tb = g_tw32[(16 * lo) << SH];
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], 0, 1000000;\n"
+      " @!p bra W_%=;\n}\n" ::"r"(bar) : "memory");
+  float2 v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int n = t + 256 * r;
+    v[r].x = (float)rows[n];
+    v[r].y = has_b ? (float)rows[N + n] : 0.0f;
+    if (SCALED) { v[r].x *= scale; v[r].y *= scale; }
+  }
+  t16_fft4096<false>(v, S, t, T1, Ta, Tb);  // slot dft16_slot(k2): X[t + 256 k2]
+  // Hilbert multiplier -i sgn(k) / N: k2 < 8 positive, k2 >= 8 negative frequencies; DC and Nyquist zero
+  const float invN = 1.0f / (float)N;
+  float2 w[16];
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) {
+    const float2 x = v[dft16_slot(k2)];
+    w[k2] = k2 < 8 ? make_float2(x.y * invN, -x.x * invN) : make_float2(-x.y * invN, x.x * invN);
+  }
+  if (t == 0) { w[0] = make_float2(0.0f, 0.0f); w[8] = make_float2(0.0f, 0.0f); }
+  t16_fft4096<true>(w, S, t, T1, Ta, Tb);   // slot dft16_slot(n2): H[t + 256 n2] (a in .x, b in .y)
+  if (early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the output rows may still be read
+  cplx<float>* dst_a = out + ra * (int64_t)N;
+  cplx<float>* dst_b = dst_a + N;
+  const unsigned span = (unsigned)(s_hi - s_lo);
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) {
+    const int n = t + 256 * n2;
+    if ((unsigned)(n - s_lo) > span) continue;
+    const float2 h = w[dft16_slot(n2)];
+    float2 a; a.x = scaled<SCALED>((float)rows[n], scale); a.y = h.x;
+    dst_a[n] = a;
+    if (has_b) { float2 b; b.x = scaled<SCALED>((float)rows[N + n], scale); b.y = h.y; dst_b[n] = b; }
+  }
+}
+
 // ------------------------ N = 8192, 256 threads: 32 values per thread
 //
 // Four-step 8192 = 64 x 128: n = n1 + 64 m, k = k2 + 128 k1,
@@ -1142,6 +1291,18 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
                        : pick4(analytic_r32_kernel<In, false, false, false>, analytic_r32_kernel<In, false, true, false>,
                                analytic_r32_kernel<In, true, false, false>, analytic_r32_kernel<In, true, true, false>,
                                scale, support);
+#ifndef TIDAS_K1_NO_T16
+        if constexpr (sizeof(In) <= 4) {
+          if (bulk && !support) {  // 16 x 16 x 16 three-pass kernel (no support-scan variant)
+            auto kt = scale != 1.0 ? analytic_t16_kernel<In, true> : analytic_t16_kernel<In, false>;
+            const size_t dyn16 = sizeof(float2) * T16_ELEMS + 2 * 4096 * sizeof(In);
+            TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn16));
+            TIDAS_CUDA_CHECK(launch_pdl(kt, dim3((unsigned)((n_rows + 1) / 2)), dim3(256), dyn16, st, rf, stride,
+                                        (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, lo, hi, early));
+            return TIDAS_OK;
+          }
+        }
+#endif
         const size_t dyn = bulk ? 2 * 4096 * sizeof(In) : 0;
         if (bulk) TIDAS_CUDA_CHECK(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         TIDAS_CUDA_CHECK(launch_pdl(k4, dim3((unsigned)((n_rows + 1) / 2)), dim3(128), dyn, st,
