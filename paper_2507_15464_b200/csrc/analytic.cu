@@ -519,8 +519,8 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
 // ------------------------ N = 4096 as 16 x 16 x 16, 256 threads: 16 values per thread
 //
 // n = n0 + 16 n1 + 256 n2, k = k0 + 16 k1 + 256 k2:
-//   A[n0, n1, k0] = DFT16_n2(x) W256^(n1 k0)
-//   B[n0, k1, k0] = DFT16_n1(A) W4096^(n0 (k0 + 16 k1))
+//   A[n0, n1, k0] = DFT16_n2(x) W4096^((n0 + 16 n1) k0)
+//   B[n0, k1, k0] = DFT16_n1(A) W256^(n0 k1)
 //   X[k0 + 16 k1 + 256 k2] = DFT16_n0(B)
 // Thread t = 16 n1 + n0 owns x[t + 256 n2]; after the three passes thread
 // t = 16 k1 + k0 owns X[t + 256 k2]. The inverse is the SAME routine with
@@ -535,72 +535,36 @@ __global__ void __launch_bounds__(128, 4) analytic_r32_kernel(const In* __restri
 constexpr int T16_LP = 17;
 constexpr int T16_ELEMS = 256 * T16_LP;
 
-// v[slot(r)] *= base * w^r, r = 0..15 (r = 0: base only when BASE); dft16 leaves
-// X[r] in slot dft16_slot(r). Powers by products of depth <= 3 past w / base.
-template <bool BASE> __device__ __forceinline__ void t16_twiddle(float2 base, float2 w, float2 (&v)[16]) {
+// v[slot(r)] *= w^r for one block of four outputs r = 4 a .. 4 a + 3 (base = w^(4a))
+template <typename SLOT>
+__device__ __forceinline__ void tw_block4(float2 base, float2 w, float2 w2, float2 w3, float2* v, int a, SLOT slot) {
+  v[slot(4 * a)] = cmul(v[slot(4 * a)], base);
+  v[slot(4 * a + 1)] = cmul(v[slot(4 * a + 1)], cmul(base, w));
+  v[slot(4 * a + 2)] = cmul(v[slot(4 * a + 2)], cmul(base, w2));
+  v[slot(4 * a + 3)] = cmul(v[slot(4 * a + 3)], cmul(base, w3));
+}
+
+// v[slot(r)] *= w^r, r = 1..15; dft16 leaves X[r] in slot dft16_slot(r).
+// Powers by products of depth <= 3 past w.
+__device__ __forceinline__ void t16_twiddle(float2 w, float2 (&v)[16]) {
   const float2 w2 = cmul(w, w), w3 = cmul(w2, w), w4 = cmul(w2, w2), w8 = cmul(w4, w4);
-  float2 b0 = base, b4 = BASE ? cmul(base, w4) : w4, b8 = BASE ? cmul(base, w8) : w8;
-  const float2 b12 = cmul(b8, w4);
-  if (BASE) v[dft16_slot(0)] = cmul(v[dft16_slot(0)], b0);
-  v[dft16_slot(1)] = cmul(v[dft16_slot(1)], BASE ? cmul(b0, w) : w);
-  v[dft16_slot(2)] = cmul(v[dft16_slot(2)], BASE ? cmul(b0, w2) : w2);
-  v[dft16_slot(3)] = cmul(v[dft16_slot(3)], BASE ? cmul(b0, w3) : w3);
-  v[dft16_slot(4)] = cmul(v[dft16_slot(4)], b4);
-  v[dft16_slot(5)] = cmul(v[dft16_slot(5)], cmul(b4, w));
-  v[dft16_slot(6)] = cmul(v[dft16_slot(6)], cmul(b4, w2));
-  v[dft16_slot(7)] = cmul(v[dft16_slot(7)], cmul(b4, w3));
-  v[dft16_slot(8)] = cmul(v[dft16_slot(8)], b8);
-  v[dft16_slot(9)] = cmul(v[dft16_slot(9)], cmul(b8, w));
-  v[dft16_slot(10)] = cmul(v[dft16_slot(10)], cmul(b8, w2));
-  v[dft16_slot(11)] = cmul(v[dft16_slot(11)], cmul(b8, w3));
-  v[dft16_slot(12)] = cmul(v[dft16_slot(12)], b12);
-  v[dft16_slot(13)] = cmul(v[dft16_slot(13)], cmul(b12, w));
-  v[dft16_slot(14)] = cmul(v[dft16_slot(14)], cmul(b12, w2));
-  v[dft16_slot(15)] = cmul(v[dft16_slot(15)], cmul(b12, w3));
+  auto slot = [](int r) { return dft16_slot(r); };
+  v[slot(1)] = cmul(v[slot(1)], w);
+  v[slot(2)] = cmul(v[slot(2)], w2);
+  v[slot(3)] = cmul(v[slot(3)], w3);
+  tw_block4(w4, w, w2, w3, v, 1, slot);
+  tw_block4(w8, w, w2, w3, v, 2, slot);
+  tw_block4(cmul(w8, w4), w, w2, w3, v, 3, slot);
 }
 
-// one 4096-point transform on the thread layout above; T1 = W256^(t >> 4),
-// Ta = W4096^((t & 15) (t >> 4)), Tb = W256^(t & 15) (forward sign; conjugated here for INV)
-template <bool INV>
-__device__ __forceinline__ void t16_fft4096(float2 (&v)[16], float2* S, int t, float2 T1, float2 Ta, float2 Tb) {
-  const int lo = t & 15, hi = t >> 4;
-  if (INV) { T1.y = -T1.y; Ta.y = -Ta.y; Tb.y = -Tb.y; }
-  dft16<INV, float>(v);                    // over n2 -> k0 in slot dft16_slot(k0)
-  t16_twiddle<false>(T1, T1, v);           // W256^(n1 k0)
-  __syncthreads();                         // the previous transform's readers are done with S
-#pragma unroll
-  for (int r = 0; r < 16; ++r) S[(16 * r + lo) * T16_LP + hi] = v[dft16_slot(r)];   // [k0][n0][n1]
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = S[t * T16_LP + r];                            // thread (k0, n0): over n1
-  dft16<INV, float>(v);                    // over n1 -> k1
-  t16_twiddle<true>(Ta, Tb, v);            // W4096^(n0 k0) W256^(n0 k1)
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < 16; ++r) S[(16 * r + hi) * T16_LP + lo] = v[dft16_slot(r)];   // [k1][k0][n0]
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = S[t * T16_LP + r];                            // thread (k1, k0): over n0
-  dft16<INV, float>(v);                    // over n0 -> k2 in slot dft16_slot(k2)
-}
-
-template <typename In, bool SCALED>
-__global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restrict__ rf, int64_t stride, float scale,
-                                                            cplx<float>* __restrict__ out, int64_t n_rows,
-                                                            int s_lo, int s_hi, int early) {
-  constexpr int N = 4096;
-  constexpr int SH = TW_LOG - 12;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* S = reinterpret_cast<float2*>(smem_raw);                       // [256][17]
-  In* rows = reinterpret_cast<In*>(smem_raw + sizeof(float2) * T16_ELEMS);  // [2][N]
-  __shared__ __align__(8) uint64_t rows_bar;
-  const int t = threadIdx.x;
-  const int64_t ra = 2 * (int64_t)blockIdx.x;
-  const bool has_b = ra + 1 < n_rows;
-  const In* src_a = rf + ra * stride;
-  const In* src_b = rf + (ra + 1) * stride;
-  const unsigned bar = (unsigned)__cvta_generic_to_shared(&rows_bar);
-  if (t == 0) {
+// Two rows of N samples land in shared memory by bulk async copies on an
+// mbarrier (thread 0 issues, everyone waits): rows_begin before the twiddle
+// loads, rows_wait after a __syncthreads.
+template <typename In>
+__device__ __forceinline__ unsigned rows_begin(In* rows, uint64_t* rows_bar, const In* src_a, const In* src_b, bool has_b,
+                                               int N, int early) {
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(rows_bar);
+  if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(bar));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -608,7 +572,7 @@ __global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restri
   // wait for the kernel ahead from here to just before the stores
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (!early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     const unsigned bytes = (unsigned)(N * sizeof(In));
     uint64_t pol;  // RF rows are read once: evict-first in L2
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
@@ -623,14 +587,59 @@ __global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restri
           ::"r"((unsigned)__cvta_generic_to_shared(rows + N)), "l"(src_b), "r"(bytes), "r"(bar), "l"(pol)
           : "memory");
   }
-  // per-thread table twiddles, loaded while the rows are in flight
-  const int lo = t & 15, hi = t >> 4;
-  const float2 T1 = g_tw32[(16 * hi) << SH], Ta = g_tw32[(lo * hi) << SH], Tb = g_tw32[(16 * lo) << SH];
-  __syncthreads();  // the barrier is initialised before anyone waits on it
+  return bar;
+}
+__device__ __forceinline__ void rows_wait(unsigned bar) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], 0, 1000000;\n"
       " @!p bra W_%=;\n}\n" ::"r"(bar) : "memory");
+}
+
+// one 4096-point transform on the thread layout above; Tw = W4096^t (the pass-1
+// twiddle W256^(n1 k0) and the k0 part W4096^(n0 k0) of the pass-2 twiddle are
+// both functions of the pass-1 thread (n0, n1) and slot k0: one factor Tw^k0),
+// Tb = W256^(t & 15) (forward sign; conjugated here for INV)
+template <bool INV>
+__device__ __forceinline__ void t16_fft4096(float2 (&v)[16], float2* S, int t, float2 Tw, float2 Tb) {
+  const int lo = t & 15, hi = t >> 4;
+  if (INV) { Tw.y = -Tw.y; Tb.y = -Tb.y; }
+  dft16<INV, float>(v);                    // over n2 -> k0 in slot dft16_slot(k0)
+  t16_twiddle(Tw, v);                  // W4096^((n0 + 16 n1) k0)
+  __syncthreads();                         // the previous transform's readers are done with S
+#pragma unroll
+  for (int r = 0; r < 16; ++r) S[(16 * r + lo) * T16_LP + hi] = v[dft16_slot(r)];   // [k0][n0][n1]
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = S[t * T16_LP + r];                            // thread (k0, n0): over n1
+  dft16<INV, float>(v);                    // over n1 -> k1
+  t16_twiddle(Tb, v);                  // W256^(n0 k1)
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) S[(16 * r + hi) * T16_LP + lo] = v[dft16_slot(r)];   // [k1][k0][n0]
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = S[t * T16_LP + r];                            // thread (k1, k0): over n0
+  dft16<INV, float>(v);                    // over n0 -> k2 in slot dft16_slot(k2)
+}
+
+template <typename In, bool SCALED>
+__global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restrict__ rf, int64_t stride, float scale,
+                                                            cplx<float>* __restrict__ out, int64_t n_rows,
+                                                            int s_lo, int s_hi, int early) {
+  constexpr int N = 4096;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* S = reinterpret_cast<float2*>(smem_raw);                       // [256][17]
+  In* rows = reinterpret_cast<In*>(smem_raw + sizeof(float2) * T16_ELEMS);  // [2][N]
+  __shared__ __align__(8) uint64_t rows_bar;
+  const int t = threadIdx.x;
+  const int64_t ra = 2 * (int64_t)blockIdx.x;
+  const bool has_b = ra + 1 < n_rows;
+  const unsigned bar = rows_begin(rows, &rows_bar, rf + ra * stride, rf + (ra + 1) * stride, has_b, N, early);
+  // per-thread table twiddles, loaded while the rows are in flight
+  const float2 Tw = g_tw32[t << (TW_LOG - 12)], Tb = g_tw32[(t & 15) << (TW_LOG - 8)];
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  rows_wait(bar);
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
@@ -639,7 +648,7 @@ __global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restri
     v[r].y = has_b ? (float)rows[N + n] : 0.0f;
     if (SCALED) { v[r].x *= scale; v[r].y *= scale; }
   }
-  t16_fft4096<false>(v, S, t, T1, Ta, Tb);  // slot dft16_slot(k2): X[t + 256 k2]
+  t16_fft4096<false>(v, S, t, Tw, Tb);  // slot dft16_slot(k2): X[t + 256 k2]
   // Hilbert multiplier -i sgn(k) / N: k2 < 8 positive, k2 >= 8 negative frequencies; DC and Nyquist zero
   const float invN = 1.0f / (float)N;
   float2 w[16];
@@ -649,7 +658,7 @@ __global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restri
     w[k2] = k2 < 8 ? make_float2(x.y * invN, -x.x * invN) : make_float2(-x.y * invN, x.x * invN);
   }
   if (t == 0) { w[0] = make_float2(0.0f, 0.0f); w[8] = make_float2(0.0f, 0.0f); }
-  t16_fft4096<true>(w, S, t, T1, Ta, Tb);   // slot dft16_slot(n2): H[t + 256 n2] (a in .x, b in .y)
+  t16_fft4096<true>(w, S, t, Tw, Tb);   // slot dft16_slot(n2): H[t + 256 n2] (a in .x, b in .y)
   if (early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the output rows may still be read
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
@@ -659,6 +668,143 @@ __global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restri
     const int n = t + 256 * n2;
     if ((unsigned)(n - s_lo) > span) continue;
     const float2 h = w[dft16_slot(n2)];
+    float2 a; a.x = scaled<SCALED>((float)rows[n], scale); a.y = h.x;
+    dst_a[n] = a;
+    if (has_b) { float2 b; b.x = scaled<SCALED>((float)rows[N + n], scale); b.y = h.y; dst_b[n] = b; }
+  }
+}
+
+// ------------------------ N = 8192 as 32 x 16 x 16, 256 threads: 32 values per thread
+//
+// The same three passes with a 32-point first pass: n = n0 + 16 n1 + 256 n2
+// (n2 < 32), k = k0 + 32 k1 + 512 k2 (k0 < 32):
+//   A[n0, n1, k0] = DFT32_n2(x) W8192^((n0 + 16 n1) k0)
+//   B[n0, k1, k0] = DFT16_n1(A) W256^(n0 k1)
+//   X[k0 + 32 k1 + 512 k2] = DFT16_n0(B)
+// Thread t = 16 n1 + n0 owns x[t + 256 m], m < 32. Passes 2 and 3 have 512
+// (k0, n0) / (k1, k0) columns: thread t takes columns t and t + 256 of the
+// [column][17] transposes, i.e. pass 2 (k0 = (t >> 4) + 16 c, n0 = t & 15) and
+// pass 3 (k1 = (t >> 5) + 8 c, k0 = t & 31), and ends owning X[t + 256 m] with
+// m = c + 2 k2 in slot 16 c + dft16_slot(k2) — the input layout again, so the
+// inverse is the same routine with conjugate twiddles.
+constexpr int T32_ELEMS = 512 * T16_LP;
+__host__ __device__ constexpr int t32_slot(int m) { return 16 * (m & 1) + dft16_slot(m >> 1); }
+
+template <bool INV>
+__device__ __forceinline__ void t32_fft8192(float2 (&v)[32], float2* S, int t, float2 Tw, float2 Tb) {
+  const int lo = t & 15, hi = t >> 4;
+  if (INV) { Tw.y = -Tw.y; Tb.y = -Tb.y; }
+  dft32<INV>(v);                           // over n2 -> k0 in slot sig32_inv(k0)
+  {                                        // W8192^(t k0), k0 = 1..31
+    const float2 w2 = cmul(Tw, Tw), w3 = cmul(w2, Tw), w4 = cmul(w2, w2), w8 = cmul(w4, w4), w16 = cmul(w8, w8);
+    auto slot = [](int r) { return sig32_inv(r); };
+    v[slot(1)] = cmul(v[slot(1)], Tw);
+    v[slot(2)] = cmul(v[slot(2)], w2);
+    v[slot(3)] = cmul(v[slot(3)], w3);
+    tw_block4(w4, Tw, w2, w3, v, 1, slot);
+    tw_block4(w8, Tw, w2, w3, v, 2, slot);
+    tw_block4(cmul(w8, w4), Tw, w2, w3, v, 3, slot);
+    tw_block4(w16, Tw, w2, w3, v, 4, slot);
+    tw_block4(cmul(w16, w4), Tw, w2, w3, v, 5, slot);
+    const float2 w24 = cmul(w16, w8);
+    tw_block4(w24, Tw, w2, w3, v, 6, slot);
+    tw_block4(cmul(w24, w4), Tw, w2, w3, v, 7, slot);
+  }
+  __syncthreads();                         // the previous transform's readers are done with S
+#pragma unroll
+  for (int r = 0; r < 32; ++r) S[(16 * r + lo) * T16_LP + hi] = v[sig32_inv(r)];     // [k0][n0][n1]
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[16 * c + r] = S[(t + 256 * c) * T16_LP + r];     // columns (k0, n0): over n1
+  dft16<INV, float>(v);                    // over n1 -> k1
+  dft16<INV, float>(v + 16);
+  {                                        // W256^(n0 k1) on both columns
+    const float2 w2 = cmul(Tb, Tb), w3 = cmul(w2, Tb), w4 = cmul(w2, w2), w8 = cmul(w4, w4), w12 = cmul(w8, w4);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float2* u = v + 16 * c;
+      auto slot = [](int r) { return dft16_slot(r); };
+      u[slot(1)] = cmul(u[slot(1)], Tb);
+      u[slot(2)] = cmul(u[slot(2)], w2);
+      u[slot(3)] = cmul(u[slot(3)], w3);
+    }
+    float2 p[3][3];                        // w^(4a + b), a, b = 1..3: shared by the two columns
+    const float2 base[3] = {w4, w8, w12}, wb[3] = {Tb, w2, w3};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) p[a][b] = cmul(base[a], wb[b]);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float2* u = v + 16 * c;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        u[dft16_slot(4 * a + 4)] = cmul(u[dft16_slot(4 * a + 4)], base[a]);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) u[dft16_slot(4 * a + 5 + b)] = cmul(u[dft16_slot(4 * a + 5 + b)], p[a][b]);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int r = 0; r < 16; ++r) S[(32 * r + hi + 16 * c) * T16_LP + lo] = v[16 * c + dft16_slot(r)];  // [k1][k0][n0]
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[16 * c + r] = S[(t + 256 * c) * T16_LP + r];     // columns (k1, k0): over n0
+  dft16<INV, float>(v);                    // over n0 -> k2: X[t + 256 (c + 2 k2)] in slot 16 c + dft16_slot(k2)
+  dft16<INV, float>(v + 16);
+}
+
+template <typename In, bool SCALED>
+__global__ void __launch_bounds__(256, 2) analytic_t32_kernel(const In* __restrict__ rf, int64_t stride, float scale,
+                                                            cplx<float>* __restrict__ out, int64_t n_rows,
+                                                            int s_lo, int s_hi, int early) {
+  constexpr int N = 8192;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* S = reinterpret_cast<float2*>(smem_raw);                       // [512][17]
+  In* rows = reinterpret_cast<In*>(smem_raw + sizeof(float2) * T32_ELEMS);  // [2][N]
+  __shared__ __align__(8) uint64_t rows_bar;
+  const int t = threadIdx.x;
+  const int64_t ra = 2 * (int64_t)blockIdx.x;
+  const bool has_b = ra + 1 < n_rows;
+  const unsigned bar = rows_begin(rows, &rows_bar, rf + ra * stride, rf + (ra + 1) * stride, has_b, N, early);
+  const float2 Tw = g_tw32[t << (TW_LOG - 13)], Tb = g_tw32[(t & 15) << (TW_LOG - 8)];
+  __syncthreads();
+  rows_wait(bar);
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int n = t + 256 * m;
+    v[m].x = (float)rows[n];
+    v[m].y = has_b ? (float)rows[N + n] : 0.0f;
+    if (SCALED) { v[m].x *= scale; v[m].y *= scale; }
+  }
+  t32_fft8192<false>(v, S, t, Tw, Tb);  // slot t32_slot(m): X[t + 256 m]
+  // Hilbert multiplier -i sgn(k) / N: m < 16 positive, m >= 16 negative frequencies; DC and Nyquist zero
+  const float invN = 1.0f / (float)N;
+  float2 w[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const float2 x = v[t32_slot(m)];
+    w[m] = m < 16 ? make_float2(x.y * invN, -x.x * invN) : make_float2(-x.y * invN, x.x * invN);
+  }
+  if (t == 0) { w[0] = make_float2(0.0f, 0.0f); w[16] = make_float2(0.0f, 0.0f); }
+  t32_fft8192<true>(w, S, t, Tw, Tb);   // slot t32_slot(m): H[t + 256 m] (a in .x, b in .y)
+  if (early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the output rows may still be read
+  cplx<float>* dst_a = out + ra * (int64_t)N;
+  cplx<float>* dst_b = dst_a + N;
+  const unsigned span = (unsigned)(s_hi - s_lo);
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int n = t + 256 * m;
+    if ((unsigned)(n - s_lo) > span) continue;
+    const float2 h = w[t32_slot(m)];
     float2 a; a.x = scaled<SCALED>((float)rows[n], scale); a.y = h.x;
     dst_a[n] = a;
     if (has_b) { float2 b; b.x = scaled<SCALED>((float)rows[N + n], scale); b.y = h.y; dst_b[n] = b; }
@@ -1273,6 +1419,19 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
         return TIDAS_OK;
       }
       if (!delay && logN == 13) {
+#ifndef TIDAS_K1_NO_T16
+        if constexpr (sizeof(In) == 2) {  // int16 rows (cfg5): 32 x 16 x 16 three-pass kernel, two CTAs / SM
+          const bool bulk = (reinterpret_cast<uintptr_t>(rf) & 15) == 0 && ((stride * (int64_t)sizeof(In)) & 15) == 0;
+          if (bulk && !support) {
+            auto kt = scale != 1.0 ? analytic_t32_kernel<In, true> : analytic_t32_kernel<In, false>;
+            const size_t dyn32 = sizeof(float2) * T32_ELEMS + 2 * 8192 * sizeof(In);
+            TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn32));
+            TIDAS_CUDA_CHECK(launch_pdl(kt, dim3((unsigned)((n_rows + 1) / 2)), dim3(256), dyn32, st, rf, stride,
+                                        (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, lo, hi, early));
+            return TIDAS_OK;
+          }
+        }
+#endif
         auto kr = pick4(analytic_r8192_kernel<In, false, false>, analytic_r8192_kernel<In, false, true>,
                         analytic_r8192_kernel<In, true, false>, analytic_r8192_kernel<In, true, true>, scale, support);
         const size_t smem8 = sizeof(float2) * 128 * 65;
