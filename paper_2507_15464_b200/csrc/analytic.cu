@@ -623,32 +623,79 @@ __device__ __forceinline__ void t16_fft4096(float2 (&v)[16], float2* S, int t, f
   dft16<INV, float>(v);                    // over n0 -> k2 in slot dft16_slot(k2)
 }
 
-template <typename In, bool SCALED>
-__global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restrict__ rf, int64_t stride, float scale,
+// N = 2048 as 16 x 8 x 16 on 128 threads, same thread layout (t = n0 + 16 n1 owns
+// x[t + 128 n2]): n = n0 + 16 n1 + 128 n2 (n1 < 8), k = k0 + 16 k1 + 128 k2 (k1 < 8),
+//   A[n0, n1, k0] = DFT16_n2(x) W2048^((n0 + 16 n1) k0)
+//   B[n0, k1, k0] = DFT8_n1(A) W128^(n0 k1)
+//   X[k0 + 16 k1 + 128 k2] = DFT16_n0(B)
+// The middle pass has 256 (k0, n0) columns of 8: thread t takes columns t and
+// t + 128 of a [256][9] transpose; the last is [128][17] as above.
+constexpr int T8_LP = 9;
+constexpr int T8_ELEMS = 256 * T8_LP;  // >= 128 * T16_LP
+
+template <bool INV>
+__device__ __forceinline__ void t8_fft2048(float2 (&v)[16], float2* S, int t, float2 Tw, float2 Tb) {
+  const int lo = t & 15, hi = t >> 4;
+  if (INV) { Tw.y = -Tw.y; Tb.y = -Tb.y; }
+  dft16<INV, float>(v);                    // over n2 -> k0 in slot dft16_slot(k0)
+  t16_twiddle(Tw, v);                      // W2048^((n0 + 16 n1) k0)
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) S[(16 * r + lo) * T8_LP + hi] = v[dft16_slot(r)];    // [k0][n0][n1]
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[8 * c + r] = S[(t + 128 * c) * T8_LP + r];        // columns (k0 = hi + 8 c, n0): over n1
+  dft8<INV, float>(v);                     // over n1 -> k1 (natural order)
+  dft8<INV, float>(v + 8);
+  {                                        // W128^(n0 k1), k1 = 1..7, on both columns
+    const float2 w2 = cmul(Tb, Tb), w3 = cmul(w2, Tb), w4 = cmul(w2, w2);
+    const float2 p[7] = {Tb, w2, w3, w4, cmul(w4, Tb), cmul(w4, w2), cmul(w4, w3)};
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int r = 1; r < 8; ++r) v[8 * c + r] = cmul(v[8 * c + r], p[r - 1]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) S[(16 * r + hi + 8 * c) * T16_LP + lo] = v[8 * c + r];  // [k1][k0][n0]
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = S[t * T16_LP + r];                            // thread (k1, k0): over n0
+  dft16<INV, float>(v);                    // over n0 -> k2 in slot dft16_slot(k2)
+}
+
+template <typename In, bool SCALED, int N>
+__global__ void __launch_bounds__(N / 16, N == 4096 ? 3 : 4) analytic_t16_kernel(const In* __restrict__ rf, int64_t stride, float scale,
                                                             cplx<float>* __restrict__ out, int64_t n_rows,
                                                             int s_lo, int s_hi, int early) {
-  constexpr int N = 4096;
+  constexpr int NT = N / 16, LOGN = N == 4096 ? 12 : 11;
+  static_assert(N == 4096 || N == 2048, "three-pass kernel lengths");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* S = reinterpret_cast<float2*>(smem_raw);                       // [256][17]
-  In* rows = reinterpret_cast<In*>(smem_raw + sizeof(float2) * T16_ELEMS);  // [2][N]
+  float2* S = reinterpret_cast<float2*>(smem_raw);                       // [256][17] / [256][9]
+  In* rows = reinterpret_cast<In*>(smem_raw + sizeof(float2) * (N == 4096 ? T16_ELEMS : T8_ELEMS));  // [2][N]
   __shared__ __align__(8) uint64_t rows_bar;
   const int t = threadIdx.x;
   const int64_t ra = 2 * (int64_t)blockIdx.x;
   const bool has_b = ra + 1 < n_rows;
   const unsigned bar = rows_begin(rows, &rows_bar, rf + ra * stride, rf + (ra + 1) * stride, has_b, N, early);
   // per-thread table twiddles, loaded while the rows are in flight
-  const float2 Tw = g_tw32[t << (TW_LOG - 12)], Tb = g_tw32[(t & 15) << (TW_LOG - 8)];
+  const float2 Tw = g_tw32[t << (TW_LOG - LOGN)], Tb = g_tw32[(t & 15) << (TW_LOG - LOGN + 4)];
   __syncthreads();  // the barrier is initialised before anyone waits on it
   rows_wait(bar);
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const int n = t + 256 * r;
+    const int n = t + NT * r;
     v[r].x = (float)rows[n];
     v[r].y = has_b ? (float)rows[N + n] : 0.0f;
     if (SCALED) { v[r].x *= scale; v[r].y *= scale; }
   }
-  t16_fft4096<false>(v, S, t, Tw, Tb);  // slot dft16_slot(k2): X[t + 256 k2]
+  if constexpr (N == 4096) t16_fft4096<false>(v, S, t, Tw, Tb);  // slot dft16_slot(k2): X[t + NT k2]
+  else t8_fft2048<false>(v, S, t, Tw, Tb);
   // Hilbert multiplier -i sgn(k) / N: k2 < 8 positive, k2 >= 8 negative frequencies; DC and Nyquist zero
   const float invN = 1.0f / (float)N;
   float2 w[16];
@@ -658,14 +705,15 @@ __global__ void __launch_bounds__(256, 3) analytic_t16_kernel(const In* __restri
     w[k2] = k2 < 8 ? make_float2(x.y * invN, -x.x * invN) : make_float2(-x.y * invN, x.x * invN);
   }
   if (t == 0) { w[0] = make_float2(0.0f, 0.0f); w[8] = make_float2(0.0f, 0.0f); }
-  t16_fft4096<true>(w, S, t, Tw, Tb);   // slot dft16_slot(n2): H[t + 256 n2] (a in .x, b in .y)
+  if constexpr (N == 4096) t16_fft4096<true>(w, S, t, Tw, Tb);   // slot dft16_slot(n2): H[t + NT n2] (a in .x, b in .y)
+  else t8_fft2048<true>(w, S, t, Tw, Tb);
   if (early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the output rows may still be read
   cplx<float>* dst_a = out + ra * (int64_t)N;
   cplx<float>* dst_b = dst_a + N;
   const unsigned span = (unsigned)(s_hi - s_lo);
 #pragma unroll
   for (int n2 = 0; n2 < 16; ++n2) {
-    const int n = t + 256 * n2;
+    const int n = t + NT * n2;
     if ((unsigned)(n - s_lo) > span) continue;
     const float2 h = w[dft16_slot(n2)];
     float2 a; a.x = scaled<SCALED>((float)rows[n], scale); a.y = h.x;
@@ -1412,6 +1460,17 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
       // four-step FFTs in registers (analytic_r2048_kernel / analytic_r32_kernel /
       // analytic_r8192_kernel); other lengths take the shared-memory Stockham kernel
       if (!delay && logN == 11) {
+#ifndef TIDAS_K1_NO_T16
+        if ((reinterpret_cast<uintptr_t>(rf) & 15) == 0 && ((stride * (int64_t)sizeof(In)) & 15) == 0 && !support) {
+          // 16 x 8 x 16 three-pass kernel on bulk-copied rows (16-byte aligned; f64 / f32 / int16)
+          auto kt = scale != 1.0 ? analytic_t16_kernel<In, true, 2048> : analytic_t16_kernel<In, false, 2048>;
+          const size_t dyn8 = sizeof(float2) * T8_ELEMS + 2 * 2048 * sizeof(In);
+          TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn8));
+          TIDAS_CUDA_CHECK(launch_pdl(kt, dim3((unsigned)((n_rows + 1) / 2)), dim3(128), dyn8, st, rf, stride,
+                                      (float)scale, reinterpret_cast<cplx<float>*>(out), n_rows, lo, hi, early));
+          return TIDAS_OK;
+        }
+#endif
         auto k2 = pick4(analytic_r2048_kernel<In, false, false>, analytic_r2048_kernel<In, false, true>,
                         analytic_r2048_kernel<In, true, false>, analytic_r2048_kernel<In, true, true>, scale, support);
         TIDAS_CUDA_CHECK(launch_pdl(k2, dim3((unsigned)((n_rows + 1) / 2)), dim3(64), 0, st,
@@ -1453,7 +1512,7 @@ static int launch_analytic(const In* rf, int64_t stride, double scale, void* out
 #ifndef TIDAS_K1_NO_T16
         if constexpr (sizeof(In) <= 4) {
           if (bulk && !support) {  // 16 x 16 x 16 three-pass kernel (no support-scan variant)
-            auto kt = scale != 1.0 ? analytic_t16_kernel<In, true> : analytic_t16_kernel<In, false>;
+            auto kt = scale != 1.0 ? analytic_t16_kernel<In, true, 4096> : analytic_t16_kernel<In, false, 4096>;
             const size_t dyn16 = sizeof(float2) * T16_ELEMS + 2 * 4096 * sizeof(In);
             TIDAS_CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn16));
             TIDAS_CUDA_CHECK(launch_pdl(kt, dim3((unsigned)((n_rows + 1) / 2)), dim3(256), dyn16, st, rf, stride,
