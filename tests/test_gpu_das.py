@@ -73,7 +73,7 @@ def test_analytic_support_scan():
 
 @pytest.mark.parametrize("dtype", [np.float32, np.int16, np.float64])
 def test_analytic_4096_fused_odd_rows_and_support(dtype, rng):
-    """FP32 N = 4096 runs the four-step register kernel: odd row count (last CTA has
+    """FP32 N = 4096 runs the three-pass register kernel: odd row count (last CTA has
     one channel), zero rows and head/tail zeros for the support scan."""
     x = (rng.standard_normal((7, 4096)) * (1000 if dtype == np.int16 else 1)).astype(dtype)
     x[2] = 0
@@ -109,9 +109,37 @@ def test_analytic_strided_rows_through_the_abi(n, pad, offset, rng):
 
 
 @pytest.mark.parametrize("n", [2048, 4096, 8192])
+@pytest.mark.parametrize("dtype", [torch.int16, torch.float32, torch.float64])
+def test_analytic_three_pass_unaligned_rows_bitwise(n, dtype):
+    """Rows that are not 16-byte aligned take plain loads instead of bulk copies
+    (analytic_tp_kernel BULK = false): same arithmetic, so the analytic rows, the
+    support scan and a ranged store must equal the aligned run bitwise."""
+    g = torch.Generator(device=DEV).manual_seed(n)
+    rows = 3
+    base = torch.randn(rows * n + 1, device=DEV, generator=g) * 500
+    base = base.round().to(dtype) if dtype == torch.int16 else base.to(dtype)
+    base[1 + n:1 + n + 37] = 0          # head zeros of row 1
+    shifted = base[1:].view(rows, n)     # element offset 1: 2 / 4 / 8 bytes past alignment
+    aligned = shifted.clone()
+    assert shifted.data_ptr() % 16 != 0 and aligned.data_ptr() % 16 == 0
+    sup_a = torch.empty((rows, 2), dtype=torch.int32, device=DEV)
+    sup_s = torch.empty((rows, 2), dtype=torch.int32, device=DEV)
+    a = tb.rf_analytic(aligned, "f32", scale=0.5, support=sup_a)
+    s_ = tb.rf_analytic(shifted, "f32", scale=0.5, support=sup_s)
+    assert torch.equal(a, s_) and torch.equal(sup_a, sup_s)
+    assert int(sup_a[1, 0]) == 37
+    lo, hi = n // 7, n // 2 + 5
+    out_a = torch.zeros((rows, n), dtype=torch.complex64, device=DEV)
+    out_s = torch.zeros((rows, n), dtype=torch.complex64, device=DEV)
+    tb.rf_analytic(aligned, "f32", out=out_a, sample_range=(lo, hi))
+    tb.rf_analytic(shifted, "f32", out=out_s, sample_range=(lo, hi))
+    assert torch.equal(out_a, out_s) and bool((out_a[:, :lo] == 0).all()) and bool((out_a[:, hi + 1:] == 0).all())
+
+
+@pytest.mark.parametrize("n", [2048, 4096, 8192])
 @pytest.mark.parametrize("rows", [1, 2, 3])
 def test_analytic_register_fft_scale_and_row_counts(n, rows, rng):
-    """The register four-step kernels (N = 2048 / 4096 / 8192) with one, two and
+    """The three-pass register kernels (N = 2048 / 4096 / 8192) with one, two and
     three rows (a lone last channel) and a non-unit ingest scale on int16."""
     x = (rng.standard_normal((rows, n)) * 1000).astype(np.int16)
     scale = 1e-3
