@@ -136,6 +136,40 @@ def test_analytic_three_pass_unaligned_rows_bitwise(n, dtype):
     assert torch.equal(out_a, out_s) and bool((out_a[:, :lo] == 0).all()) and bool((out_a[:, hi + 1:] == 0).all())
 
 
+@pytest.mark.parametrize("n,channels,dtype", [(2048, 64, torch.float64), (4096, 128, torch.float32),
+                                              (8192, 256, torch.int16)])
+def test_analytic_full_size_properties(n, channels, dtype):
+    """Size-independent properties of K1 on BASELINE-sized batches (cfg1 / cfg2 / cfg5
+    channel counts and trace lengths, 16 frames), no oracle needed: the real part is
+    the ingested sample exactly; the transform commutes with a circular shift of the
+    row (what lets K2 gather instead of shifting full traces); it is
+    linear; and for zero-mean rows with no Nyquist content H(H(x)) = -x."""
+    rows = 16 * channels
+    g = torch.Generator(device=DEV).manual_seed(n + channels)
+    x = torch.randn((rows, n), device=DEV, generator=g) * 300
+    x = x.round().to(dtype) if dtype == torch.int16 else x.to(dtype)
+    a = tb.rf_analytic(x, "f32")
+    assert a.shape == (rows, n) and a.dtype == torch.complex64
+    assert torch.equal(a.real, x.to(torch.float32))
+    peak = float(a.abs().max())
+    shift = n // 3 + 1
+    a_s = tb.rf_analytic(torch.roll(x, shift, dims=1).contiguous(), "f32")
+    assert float((a_s - torch.roll(a, shift, dims=1)).abs().max()) / peak < 2e-6
+    if dtype != torch.int16:  # linearity on the float ingests (an int16 sum could clip)
+        y = (torch.randn((rows, n), device=DEV, generator=g) * 300).to(dtype)
+        lin = tb.rf_analytic((2 * x - y).contiguous(), "f32")
+        assert float((lin - (2 * a - tb.rf_analytic(y, "f32"))).abs().max()) / peak < 4e-6
+    # H(H(x)) = -x once DC and Nyquist are removed (the one-sided mask zeroes both in H)
+    xf = x.to(torch.float32)
+    alt = torch.ones(n, device=DEV)
+    alt[1::2] = -1
+    xf = xf - xf.mean(dim=1, keepdim=True)
+    xf = xf - (xf * alt).mean(dim=1, keepdim=True) * alt
+    h = tb.rf_analytic(xf.contiguous(), "f32").imag.contiguous()
+    hh = tb.rf_analytic(h, "f32").imag
+    assert float((hh + xf).abs().max()) / float(xf.abs().max()) < 4e-6
+
+
 @pytest.mark.parametrize("n", [2048, 4096, 8192])
 @pytest.mark.parametrize("rows", [1, 2, 3])
 def test_analytic_register_fft_scale_and_row_counts(n, rows, rng):
