@@ -336,6 +336,43 @@ def test_cfg5_full_size_int16_frames_sampled_pixels():
     _subgrid_parity(cfg, q, torch.as_tensor(q).to(DEV), [0.0], "envelope")
 
 
+@pytest.mark.parametrize("cfg,frames,dtype", [(CFG2, 16, torch.float32), (CFG3, 2, torch.float32),
+                                              (CFG5, 4, torch.int16)], ids=["cfg2", "cfg3", "cfg5"])
+def test_das_full_size_properties(cfg, frames, dtype):
+    """Size-independent properties of K1 + K2 at the full BASELINE grids and trace
+    lengths (no oracle needed): the IQ image is linear in the RF; frames are
+    independent (a permuted batch gives the permuted images bitwise); coherent =
+    |IQ|; the envelope image is finite, non-negative, exactly homogeneous under a
+    power-of-two gain and, for one transmit, never below |IQ| (np.interp of two
+    magnitudes against the magnitude of the interpolated sum)."""
+    ang = cfg.get("angles", (0.0,))
+    x, z = grid(cfg)
+    kw = dict(n_el=cfg["n_el"], pitch=cfg["pitch"], fs=cfg["fs"], c=cfg["c"], n_samples=cfg["n_samples"],
+              x=x, z=z, angles=ang, f_number=cfg["f_number"])
+    g = torch.Generator(device=DEV).manual_seed(len(ang) * 1000 + frames)
+    shape = (frames, len(ang), cfg["n_el"], cfg["n_samples"])
+    a = (torch.randn(shape, device=DEV, generator=g) * 200).round()
+    b = (torch.randn(shape, device=DEV, generator=g) * 200).round()
+    for t in (a, b):  # head / tail zeros, as an acquisition has them
+        t[..., :64] = 0
+        t[..., -64:] = 0
+    iq = tb.plane_wave_plan(out="iq", **kw)
+    ia, ib = tb.das_image(a.to(dtype), iq), tb.das_image(b.to(dtype), iq)
+    iab = tb.das_image((a - b).to(dtype), iq)   # |a - b| stays far inside int16
+    peak = float(ia.abs().max())
+    assert peak > 0 and float((iab - (ia - ib)).abs().max()) / peak < 2e-5
+    perm = torch.randperm(frames, device=DEV, generator=g)
+    assert torch.equal(tb.das_image(a[perm].to(dtype).contiguous(), iq), ia[perm])
+    coh = tb.das_image(a.to(dtype), tb.plane_wave_plan(out="coherent", **kw))
+    assert float((coh - ia.abs()).abs().max()) / peak < 2e-6
+    env_plan = tb.plane_wave_plan(out="envelope", **kw)
+    env = tb.das_image(a.to(dtype), env_plan)
+    assert bool((env >= 0).all()) and bool(torch.isfinite(env).all())
+    assert torch.equal(tb.das_image((4 * a).to(dtype), env_plan), 4 * env)   # exact: power-of-two gain
+    if len(ang) == 1:  # one transmit: np.interp of two magnitudes >= the magnitude of the interpolated IQ
+        assert bool((env >= ia.abs() * (1 - 1e-5) - 1e-6 * peak).all())
+
+
 def test_iq_output_and_ragged_grid():
     cfg = CFG2
     rf, _ = speckle_rf(cfg, seed=7, n_scat=200)
